@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark: 1080p frames/s of the per-frame temporal-consistency step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One process per GPU (torchrun for N > 1).  Streams are independent (SURVEY
+§8(e)): every rank runs its own 1080p stream, no collective on the data path
+(torch.distributed is used only for the timing barrier and the max over
+ranks) -> "scaling": "weak".
+
+A step = one stabilize_step of a 1920x1080 RGB stream: push the next
+(input, processed) pair, provide the two flows, fused warp/weights/blend (K1),
+150-iteration screened-Poisson solve (K2), commit.  The consistency params
+alternate per frame (k1 0.3/0.5 with k2 0.5/0.3, lambda 2.0/0.5), the
+"interactive local/global blend" of BASELINE config 2.
+
+`value` is device-timed with inputs resident in HBM; `e2e` is the same step
+through the C ABI from pinned host buffers (H2D of the pair + D2H of O_t inside
+the timed region).  `--impl reference` times the CPU restatement of the
+reference step (oracle/, all host threads) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, W = 1080, 1920
+METRIC = "1080p frames/s (flow+warp+blend), per stream and box aggregate at 1/2/4/8 GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--height", type=int, default=H)
+    ap.add_argument("--width", type=int, default=W)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def params_for(t):
+    from paper_2301_00750_b200.consistency import ConsistencyParams
+
+    if t % 2 == 0:
+        return ConsistencyParams(k1=0.3, k2=0.5, lam=2.0)
+    return ConsistencyParams(k1=0.5, k2=0.3, lam=0.5)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """CPU restatement of the reference step (oracle/, test infrastructure)
+    timed on the host cores: the reference arm.  Rank 0 only."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+
+    import oracle as orc
+    from paper_2301_00750_b200 import synthetic
+
+    orc.build()
+    cores = os.cpu_count() or 1
+    orc.set_threads(cores)
+    h, w = args.height, args.width
+    seq = synthetic.translating_sequence(frames=3, height=h, width=w, step=(2, 1), seed=0)
+    fp = orc.constant_flow(h, w, 2, 1, -1)
+    fn = orc.constant_flow(h, w, 2, 1, 1)
+    prm = orc.Params()
+    steps = max(1, min(args.steps, 20))
+    times = []
+    for i in range(max(0, min(args.warmup, 1)) + steps):
+        t0 = time.perf_counter()
+        orc.run_step(seq.inputs[0], seq.processed[0], seq.inputs[1], seq.processed[1],
+                     seq.inputs[2], seq.processed[2], seq.processed[0], fp, fn, prm)
+        dt = time.perf_counter() - t0
+        if i >= min(args.warmup, 1):
+            times.append(dt)
+        if sum(times) > 60.0:
+            break
+    sec = sum(times) / len(times)
+    fps = 1.0 / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(fps, 4), "unit": "frames/s",
+        "n_gpus": world, "steps": len(times), "warmup": min(args.warmup, 1),
+        "ms_per_step": round(sec * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{w}x{h} single-stream consistency step (default preset, "
+                               f"150 iterations, ConstantFlow(2,1) flows)",
+                   "flow": "constant (provider seam)"},
+        "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"{len(times)} full {w}x{h} steps of the C restatement "
+                                   f"(oracle/streamstab_oracle.c, OpenMP {cores} threads)"},
+        "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(h, w, budget_s=20.0):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    from paper_2301_00750_b200 import synthetic
+
+    orc.build()
+    cores = os.cpu_count() or 1
+    orc.set_threads(cores)
+    seq = synthetic.translating_sequence(frames=3, height=h, width=w, step=(2, 1), seed=0)
+    fp = orc.constant_flow(h, w, 2, 1, -1)
+    fn = orc.constant_flow(h, w, 2, 1, 1)
+    times = []
+    while not times or (sum(times) < budget_s and len(times) < 3):
+        t0 = time.perf_counter()
+        orc.run_step(seq.inputs[0], seq.processed[0], seq.inputs[1], seq.processed[1],
+                     seq.inputs[2], seq.processed[2], seq.processed[0], fp, fn, orc.Params())
+        times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    return {"value": round(1.0 / sec, 4), "unit": "frames/s", "cores": cores, "kind": "port",
+            "sample": f"{len(times)} full {w}x{h} consistency steps, C restatement "
+                      f"(oracle/streamstab_oracle.c) on {cores} host threads"}
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2301_00750_b200 as ss
+    from paper_2301_00750_b200 import _lib
+    from paper_2301_00750_b200.consistency import _run_step
+    from paper_2301_00750_b200.synthetic import DeviceSequence
+
+    h, w = args.height, args.width
+    L = _lib.lib()
+    seq = DeviceSequence(h, w, step=(2, 1), seed=rank)
+    flow = ss.ConstantFlow(2, 1)
+    state = ss.SessionState(params=params_for(0))
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    pos = 0
+
+    def push():
+        nonlocal pos
+        pos += 1
+        i, p = seq.frame(pos)
+        state.push_pair(pos, i, p)
+
+    push()
+    push()
+
+    def step():
+        push()
+        state.params = params_for(pos)
+        _run_step(state, flow, with_next=True, return_host=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region (inputs generated in HBM) -------------------
+    sampler = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    blend_ms, solve_ms = [], []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for k in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+        tm = state.last_timing
+        blend_ms.append(tm.warp_blend_ms)
+        solve_ms.append(tm.solve_ms)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * 1e3 / ms_per_step  # frames/s over all ranks (one stream each)
+
+    # ---- e2e through the C ABI from pinned host buffers --------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, L, state, seq, torch, dist)
+
+    # ---- roofline of the dominant kernel (solver pass) ---------------------
+    # stage times come from CUDA events on the session stream inside ss_step:
+    # warp_blend = K1 alone, solve = the solver passes back to back
+    n_pass = math.ceil(150 / 8)
+    med_solve = sorted(solve_ms)[len(solve_ms) // 2]
+    med_blend = sorted(blend_ms)[len(blend_ms) // 2]
+    per_pass_ms = med_solve / n_pass
+    flops_per_pass = 14.0 * h * w * 3 * 8  # algorithmic FP32 ops, no halo redundancy
+    fp32_peak = 148 * 128 * 1.965e9 / 1e12  # non-FMA FP32 op rate at max SM clock, TOP/s
+    achieved = flops_per_pass / (per_pass_ms * 1e-3) / 1e12
+    k1_bytes = 130.0 * h * w  # K1 algorithmic bytes per launch
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    k1_gbs = k1_bytes / (med_blend * 1e-3) / 1e9
+    roofline = {
+        "kernel": "k_sgd_blocked (solver pass = 8 SGD-momentum iterations)",
+        "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 2),
+        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": None,
+        "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1965 MHz non-FMA op rate "
+                       "(MEASURED_PEAKS.json has no FP32 entry)",
+        "launch_ms": round(per_pass_ms, 5),
+        "secondary": {
+            "kernel": "k_presolve (K1 fused warp+weights+blend)", "bound": "hbm",
+            "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(k1_gbs / hbm_peak, 4), "traffic": None, "launch_ms": round(med_blend, 5),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+    }
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(h, w)
+    launches_per_step = 2 + 1 + n_pass  # 2 flow fills, K1, solver passes
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{w}x{h} single stream per GPU, default preset with per-frame "
+                               "interactive k1/k2/lambda schedule, 150 solver iterations",
+                   "flow": "ConstantFlow(2,1) on device (provider seam; lite flow CNN not yet "
+                           "in the step)",
+                   "streams_per_gpu": 1, "l2": "flushed between timed steps (256 MiB write)",
+                   "stage_ms_median": {"warp_blend": round(med_blend, 4),
+                                       "solve": round(med_solve, 4)}},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, L, state, seq, torch, dist):
+    """The same step through the C ABI from pinned host memory."""
+    from paper_2301_00750_b200 import _lib
+    from paper_2301_00750_b200._dev import params_struct
+
+    h, w = args.height, args.width
+    n_host = 4
+    host_i, host_p = [], []
+    for k in range(n_host):
+        i, p = seq.frame(1000 + k)
+        host_i.append(i.cpu().pin_memory())
+        host_p.append(p.cpu().pin_memory())
+    out = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
+    sess = state.handle
+    pos = [int(L.ss_solved_through(sess)) + 2]
+
+    def step(k):
+        pos[0] += 1
+        _check(L.ss_push_pair(sess, pos[0], host_i[k % n_host].data_ptr(),
+                              host_p[k % n_host].data_ptr(), _lib.SS_F32, _lib.SS_HOST), L)
+        t = int(L.ss_solved_through(sess)) + 1
+        _check(L.ss_set_constant_flow(sess, 0, 2.0, 1.0, -1), L)
+        _check(L.ss_set_constant_flow(sess, 1, 2.0, 1.0, 1), L)
+        prm = params_struct(params_for(t))
+        it = ctypes.c_int(0)
+        _check(L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)), L)
+        _check(L.ss_output(sess, out.data_ptr(), _lib.SS_F32, _lib.SS_HOST), L)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        step(k)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    world = dist.get_world_size() if dist else 1
+    return {"value": round(world * args.steps / dt, 3), "unit": "frames/s",
+            "h2d_bytes_per_step": 2 * h * w * 3 * 4, "d2h_bytes_per_step": h * w * 3 * 4,
+            "path": "C ABI: ss_push_pair(host pinned f32) + ss_set_constant_flow x2 + ss_step "
+                    "+ ss_output(host)", "timer": "host wall clock around K steps, "
+                                                  "device synchronised at both ends"}
+
+
+def _check(rc, L):
+    if rc != 0:
+        raise RuntimeError(f"streamstab_b200 error {rc}: {L.ss_last_error().decode()}")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/*
+ * streamstab_b200.h -- C ABI of the B200-native per-frame temporal-consistency
+ * step (arXiv 2301.00750; reference package `streamstab`).
+ *
+ * The reference is pure Python/numpy and has no FFI; each entry point below
+ * replaces one reference function (cited file:line under
+ * /root/reference/pkg/src/streamstab/) and is what the reference's Python
+ * layer binds through ctypes.  Plain pointers and sizes
+ * only: no torch types.  All device work is ordered on the caller's
+ * cudaStream_t (passed as void*; NULL = legacy default stream) or, for
+ * sessions, on the session's stream.
+ *
+ * Layouts (reference boundary, imgio.py:33-46, :154-192):
+ *   frame  float32 (H, W, C) interleaved, C in {1, 3}
+ *   flow   float32 (H, W, 2) with u = horizontal, v = vertical, plus a
+ *          uint8 (H, W) validity map (1 = valid)
+ *   maps   float32 (H, W)  (weights, masks)
+ *
+ * Status codes map 1:1 onto the reference's exceptions:
+ *   SS_RESOLUTION_MISMATCH -> flow.ResolutionMismatch   (flow.py:23)
+ *   SS_VALUE_ERROR         -> ValueError
+ *   SS_SOLVER_DIVERGENCE   -> consistency.SolverDivergence(iteration)
+ */
+#ifndef STREAMSTAB_B200_H
+#define STREAMSTAB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SS_API __attribute__((visibility("default")))
+#else
+#define SS_API
+#endif
+
+enum ss_status {
+    SS_OK = 0,
+    SS_RESOLUTION_MISMATCH = 1,
+    SS_VALUE_ERROR = 2,
+    SS_SOLVER_DIVERGENCE = 3,
+    SS_CUDA_ERROR = 4,
+    SS_NO_MEMORY = 5,
+};
+
+enum ss_where { SS_HOST = 0, SS_DEVICE = 1 };
+enum ss_dtype { SS_F32 = 0, SS_U8 = 1 };
+
+/* ConsistencyParams (consistency.py:37-51), cast to float32 exactly where the
+ * reference casts with np.float32 (consistency.py:149, :207, :270-271). */
+typedef struct ss_params {
+    float k1, k2, alpha, lam, eta, kappa;
+    int32_t iterations;
+    int32_t flow_downscale;
+} ss_params;
+
+/* StepTiming (consistency.py:298-303) plus the fused pre-solve stage; device
+ * time measured with CUDA events on the session stream. */
+typedef struct ss_timing {
+    float flow_ms;
+    float warp_blend_ms;
+    float solve_ms;
+} ss_timing;
+
+/* ---- library ------------------------------------------------------------ */
+SS_API int ss_abi_version(void);
+SS_API const char *ss_status_string(int status);
+/* Last error text of the calling thread (empty string if none). */
+SS_API const char *ss_last_error(void);
+/* Select the CUDA device for the calling thread; checks it is sm_100. */
+SS_API int ss_init(int device);
+/* ConsistencyParams.validate (consistency.py:53-69). */
+SS_API int ss_params_validate(const ss_params *p);
+
+/* ---- stateless ops on device pointers (stream-ordered) ------------------ */
+/* backward_warp (flow.py:102-127).  mask may be NULL. */
+SS_API int ss_backward_warp(const float *img, int h, int w, int c, const float *uv,
+                     const uint8_t *valid, float *out, float *mask, void *stream);
+/* occlusion_mask (flow.py:130-153); bit-exact with the reference. */
+SS_API int ss_occlusion_mask(const float *fwd_uv, const uint8_t *fwd_valid, const float *bwd_uv,
+                      const uint8_t *bwd_valid, int h, int w, float *out, void *stream);
+/* warp_weight (consistency.py:133-154).  validity may be NULL. */
+SS_API int ss_warp_weight(const float *ref, const float *warped, int h, int w, int c, float alpha,
+                   float bound, const float *validity, float *out, void *stream);
+/* local_blend / input_blend (consistency.py:157-182). */
+SS_API int ss_local_blend(const float *cur, const float *prev, const float *next, const float *wp,
+                   const float *wn, int h, int w, int c, float *out, void *stream);
+/* adaptive_blend (consistency.py:190-195). */
+SS_API int ss_adaptive_blend(const float *global_img, const float *local_img, const float *wp, int h,
+                      int w, int c, float *out, void *stream);
+/* consistency_weight (consistency.py:198-208). */
+SS_API int ss_consistency_weight(const float *cur, const float *blended, int h, int w, int c,
+                          float alpha, float lam, float *out, void *stream);
+/* laplacian (consistency.py:211-227). */
+SS_API int ss_laplacian(const float *img, int h, int w, int c, float *out, void *stream);
+/* solve_screened_poisson (consistency.py:253-295).  init may equal target.
+ * Synchronises the stream to report divergence; on SS_SOLVER_DIVERGENCE
+ * *div_iter holds the 1-based iteration the reference would raise with. */
+SS_API int ss_solve_screened_poisson(const float *processed, const float *target, const float *wc,
+                              int h, int w, int c, const ss_params *p, const float *init,
+                              float *out, int *div_iter, void *stream);
+
+/* ---- sessions: SessionState + stabilize_step (consistency.py:306-413) ---- */
+typedef struct ss_session ss_session;
+
+/* One stream's device-resident state: the (t-1, t, t+1) ring of
+ * (input, processed) pairs, O_{t-1}, flows and solver buffers.  stream may be
+ * NULL (the session creates its own non-blocking stream). */
+SS_API int ss_session_create(int h, int w, int c_in, int c_proc, void *stream, ss_session **out);
+SS_API int ss_session_destroy(ss_session *s);
+SS_API int ss_session_reset(ss_session *s);
+/* SessionState.push_pair (consistency.py:321-340).  I has c_in channels, P
+ * has c_proc; dtype SS_U8 frames are normalised by 1/255 (imgio.py:132). */
+SS_API int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, int dtype,
+                 int where);
+/* Position the next step will solve (solved_through + 1) and the state. */
+SS_API int64_t ss_solved_through(const ss_session *s);
+SS_API int ss_pending(const ss_session *s, int64_t *t, int *has_prev, int *has_next);
+/* Provide the flows for the pending step t: which = 0 -> flow t->t-1,
+ * which = 1 -> flow t->t+1 (FlowProvider.flow_between, flow.py:353-358,
+ * called at consistency.py:380, :384).  valid may be NULL (all valid). */
+SS_API int ss_set_flow(ss_session *s, int which, const float *uv, const uint8_t *valid, int where);
+/* Fill a flow slot with ConstantFlow(u, v) (flow.py:406-425) on device. */
+SS_API int ss_set_constant_flow(ss_session *s, int which, double u, double v, int steps);
+/* _snippet checks only (consistency.py:342-353): SS_OK if a step with
+ * with_next could run now, else SS_VALUE_ERROR with the reference's message;
+ * *t receives the position that would be solved. */
+SS_API int ss_check_step(const ss_session *s, int with_next, int64_t *t);
+/* stabilize_step (with_next = 1) / stream_end_step (with_next = 0)
+ * (consistency.py:356-413).  On SS_SOLVER_DIVERGENCE the state is not
+ * advanced and *div_iter is set. */
+SS_API int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter);
+/* Copy O_{solved_through} (the last output, or P_1 after the first push). */
+SS_API int ss_output(const ss_session *s, void *dst, int dtype, int where);
+/* Device pointer of the current output (H, W, c_proc) float32; valid until
+ * the next ss_step / ss_push_pair. */
+SS_API const float *ss_output_device(const ss_session *s);
+SS_API int ss_last_timing(const ss_session *s, ss_timing *t);
+/* Copy the flows used by the last step (for feeding back into the
+ * reference's FloDirFlow / FlowProvider seam). */
+SS_API int ss_flows(const ss_session *s, int which, float *uv_dst, uint8_t *valid_dst, int where);
+SS_API void *ss_session_stream(const ss_session *s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STREAMSTAB_B200_H */

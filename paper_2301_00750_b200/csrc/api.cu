@@ -1,0 +1,589 @@
+// C ABI (include/streamstab_b200.h): stateless ops and the device-resident
+// session that replaces SessionState + stabilize_step / stream_end_step
+// (consistency.py:306-413).  The index logic (3-pair ring, consecutive
+// positions, one-frame latency, error texts) follows consistency.py:321-353
+// exactly; the per-frame math is K1 (k_presolve) + K2 (solve_planar).
+#include <cstring>
+#include <string>
+
+#include "ss_common.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int cuda_status(cudaError_t e, const char *what)
+{
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? SS_NO_MEMORY : SS_CUDA_ERROR;
+}
+
+static int check_c(int c)
+{
+    if (c != 1 && c != 3) {
+        set_error("frame must be (H, W, 1|3)");
+        return SS_VALUE_ERROR;
+    }
+    return SS_OK;
+}
+
+static int check_hw(int h, int w)
+{
+    if (h <= 0 || w <= 0) {
+        set_error("zero-sized frame");
+        return SS_VALUE_ERROR;
+    }
+    return SS_OK;
+}
+
+// u8 -> f32 (x / 255) ingest, HWC
+__global__ void k_u8_to_f32(const uint8_t *__restrict__ src, long n, float *__restrict__ dst)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = __fdiv_rn((float)src[i], 255.0f);
+}
+
+// rint(clip(x, 0, 1) * 255) -> u8 (service.py:101-102, imgio.py:132)
+__global__ void k_f32_to_u8(const float *__restrict__ src, long n, uint8_t *__restrict__ dst)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = (uint8_t)rintf(__fmul_rn(fminf(fmaxf(src[i], 0.0f), 1.0f), 255.0f));
+}
+
+__global__ void k_fill_flow(float *__restrict__ uv, uint8_t *__restrict__ valid, long n, float u,
+                            float v)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        reinterpret_cast<float2 *>(uv)[i] = make_float2(u, v);
+        valid[i] = 1;
+    }
+}
+
+}  // namespace ss
+
+using namespace ss;
+
+// ---------------------------------------------------------------------------
+struct ss_session {
+    int h, w, ci, cp;
+    cudaStream_t stream;
+    bool own_stream;
+    struct Slot {
+        int64_t pos;
+        float *I, *P;
+    } slot[3];
+    int order[3];  // slot indices in push order (oldest first)
+    int n_pairs;
+    float *O, *O_new;  // prev_output (HWC) and solver output
+    bool has_output;
+    int64_t solved_through;
+    // flows for the pending step: [0] t -> t-1, [1] t -> t+1
+    float *uv[2];
+    uint8_t *valid[2];
+    int64_t flow_for[2];  // step position the slot was provided for (-1 none)
+    float *A, *lapP, *wc;  // planar solver inputs
+    SolverWork solver;
+    cudaEvent_t ev[3];
+    ss_timing timing;
+};
+
+static int session_alloc(ss_session *s)
+{
+    const size_t px = (size_t)s->h * s->w;
+    for (auto &sl : s->slot) {
+        SS_CUDA_TRY(cudaMalloc(&sl.I, px * s->ci * sizeof(float)));
+        SS_CUDA_TRY(cudaMalloc(&sl.P, px * s->cp * sizeof(float)));
+        sl.pos = 0;
+    }
+    SS_CUDA_TRY(cudaMalloc(&s->O, px * s->cp * sizeof(float)));
+    SS_CUDA_TRY(cudaMalloc(&s->O_new, px * s->cp * sizeof(float)));
+    for (int k = 0; k < 2; ++k) {
+        SS_CUDA_TRY(cudaMalloc(&s->uv[k], px * 2 * sizeof(float)));
+        SS_CUDA_TRY(cudaMalloc(&s->valid[k], px));
+    }
+    SS_CUDA_TRY(cudaMalloc(&s->A, px * s->cp * sizeof(float)));
+    SS_CUDA_TRY(cudaMalloc(&s->lapP, px * s->cp * sizeof(float)));
+    SS_CUDA_TRY(cudaMalloc(&s->wc, px * sizeof(float)));
+    for (auto &e : s->ev) SS_CUDA_TRY(cudaEventCreate(&e));
+    s->solver.h = s->h;
+    s->solver.w = s->w;
+    s->solver.c = s->cp;
+    return s->solver.ensure(s->h, s->w, s->cp, 150) == SS_OK ? SS_OK : SS_NO_MEMORY;
+}
+
+static void session_free(ss_session *s)
+{
+    for (auto &sl : s->slot) {
+        cudaFree(sl.I);
+        cudaFree(sl.P);
+    }
+    cudaFree(s->O);
+    cudaFree(s->O_new);
+    for (int k = 0; k < 2; ++k) {
+        cudaFree(s->uv[k]);
+        cudaFree(s->valid[k]);
+    }
+    cudaFree(s->A);
+    cudaFree(s->lapP);
+    cudaFree(s->wc);
+    for (auto &e : s->ev)
+        if (e) cudaEventDestroy(e);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+}
+
+static int copy_frame(ss_session *s, float *dst, const void *src, int c, int dtype, int where)
+{
+    const size_t n = (size_t)s->h * s->w * c;
+    const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (dtype == SS_F32) {
+        SS_CUDA_TRY(cudaMemcpyAsync(dst, src, n * sizeof(float), kind, s->stream));
+        return SS_OK;
+    }
+    if (dtype != SS_U8) {
+        set_error("unsupported dtype");
+        return SS_VALUE_ERROR;
+    }
+    // stage u8 in the tail of dst (4x smaller), then widen in place-safe order
+    // via a separate staging buffer: use O_new as scratch (not live here)
+    uint8_t *stage = reinterpret_cast<uint8_t *>(s->O_new);
+    if ((size_t)s->h * s->w * s->cp * sizeof(float) < n) {
+        set_error("u8 staging buffer too small");
+        return SS_VALUE_ERROR;
+    }
+    SS_CUDA_TRY(cudaMemcpyAsync(stage, src, n, kind, s->stream));
+    k_u8_to_f32<<<blocks_for((long)n, 256), 256, 0, s->stream>>>(stage, (long)n, dst);
+    SS_LAUNCH_CHECK("k_u8_to_f32");
+    return SS_OK;
+}
+
+extern "C" {
+
+int ss_abi_version(void) { return SS_ABI_VERSION; }
+
+const char *ss_status_string(int status)
+{
+    switch (status) {
+    case SS_OK: return "ok";
+    case SS_RESOLUTION_MISMATCH: return "resolution mismatch";
+    case SS_VALUE_ERROR: return "value error";
+    case SS_SOLVER_DIVERGENCE: return "solver divergence";
+    case SS_CUDA_ERROR: return "cuda error";
+    case SS_NO_MEMORY: return "out of device memory";
+    default: return "unknown status";
+    }
+}
+
+const char *ss_last_error(void) { return g_last_error.c_str(); }
+
+int ss_init(int device)
+{
+    SS_CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    SS_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        set_error("streamstab_b200 targets sm_100 (B200); found sm_" + std::to_string(prop.major) +
+                  std::to_string(prop.minor));
+        return SS_CUDA_ERROR;
+    }
+    return SS_OK;
+}
+
+int ss_params_validate(const ss_params *p)
+{
+    // consistency.py:53-69, same order and messages
+    if (!(0.0f <= p->k1 && p->k1 < 1.0f && 0.0f <= p->k2 && p->k2 < 1.0f)) {
+        set_error("k1 and k2 must lie in [0, 1)");
+        return SS_VALUE_ERROR;
+    }
+    if ((double)p->k1 + (double)p->k2 <= 0.0) {
+        set_error("k1+k2 must be > 0");
+        return SS_VALUE_ERROR;
+    }
+    if ((double)p->k1 + (double)p->k2 >= 1.0) {
+        set_error("k1+k2 must be < 1");
+        return SS_VALUE_ERROR;
+    }
+    if (p->lam < 0.0f) {
+        set_error("lambda must be >= 0");
+        return SS_VALUE_ERROR;
+    }
+    if (p->eta <= 0.0f) {
+        set_error("eta must be > 0");
+        return SS_VALUE_ERROR;
+    }
+    if (!(0.0f <= p->kappa && p->kappa < 1.0f)) {
+        set_error("kappa must be in [0, 1)");
+        return SS_VALUE_ERROR;
+    }
+    if (p->iterations < 1) {
+        set_error("iterations must be >= 1");
+        return SS_VALUE_ERROR;
+    }
+    if (p->flow_downscale != 1 && p->flow_downscale != 2 && p->flow_downscale != 4) {
+        set_error("flow_downscale must be 1, 2 or 4");
+        return SS_VALUE_ERROR;
+    }
+    return SS_OK;
+}
+
+// ---- stateless ops ----------------------------------------------------------
+int ss_backward_warp(const float *img, int h, int w, int c, const float *uv, const uint8_t *valid,
+                     float *out, float *mask, void *stream)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    return launch_backward_warp(img, h, w, c, uv, valid, out, mask, (cudaStream_t)stream);
+}
+
+int ss_occlusion_mask(const float *fwd_uv, const uint8_t *fwd_valid, const float *bwd_uv,
+                      const uint8_t *bwd_valid, int h, int w, float *out, void *stream)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    return launch_occlusion(fwd_uv, fwd_valid, bwd_uv, bwd_valid, h, w, out, (cudaStream_t)stream);
+}
+
+int ss_warp_weight(const float *ref, const float *warped, int h, int w, int c, float alpha,
+                   float bound, const float *validity, float *out, void *stream)
+{
+    if (!(0.0f <= bound && bound < 1.0f)) {
+        set_error("bound must lie in [0, 1)");
+        return SS_VALUE_ERROR;
+    }
+    return launch_warp_weight(ref, warped, (long)h * w, c, alpha, bound, validity, out,
+                              (cudaStream_t)stream);
+}
+
+int ss_local_blend(const float *cur, const float *prev, const float *next, const float *wp,
+                   const float *wn, int h, int w, int c, float *out, void *stream)
+{
+    return launch_local_blend(cur, prev, next, wp, wn, (long)h * w, c, out, (cudaStream_t)stream);
+}
+
+int ss_adaptive_blend(const float *g, const float *l, const float *wp, int h, int w, int c,
+                      float *out, void *stream)
+{
+    return launch_adaptive_blend(g, l, wp, (long)h * w, c, out, (cudaStream_t)stream);
+}
+
+int ss_consistency_weight(const float *cur, const float *blended, int h, int w, int c,
+                          float alpha, float lam, float *out, void *stream)
+{
+    if (lam < 0.0f) {
+        set_error("lambda must be >= 0");
+        return SS_VALUE_ERROR;
+    }
+    return launch_consistency_weight(cur, blended, (long)h * w, c, alpha, lam, out,
+                                     (cudaStream_t)stream);
+}
+
+int ss_laplacian(const float *img, int h, int w, int c, float *out, void *stream)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    return launch_laplacian(img, h, w, c, out, false, (cudaStream_t)stream);
+}
+
+int ss_solve_screened_poisson(const float *processed, const float *target, const float *wc,
+                              int h, int w, int c, const ss_params *p, const float *init,
+                              float *out, int *div_iter, void *stream)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    if (int rc = check_c(c)) return rc;
+    if (p->iterations < 1) {
+        set_error("iterations must be >= 1");
+        return SS_VALUE_ERROR;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    static thread_local SolverWork wk;
+    const size_t n = (size_t)h * w * c;
+    struct Tmp {
+        float *p = nullptr;
+        ~Tmp() { cudaFree(p); }
+    } tA, tL, tI;
+    SS_CUDA_TRY(cudaMalloc(&tA.p, n * sizeof(float)));
+    SS_CUDA_TRY(cudaMalloc(&tL.p, n * sizeof(float)));
+    if (init && init != target) SS_CUDA_TRY(cudaMalloc(&tI.p, n * sizeof(float)));
+    wk.h = h; wk.w = w; wk.c = c;
+    if (int rc = wk.ensure(h, w, c, p->iterations)) return rc;
+    if (int rc = launch_hwc_to_planar(target, h, w, c, tA.p, st)) return rc;
+    if (int rc = launch_laplacian(processed, h, w, c, tL.p, true, st)) return rc;
+    if (tI.p)
+        if (int rc = launch_hwc_to_planar(init, h, w, c, tI.p, st)) return rc;
+    const int rc = solve_planar(wk, tA.p, tI.p ? tI.p : tA.p, tL.p, wc, *p, out, div_iter, st);
+    cudaStreamSynchronize(st);  // temporaries are freed on return
+    return rc;
+}
+
+// ---- sessions ----------------------------------------------------------------
+int ss_session_create(int h, int w, int c_in, int c_proc, void *stream, ss_session **out)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    if (int rc = check_c(c_in)) return rc;
+    if (int rc = check_c(c_proc)) return rc;
+    ss_session *s = new (std::nothrow) ss_session();
+    if (!s) return SS_NO_MEMORY;
+    s->h = h;
+    s->w = w;
+    s->ci = c_in;
+    s->cp = c_proc;
+    s->n_pairs = 0;
+    s->has_output = false;
+    s->solved_through = 0;
+    s->flow_for[0] = s->flow_for[1] = -1;
+    if (stream) {
+        s->stream = (cudaStream_t)stream;
+        s->own_stream = false;
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete s;
+            return cuda_status(e, "cudaStreamCreate");
+        }
+        s->own_stream = true;
+    }
+    int rc = session_alloc(s);
+    if (rc) {
+        session_free(s);
+        delete s;
+        return rc;
+    }
+    *out = s;
+    return SS_OK;
+}
+
+int ss_session_destroy(ss_session *s)
+{
+    if (!s) return SS_OK;
+    cudaStreamSynchronize(s->stream);
+    session_free(s);
+    delete s;
+    return SS_OK;
+}
+
+int ss_session_reset(ss_session *s)
+{
+    s->n_pairs = 0;
+    s->has_output = false;
+    s->solved_through = 0;
+    s->flow_for[0] = s->flow_for[1] = -1;
+    s->timing = ss_timing{};
+    return SS_OK;
+}
+
+void *ss_session_stream(const ss_session *s) { return (void *)s->stream; }
+
+int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, int dtype,
+                 int where)
+{
+    // consistency.py:326-330
+    if (s->n_pairs > 0) {
+        const int64_t last = s->slot[s->order[s->n_pairs - 1]].pos;
+        if (position != last + 1) {
+            set_error("non-consecutive frame position " + std::to_string(position) + " after " +
+                      std::to_string(last));
+            return SS_VALUE_ERROR;
+        }
+    }
+    // choose the slot: a free one, else the oldest (pop(0), :336-337)
+    int idx;
+    if (s->n_pairs < 3) {
+        bool used[3] = {false, false, false};
+        for (int i = 0; i < s->n_pairs; ++i) used[s->order[i]] = true;
+        idx = !used[0] ? 0 : (!used[1] ? 1 : 2);
+        s->order[s->n_pairs++] = idx;
+    } else {
+        idx = s->order[0];
+        s->order[0] = s->order[1];
+        s->order[1] = s->order[2];
+        s->order[2] = idx;
+    }
+    auto &sl = s->slot[idx];
+    if (int rc = copy_frame(s, sl.I, I, s->ci, dtype, where)) return rc;
+    if (int rc = copy_frame(s, sl.P, P, s->cp, dtype, where)) return rc;
+    sl.pos = position;
+    if (!s->has_output) {  // :338-340 (prev_output = first processed frame)
+        SS_CUDA_TRY(cudaMemcpyAsync(s->O, sl.P, (size_t)s->h * s->w * s->cp * sizeof(float),
+                                    cudaMemcpyDeviceToDevice, s->stream));
+        s->has_output = true;
+        s->solved_through = position;
+    }
+    return SS_OK;
+}
+
+int64_t ss_solved_through(const ss_session *s) { return s->solved_through; }
+
+static const ss_session::Slot *find_pos(const ss_session *s, int64_t pos)
+{
+    for (int i = 0; i < s->n_pairs; ++i)
+        if (s->slot[s->order[i]].pos == pos) return &s->slot[s->order[i]];
+    return nullptr;
+}
+
+int ss_pending(const ss_session *s, int64_t *t, int *has_prev, int *has_next)
+{
+    const int64_t tt = s->solved_through + 1;
+    if (t) *t = tt;
+    if (has_prev) *has_prev = find_pos(s, tt - 1) && find_pos(s, tt);
+    if (has_next) *has_next = find_pos(s, tt + 1) != nullptr;
+    return SS_OK;
+}
+
+int ss_set_flow(ss_session *s, int which, const float *uv, const uint8_t *valid, int where)
+{
+    if (which != 0 && which != 1) {
+        set_error("which must be 0 (to previous) or 1 (to next)");
+        return SS_VALUE_ERROR;
+    }
+    const size_t px = (size_t)s->h * s->w;
+    const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    SS_CUDA_TRY(cudaMemcpyAsync(s->uv[which], uv, px * 2 * sizeof(float), kind, s->stream));
+    if (valid)
+        SS_CUDA_TRY(cudaMemcpyAsync(s->valid[which], valid, px, kind, s->stream));
+    else
+        SS_CUDA_TRY(cudaMemsetAsync(s->valid[which], 1, px, s->stream));
+    s->flow_for[which] = s->solved_through + 1;
+    return SS_OK;
+}
+
+int ss_set_constant_flow(ss_session *s, int which, double u, double v, int steps)
+{
+    if (which != 0 && which != 1) {
+        set_error("which must be 0 (to previous) or 1 (to next)");
+        return SS_VALUE_ERROR;
+    }
+    // ConstantFlow: uv = (u * steps, v * steps) in float64 then float32
+    const float fu = (float)(u * steps), fv = (float)(v * steps);
+    const long px = (long)s->h * s->w;
+    k_fill_flow<<<blocks_for(px, 256), 256, 0, s->stream>>>(s->uv[which], s->valid[which], px, fu, fv);
+    SS_LAUNCH_CHECK("k_fill_flow");
+    s->flow_for[which] = s->solved_through + 1;
+    return SS_OK;
+}
+
+int ss_check_step(const ss_session *s, int with_next, int64_t *tp)
+{
+    // _snippet (consistency.py:342-353)
+    if (!s->has_output) {
+        set_error("no buffered frames");
+        return SS_VALUE_ERROR;
+    }
+    const int64_t t = s->solved_through + 1;
+    if (tp) *tp = t;
+    if (!find_pos(s, t - 1) || !find_pos(s, t)) {
+        set_error("missing buffered frames around position " + std::to_string(t));
+        return SS_VALUE_ERROR;
+    }
+    const bool has_next = find_pos(s, t + 1) != nullptr;
+    if (with_next && !has_next) {
+        set_error("missing next frame " + std::to_string(t + 1) +
+                  "; use stream_end_step at stream end");
+        return SS_VALUE_ERROR;
+    }
+    if (!with_next && has_next) {
+        set_error("next frame is available; use stabilize_step");
+        return SS_VALUE_ERROR;
+    }
+    return SS_OK;
+}
+
+int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
+{
+    if (div_iter) *div_iter = 0;
+    int64_t t = 0;
+    if (int rc = ss_check_step(s, with_next, &t)) return rc;
+    const auto *prev = find_pos(s, t - 1), *cur = find_pos(s, t), *next = find_pos(s, t + 1);
+    if (s->flow_for[0] != t || (with_next && s->flow_for[1] != t)) {
+        set_error("flows for position " + std::to_string(t) + " were not provided");
+        return SS_VALUE_ERROR;
+    }
+    if (p->iterations < 1) {
+        set_error("iterations must be >= 1");
+        return SS_VALUE_ERROR;
+    }
+    SS_CUDA_TRY(cudaEventRecord(s->ev[0], s->stream));
+    PresolveArgs a;
+    a.h = s->h;
+    a.w = s->w;
+    a.I_prev = prev->I;
+    a.P_prev = prev->P;
+    a.I_cur = cur->I;
+    a.P_cur = cur->P;
+    a.I_next = with_next ? next->I : nullptr;
+    a.P_next = with_next ? next->P : nullptr;
+    a.O_prev = s->O;
+    a.uv_prev = s->uv[0];
+    a.valid_prev = s->valid[0];
+    a.uv_next = s->uv[1];
+    a.valid_next = s->valid[1];
+    a.p = *p;
+    a.A = s->A;
+    a.lapP = s->lapP;
+    a.wc = s->wc;
+    a.wp_out = a.wn_out = nullptr;
+    if (int rc = launch_presolve(a, s->ci, s->cp, with_next != 0, s->stream)) return rc;
+    SS_CUDA_TRY(cudaEventRecord(s->ev[1], s->stream));
+    int rc = solve_planar(s->solver, s->A, s->A, s->lapP, s->wc, *p, s->O_new, div_iter, s->stream,
+                          s->ev[2]);
+    if (rc) return rc;  // divergence: state not advanced (consistency.py:293, :410)
+    SS_CUDA_TRY(cudaEventSynchronize(s->ev[2]));
+    float t_blend = 0.f, t_solve = 0.f;
+    cudaEventElapsedTime(&t_blend, s->ev[0], s->ev[1]);
+    cudaEventElapsedTime(&t_solve, s->ev[1], s->ev[2]);
+    s->timing.warp_blend_ms = t_blend;
+    s->timing.solve_ms = t_solve;
+    float *tmp = s->O;  // commit (consistency.py:410-412)
+    s->O = s->O_new;
+    s->O_new = tmp;
+    s->solved_through = t;
+    s->flow_for[0] = s->flow_for[1] = -1;
+    return SS_OK;
+}
+
+int ss_output(const ss_session *s, void *dst, int dtype, int where)
+{
+    if (!s->has_output) {
+        set_error("no buffered frames");
+        return SS_VALUE_ERROR;
+    }
+    const size_t n = (size_t)s->h * s->w * s->cp;
+    const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (dtype == SS_F32) {
+        SS_CUDA_TRY(cudaMemcpyAsync(dst, s->O, n * sizeof(float), kind, s->stream));
+    } else if (dtype == SS_U8) {
+        uint8_t *tmp = reinterpret_cast<uint8_t *>(s->O_new);  // scratch between steps
+        k_f32_to_u8<<<blocks_for((long)n, 256), 256, 0, s->stream>>>(s->O, (long)n, tmp);
+        SS_LAUNCH_CHECK("k_f32_to_u8");
+        SS_CUDA_TRY(cudaMemcpyAsync(dst, tmp, n, kind, s->stream));
+    } else {
+        set_error("unsupported dtype");
+        return SS_VALUE_ERROR;
+    }
+    SS_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return SS_OK;
+}
+
+const float *ss_output_device(const ss_session *s) { return s->has_output ? s->O : nullptr; }
+
+int ss_last_timing(const ss_session *s, ss_timing *t)
+{
+    *t = s->timing;
+    return SS_OK;
+}
+
+int ss_flows(const ss_session *s, int which, float *uv_dst, uint8_t *valid_dst, int where)
+{
+    if (which != 0 && which != 1) {
+        set_error("which must be 0 (to previous) or 1 (to next)");
+        return SS_VALUE_ERROR;
+    }
+    const size_t px = (size_t)s->h * s->w;
+    const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (uv_dst) SS_CUDA_TRY(cudaMemcpyAsync(uv_dst, s->uv[which], px * 2 * sizeof(float), kind, s->stream));
+    if (valid_dst) SS_CUDA_TRY(cudaMemcpyAsync(valid_dst, s->valid[which], px, kind, s->stream));
+    SS_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return SS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,637 @@
+// Screened-Poisson SGD-momentum solver (consistency.py:253-295) for sm_100a.
+//
+// Per element and iteration j the reference evaluates, in float32 with one
+// rounding per op (consistency.py:282-291):
+//     g = ((((O*-4 + N) + S) + W) + E)      5-point Neumann Laplacian (:211-221)
+//     g = g - lapP ; d = (O - A) * wc ; g = (d - g) * eta
+//     m = (O - O_prev) * kappa ; O' = (O - g) + m
+// and raises SolverDivergence(j + 1) when np.sum(O') (numpy float32 pairwise
+// summation over the HWC array) is not finite (:292-293).
+//
+// Fast path (k_sgd_blocked): temporal blocking.  A CTA loads a (RH x RW)
+// region of one channel plane into registers (2 columns x R rows per
+// thread) and shared memory, runs K iterations with a K-pixel halo, and writes
+// back the interior tile.  Each element sees exactly the reference op sequence,
+// so iterates are bit-identical to the streaming kernel and to numpy.  Each
+// pass records max|O| over its iterations; a pass that reaches the "grey zone"
+// (|O| > FLT_MAX / 2n, where a float32 sum might overflow) or produces a
+// non-finite value triggers an exact replay (k_sgd_iter + a device restatement
+// of numpy's pairwise summation tree) that reports the reference's divergence
+// iteration bit-exactly.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "ss_common.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+// ---------------------------------------------------------------------------
+// streaming kernel: one iteration, all channel planes (planar [c][h][w])
+__global__ void __launch_bounds__(256) k_sgd_iter(const float *__restrict__ Ocur,
+                                                  const float *__restrict__ Oprev,
+                                                  const float *__restrict__ A,
+                                                  const float *__restrict__ lapP,
+                                                  const float *__restrict__ wc, int h, int w,
+                                                  int c, float eta, float kappa,
+                                                  float *__restrict__ Onew)
+{
+    const long hw = (long)h * w;
+    const long n = hw * c;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long)gridDim.x * blockDim.x) {
+        const long p = i % hw;
+        const int y = (int)(p / w), x = (int)(p - (long)y * w);
+        const float o = Ocur[i];
+        float g = fmul(o, -4.0f);
+        g = fadd(g, Ocur[y > 0 ? i - w : i]);
+        g = fadd(g, Ocur[y < h - 1 ? i + w : i]);
+        g = fadd(g, Ocur[x > 0 ? i - 1 : i]);
+        g = fadd(g, Ocur[x < w - 1 ? i + 1 : i]);
+        g = fsub(g, lapP[i]);
+        float d = fsub(o, A[i]);
+        d = fmul(d, wc[p]);
+        g = fsub(d, g);
+        g = fmul(g, eta);
+        float m = fsub(o, Oprev[i]);
+        m = fmul(m, kappa);
+        Onew[i] = fadd(fsub(o, g), m);
+    }
+}
+
+template <int C>
+__global__ void k_planar_clamp_to_hwc(const float *__restrict__ src, long hw,
+                                      float *__restrict__ dst)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hw) return;
+#pragma unroll
+    for (int k = 0; k < C; ++k) dst[i * C + k] = fminf(fmaxf(src[k * hw + i], 0.0f), 1.0f);
+}
+
+// ---------------------------------------------------------------------------
+// temporally blocked kernel
+namespace blk {
+constexpr int K = 8;          // iterations per pass (= halo width)
+constexpr int R = 8;          // rows per thread
+constexpr int PAIRS = 64;     // column pairs per region row -> RW = 128
+constexpr int STRIPS = 8;     // row strips -> RH = 64
+constexpr int RW = 2 * PAIRS;
+constexpr int RH = R * STRIPS;
+constexpr int OW = RW - 2 * K;  // interior tile
+constexpr int OH = RH - 2 * K;
+constexpr int SW = RW + 4;      // smem row pitch: 2 padding columns each side
+constexpr int SH = RH + 2;      // 1 padding row each side
+constexpr int THREADS = PAIRS * STRIPS;
+constexpr size_t SMEM = 2ull * SH * SW * sizeof(float);
+static_assert(K % R == 0 && K % 2 == 0, "halo must align with strips and pairs");
+}  // namespace blk
+
+struct BlockedArgs {
+    const float *O, *Oprev;  // planar input iterates (pass 0: init for both)
+    const float *A, *lapP, *wc;
+    float *Oout, *Oprev_out;  // planar outputs (non-final pass)
+    float *hwc_out;           // final pass: clamp(O) as HWC
+    int h, w, c;
+    int iters;                // iterations in this pass (<= K)
+    float eta, kappa;
+    unsigned *maxbits;        // this pass's slot
+};
+
+__device__ __forceinline__ float sgd_update(float o, float op, float N, float S, float W,
+                                            float E, float lp, float a, float wcv, float eta,
+                                            float kappa)
+{
+    float g = fmul(o, -4.0f);
+    g = fadd(g, N);
+    g = fadd(g, S);
+    g = fadd(g, W);
+    g = fadd(g, E);
+    g = fsub(g, lp);
+    float d = fsub(o, a);
+    d = fmul(d, wcv);
+    g = fsub(d, g);
+    g = fmul(g, eta);
+    float m = fsub(o, op);
+    m = fmul(m, kappa);
+    return fadd(fsub(o, g), m);
+}
+
+// One iteration for one thread's 2 x R block.  X holds the current iterate,
+// Y the previous one; Y is overwritten with the new iterate (the caller swaps
+// roles).  Reads neighbours from smem buffer `cur`, writes new values to `nxt`.
+template <bool FAST>
+__device__ __forceinline__ void blk_iter(float (&X)[blk::R][2], float (&Y)[blk::R][2],
+                                         const float (&Av)[blk::R][2],
+                                         const float (&Lv)[blk::R][2],
+                                         const float (&Wv)[blk::R][2], const float *cur,
+                                         float *nxt, int r0, int c0, int lo_r, int hi_r,
+                                         int lo_c, int hi_c, float eta, float kappa, float &mx)
+{
+    using namespace blk;
+    // smem index of region (rr, cc): (rr + 1) * SW + (cc + 2)
+    if (FAST) {
+        float wv[R], ev[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            wv[r] = cur[(r0 + r + 1) * SW + c0 + 1];
+            ev[r] = cur[(r0 + r + 1) * SW + c0 + 4];
+        }
+        const float2 nv = *reinterpret_cast<const float2 *>(cur + r0 * SW + c0 + 2);
+        const float2 sv = *reinterpret_cast<const float2 *>(cur + (r0 + R + 1) * SW + c0 + 2);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const float n0 = r == 0 ? nv.x : X[r - 1][0];
+            const float n1 = r == 0 ? nv.y : X[r - 1][1];
+            const float s0 = r == R - 1 ? sv.x : X[r + 1][0];
+            const float s1 = r == R - 1 ? sv.y : X[r + 1][1];
+            const float u0 = sgd_update(X[r][0], Y[r][0], n0, s0, wv[r], X[r][1], Lv[r][0],
+                                        Av[r][0], Wv[r][0], eta, kappa);
+            const float u1 = sgd_update(X[r][1], Y[r][1], n1, s1, X[r][0], ev[r], Lv[r][1],
+                                        Av[r][1], Wv[r][1], eta, kappa);
+            Y[r][0] = u0;
+            Y[r][1] = u1;
+            mx = fmaxf(mx, fmaxf(fabsf(u0), fabsf(u1)));
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int rr = r0 + r;
+            const int nr = max(rr - 1, lo_r), sr = min(rr + 1, hi_r);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int cc = c0 + k;
+                const int wcl = max(cc - 1, lo_c), ecl = min(cc + 1, hi_c);
+                const float N = cur[(nr + 1) * SW + cc + 2];
+                const float S = cur[(sr + 1) * SW + cc + 2];
+                const float Wn = cur[(rr + 1) * SW + wcl + 2];
+                const float En = cur[(rr + 1) * SW + ecl + 2];
+                const float u = sgd_update(X[r][k], Y[r][k], N, S, Wn, En, Lv[r][k], Av[r][k],
+                                           Wv[r][k], eta, kappa);
+                Y[r][k] = u;
+                mx = fmaxf(mx, fabsf(u));
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        *reinterpret_cast<float2 *>(nxt + (r0 + r + 1) * SW + c0 + 2) = make_float2(Y[r][0], Y[r][1]);
+}
+
+template <bool FAST>
+__device__ __forceinline__ void blk_run(float (&X)[blk::R][2], float (&Y)[blk::R][2],
+                                        const float (&Av)[blk::R][2],
+                                        const float (&Lv)[blk::R][2],
+                                        const float (&Wv)[blk::R][2], float *sm0, float *sm1,
+                                        int r0, int c0, int lo_r, int hi_r, int lo_c, int hi_c,
+                                        int iters, float eta, float kappa, float &mx)
+{
+    // iterations alternate roles: even -> (X cur, Y prev) read sm0 write sm1
+    for (int it = 0; it < iters; it += 2) {
+        blk_iter<FAST>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, eta, kappa, mx);
+        __syncthreads();
+        if (it + 1 < iters) {
+            blk_iter<FAST>(Y, X, Av, Lv, Wv, sm1, sm0, r0, c0, lo_r, hi_r, lo_c, hi_c, eta,
+                           kappa, mx);
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(blk::THREADS, 1) k_sgd_blocked(BlockedArgs a)
+{
+    using namespace blk;
+    extern __shared__ float4 smem_raw[];
+    float *sm0 = reinterpret_cast<float *>(smem_raw);
+    float *sm1 = sm0 + SH * SW;
+
+    const int p = threadIdx.x, s = threadIdx.y;
+    const int ch = blockIdx.z;
+    const int rx0 = blockIdx.x * OW - K, ry0 = blockIdx.y * OH - K;
+    const int c0 = 2 * p, r0 = s * R;  // region coords of this thread's block
+    const int h = a.h, w = a.w;
+    const long hw = (long)h * w;
+    const long plane = (long)ch * hw;
+
+    // zero both buffers (padding must be finite; interior is overwritten)
+    for (int i = threadIdx.y * PAIRS + threadIdx.x; i < 2 * SH * SW; i += THREADS) sm0[i] = 0.0f;
+
+    float X[R][2], Y[R][2], Av[R][2], Lv[R][2], Wv[R][2];
+    const int gx0 = rx0 + c0, gy0 = ry0 + r0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int gy = min(max(gy0 + r, 0), h - 1);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int gx = min(max(gx0 + k, 0), w - 1);
+            const long q = (long)gy * w + gx;
+            X[r][k] = __ldg(a.O + plane + q);
+            Y[r][k] = __ldg(a.Oprev + plane + q);
+            Av[r][k] = __ldg(a.A + plane + q);
+            Lv[r][k] = __ldg(a.lapP + plane + q);
+            Wv[r][k] = __ldg(a.wc + q);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        *reinterpret_cast<float2 *>(sm0 + (r0 + r + 1) * SW + c0 + 2) = make_float2(X[r][0], X[r][1]);
+    __syncthreads();
+
+    // clamp ranges (region coords) for the replicate boundary; the padding
+    // row/column (-1, RH / RW) bounds the region edges
+    const int lo_r = max(-ry0, -1), hi_r = min(h - 1 - ry0, RH);
+    const int lo_c = max(-rx0, -1), hi_c = min(w - 1 - rx0, RW);
+    const bool fast = gx0 >= 1 && gx0 + 2 <= w - 1 && gy0 >= 1 && gy0 + R <= h - 1;
+    float mx = 0.0f;
+    if (fast)
+        blk_run<true>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters, a.eta,
+                      a.kappa, mx);
+    else
+        blk_run<false>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters,
+                       a.eta, a.kappa, mx);
+
+    // after an odd number of iterations the current iterate lives in Y
+    const bool odd = a.iters & 1;
+    const bool interior_r = r0 >= K && r0 + R <= RH - K;
+    const bool interior_c = c0 >= K && c0 + 2 <= RW - K;
+    bool nan_seen = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int gy = gy0 + r;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const float o = odd ? Y[r][k] : X[r][k];
+            const float op = odd ? X[r][k] : Y[r][k];
+            nan_seen |= (o != o);
+            const int gx = gx0 + k;
+            if (interior_r && interior_c && gy < h && gx < w) {
+                const long q = (long)gy * w + gx;
+                if (a.hwc_out) {
+                    a.hwc_out[q * a.c + ch] = fminf(fmaxf(o, 0.0f), 1.0f);
+                } else {
+                    a.Oout[plane + q] = o;
+                    a.Oprev_out[plane + q] = op;
+                }
+            }
+        }
+    }
+    unsigned bits = nan_seen ? 0x7fffffffu : __float_as_uint(mx);
+    bits = __reduce_max_sync(0xffffffffu, bits);
+    if ((threadIdx.x & 31) == 0 && bits > *(volatile unsigned *)a.maxbits) atomicMax(a.maxbits, bits);
+}
+
+// ---------------------------------------------------------------------------
+// exact numpy pairwise summation (umath add.reduce for contiguous float32):
+//   n < 8: sequential from -0.0 ; n <= 128: 8 accumulators + tail ;
+//   else split at n2 = n/2 - (n/2) % 8.  Leaves are summed one per thread,
+//   internal nodes by height in one CTA.  Elements are read in the
+//   reference's HWC order from the planar iterate.
+__global__ void k_pairwise_leaves(const float *__restrict__ planar, long hw, int C,
+                                  const int64_t *__restrict__ leaf_start,
+                                  const int32_t *__restrict__ leaf_len, int n_leaves,
+                                  float *__restrict__ vals)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= n_leaves) return;
+    const long s = leaf_start[l];
+    const int n = leaf_len[l];
+    auto at = [&](long e) { return planar[(e % C) * hw + e / C]; };
+    float res;
+    if (n < 8) {
+        res = -0.0f;
+        for (int i = 0; i < n; ++i) res = fadd(res, at(s + i));
+    } else {
+        float r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = at(s + j);
+        int i;
+        for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = fadd(r[j], at(s + i + j));
+        res = fadd(fadd(fadd(r[0], r[1]), fadd(r[2], r[3])), fadd(fadd(r[4], r[5]), fadd(r[6], r[7])));
+        for (; i < n; ++i) res = fadd(res, at(s + i));
+    }
+    vals[l] = res;
+}
+
+__global__ void k_pairwise_combine(const int32_t *__restrict__ left,
+                                   const int32_t *__restrict__ right,
+                                   const int *__restrict__ group_off, int n_groups, int n_leaves,
+                                   float *__restrict__ vals, float *__restrict__ out)
+{
+    for (int g = 0; g < n_groups; ++g) {
+        for (int i = group_off[g] + threadIdx.x; i < group_off[g + 1]; i += blockDim.x)
+            vals[n_leaves + i] = fadd(vals[left[i]], vals[right[i]]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int total = n_leaves + (n_groups ? group_off[n_groups] : 0);
+        *out = vals[total - 1];
+    }
+}
+
+void PairwisePlan::release()
+{
+    cudaFree(d_leaf_start);
+    cudaFree(d_leaf_len);
+    cudaFree(d_left);
+    cudaFree(d_right);
+    cudaFree(d_vals);
+    d_leaf_start = nullptr;
+    d_leaf_len = nullptr;
+    d_left = d_right = nullptr;
+    d_vals = nullptr;
+    n = 0;
+}
+
+PairwisePlan::~PairwisePlan() { release(); }
+
+namespace {
+struct Node {
+    int left, right;  // -1 for leaves
+    long start;
+    int len;
+    int height;
+};
+int build_tree(std::vector<Node> &nodes, long start, long n)
+{
+    if (n <= 128) {
+        nodes.push_back({-1, -1, start, (int)n, 0});
+        return (int)nodes.size() - 1;
+    }
+    long n2 = n / 2;
+    n2 -= n2 % 8;
+    const int l = build_tree(nodes, start, n2);
+    const int r = build_tree(nodes, start + n2, n - n2);
+    nodes.push_back({l, r, 0, 0, 1 + std::max(nodes[l].height, nodes[r].height)});
+    return (int)nodes.size() - 1;
+}
+}  // namespace
+
+int PairwisePlan::build(long hw_, int C_)
+{
+    if (hw_ * C_ == n && C_ == C) return SS_OK;
+    release();
+    hw = hw_;
+    C = C_;
+    n = hw * C;
+    std::vector<Node> nodes;
+    nodes.reserve((size_t)(2 * n / 64 + 16));
+    build_tree(nodes, 0, n);
+    // renumber: leaves first (in order), then internal nodes grouped by height
+    std::vector<int> id(nodes.size());
+    std::vector<int64_t> ls;
+    std::vector<int32_t> ll;
+    int maxh = 0;
+    for (size_t i = 0; i < nodes.size(); ++i) {
+        if (nodes[i].left < 0) {
+            id[i] = (int)ls.size();
+            ls.push_back(nodes[i].start);
+            ll.push_back(nodes[i].len);
+        }
+        maxh = std::max(maxh, nodes[i].height);
+    }
+    n_leaves = (int)ls.size();
+    std::vector<std::vector<int>> by_h(maxh + 1);
+    for (size_t i = 0; i < nodes.size(); ++i)
+        if (nodes[i].left >= 0) by_h[nodes[i].height].push_back((int)i);
+    std::vector<int32_t> lf, rt;
+    group_off.assign(1, 0);
+    int next = n_leaves;
+    for (int hgt = 1; hgt <= maxh; ++hgt) {
+        for (int i : by_h[hgt]) id[i] = next++;
+        group_off.push_back(group_off.back() + (int)by_h[hgt].size());
+    }
+    for (int hgt = 1; hgt <= maxh; ++hgt)
+        for (int i : by_h[hgt]) {
+            lf.push_back(id[nodes[i].left]);
+            rt.push_back(id[nodes[i].right]);
+        }
+    n_nodes = next;
+    SS_CUDA_TRY(cudaMalloc(&d_leaf_start, ls.size() * sizeof(int64_t)));
+    SS_CUDA_TRY(cudaMalloc(&d_leaf_len, ll.size() * sizeof(int32_t)));
+    SS_CUDA_TRY(cudaMalloc(&d_left, std::max<size_t>(1, lf.size()) * sizeof(int32_t)));
+    SS_CUDA_TRY(cudaMalloc(&d_right, std::max<size_t>(1, rt.size()) * sizeof(int32_t)));
+    SS_CUDA_TRY(cudaMalloc(&d_vals, (size_t)n_nodes * sizeof(float) + group_off.size() * sizeof(int) + 16));
+    SS_CUDA_TRY(cudaMemcpy(d_leaf_start, ls.data(), ls.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SS_CUDA_TRY(cudaMemcpy(d_leaf_len, ll.data(), ll.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (!lf.empty()) {
+        SS_CUDA_TRY(cudaMemcpy(d_left, lf.data(), lf.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        SS_CUDA_TRY(cudaMemcpy(d_right, rt.data(), rt.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    // group offsets live after the node values
+    int *d_off = reinterpret_cast<int *>(d_vals + n_nodes);
+    SS_CUDA_TRY(cudaMemcpy(d_off, group_off.data(), group_off.size() * sizeof(int), cudaMemcpyHostToDevice));
+    return SS_OK;
+}
+
+static int pairwise_sum(PairwisePlan &pl, const float *planar, float *out, cudaStream_t st)
+{
+    const int th = 128;
+    k_pairwise_leaves<<<blocks_for(pl.n_leaves, th), th, 0, st>>>(
+        planar, pl.hw, pl.C, pl.d_leaf_start, pl.d_leaf_len, pl.n_leaves, pl.d_vals);
+    const int *d_off = reinterpret_cast<const int *>(pl.d_vals + pl.n_nodes);
+    k_pairwise_combine<<<1, 1024, 0, st>>>(pl.d_left, pl.d_right, d_off,
+                                           (int)pl.group_off.size() - 1, pl.n_leaves, pl.d_vals,
+                                           out);
+    SS_LAUNCH_CHECK("pairwise_sum");
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+SolverWork::~SolverWork()
+{
+    for (auto &s : O)
+        for (auto &b : s) cudaFree(b);
+    cudaFree(maxbits);
+    cudaFree(sums);
+    cudaFree(d_result);
+    cudaFreeHost(h_result);
+}
+
+int SolverWork::ensure(int h_, int w_, int c_, int iterations)
+{
+    if (h_ != h || w_ != w || c_ != c) {
+        for (auto &s : O)
+            for (auto &b : s) {
+                cudaFree(b);
+                b = nullptr;
+            }
+        h = h_; w = w_; c = c_;
+        const size_t bytes = (size_t)h * w * c * sizeof(float);
+        for (auto &s : O)
+            for (auto &b : s) SS_CUDA_TRY(cudaMalloc(&b, bytes));
+    }
+    if (iterations > maxiters) {
+        cudaFree(maxbits);
+        cudaFree(sums);
+        maxbits = nullptr;
+        sums = nullptr;
+        maxiters = iterations;
+        SS_CUDA_TRY(cudaMalloc(&maxbits, (size_t)maxiters * sizeof(unsigned)));
+        SS_CUDA_TRY(cudaMalloc(&sums, (size_t)maxiters * sizeof(float)));
+    }
+    if (!h_result) {
+        SS_CUDA_TRY(cudaHostAlloc(&h_result, 4 * sizeof(int), cudaHostAllocDefault));
+        SS_CUDA_TRY(cudaMalloc(&d_result, 4 * sizeof(int)));
+    }
+    return SS_OK;
+}
+
+int solver_variant()
+{
+    static int v = [] {
+        const char *e = getenv("SS_SOLVER");
+        if (e && !strcmp(e, "stream")) return 0;
+        return 1;
+    }();
+    return v;
+}
+
+static int run_streaming(SolverWork &wk, const float *A, const float *init, const float *lapP,
+                         const float *wc, const ss_params &p, int n_iters, float *sums_from,
+                         int sum_from_iter, float **final_cur, cudaStream_t st)
+{
+    // buffers: O[0][0], O[0][1], O[1][0] rotate as (prev, cur, upd)
+    const long hw = (long)wk.h * wk.w;
+    const long n = hw * wk.c;
+    float *bufs[3] = {wk.O[0][0], wk.O[0][1], wk.O[1][0]};
+    SS_CUDA_TRY(cudaMemcpyAsync(bufs[0], init, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    SS_CUDA_TRY(cudaMemcpyAsync(bufs[1], init, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    int prev = 0, cur = 1, upd = 2;
+    const int th = 256;
+    const unsigned nb = (unsigned)std::min<long>(blocks_for(n, th), 148L * 16);
+    for (int j = 0; j < n_iters; ++j) {
+        k_sgd_iter<<<nb, th, 0, st>>>(bufs[cur], bufs[prev], A, lapP, wc, wk.h, wk.w, wk.c, p.eta,
+                                      p.kappa, bufs[upd]);
+        SS_LAUNCH_CHECK("k_sgd_iter");
+        if (sums_from && j >= sum_from_iter) {
+            int rc = pairwise_sum(wk.plan, bufs[upd], sums_from + j, st);
+            if (rc) return rc;
+        }
+        const int t = prev;
+        prev = cur;
+        cur = upd;
+        upd = t;
+    }
+    *final_cur = bufs[cur];
+    return SS_OK;
+}
+
+static int write_output(const float *planar, int h, int w, int c, float *out_hwc, cudaStream_t st)
+{
+    const long hw = (long)h * w;
+    if (c == 1)
+        k_planar_clamp_to_hwc<1><<<blocks_for(hw, 256), 256, 0, st>>>(planar, hw, out_hwc);
+    else
+        k_planar_clamp_to_hwc<3><<<blocks_for(hw, 256), 256, 0, st>>>(planar, hw, out_hwc);
+    SS_LAUNCH_CHECK("k_planar_clamp_to_hwc");
+    return SS_OK;
+}
+
+int solve_planar(SolverWork &wk, const float *A, const float *init, const float *lapP,
+                 const float *wc, const ss_params &p, float *out_hwc, int *div_iter,
+                 cudaStream_t st, cudaEvent_t done_ev)
+{
+    const int iters = p.iterations;
+    if (div_iter) *div_iter = 0;
+    if (iters < 1) {
+        set_error("iterations must be >= 1");
+        return SS_VALUE_ERROR;
+    }
+    int rc = wk.ensure(wk.h, wk.w, wk.c, iters);
+    if (rc) return rc;
+    if (!init) init = A;
+    const long hw = (long)wk.h * wk.w;
+    const long n = hw * wk.c;
+    const int n_pass = solver_variant() == 1 ? (iters + blk::K - 1) / blk::K : 0;
+
+    if (solver_variant() == 1) {
+        static bool attr = false;
+        if (!attr) {
+            SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)blk::SMEM));
+            attr = true;
+        }
+        SS_CUDA_TRY(cudaMemsetAsync(wk.maxbits, 0, (size_t)n_pass * sizeof(unsigned), st));
+        const dim3 grid((wk.w + blk::OW - 1) / blk::OW, (wk.h + blk::OH - 1) / blk::OH, wk.c);
+        const dim3 block(blk::PAIRS, blk::STRIPS);
+        const float *src_o = init, *src_op = init;
+        int set = 0;
+        for (int ps = 0; ps < n_pass; ++ps) {
+            BlockedArgs a;
+            a.O = src_o;
+            a.Oprev = src_op;
+            a.A = A;
+            a.lapP = lapP;
+            a.wc = wc;
+            a.Oout = wk.O[set][0];
+            a.Oprev_out = wk.O[set][1];
+            a.hwc_out = ps == n_pass - 1 ? out_hwc : nullptr;
+            a.h = wk.h; a.w = wk.w; a.c = wk.c;
+            a.iters = std::min(blk::K, iters - ps * blk::K);
+            a.eta = p.eta;
+            a.kappa = p.kappa;
+            a.maxbits = wk.maxbits + ps;
+            k_sgd_blocked<<<grid, block, blk::SMEM, st>>>(a);
+            SS_LAUNCH_CHECK("k_sgd_blocked");
+            src_o = wk.O[set][0];
+            src_op = wk.O[set][1];
+            set ^= 1;
+        }
+        if (done_ev) SS_CUDA_TRY(cudaEventRecord(done_ev, st));
+    } else {
+        float *fin = nullptr;
+        rc = run_streaming(wk, A, init, lapP, wc, p, iters, nullptr, 0, &fin, st);
+        if (rc) return rc;
+        if (done_ev) SS_CUDA_TRY(cudaEventRecord(done_ev, st));
+    }
+
+    // grey-zone test on the per-pass maxima (blocked) -- the streaming path
+    // always takes the exact check below
+    static thread_local std::vector<unsigned> hb;
+    const float thr = (float)(FLT_MAX / (2.0 * (double)n));
+    unsigned thr_bits;
+    std::memcpy(&thr_bits, &thr, sizeof thr_bits);
+    int first_grey_pass = -1;
+    if (solver_variant() == 1) {
+        hb.resize(n_pass);
+        SS_CUDA_TRY(cudaMemcpyAsync(hb.data(), wk.maxbits, n_pass * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        SS_CUDA_TRY(cudaStreamSynchronize(st));
+        for (int ps = 0; ps < n_pass; ++ps)
+            if (hb[ps] > thr_bits) {
+                first_grey_pass = ps;
+                break;
+            }
+        if (first_grey_pass < 0) return SS_OK;
+    } else {
+        first_grey_pass = 0;
+    }
+
+    // exact replay with numpy's pairwise sum from the first grey iteration
+    rc = wk.plan.build(hw, wk.c);
+    if (rc) return rc;
+    const int from_iter = solver_variant() == 1 ? first_grey_pass * blk::K : 0;
+    float *fin = nullptr;
+    rc = run_streaming(wk, A, init, lapP, wc, p, iters, wk.sums, from_iter, &fin, st);
+    if (rc) return rc;
+    static thread_local std::vector<float> hs;
+    hs.resize(iters);
+    SS_CUDA_TRY(cudaMemcpyAsync(hs.data(), wk.sums, iters * sizeof(float), cudaMemcpyDeviceToHost, st));
+    SS_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int j = from_iter; j < iters; ++j) {
+        if (!std::isfinite(hs[j])) {
+            if (div_iter) *div_iter = j + 1;
+            set_error("solver diverged at iteration " + std::to_string(j + 1));
+            return SS_SOLVER_DIVERGENCE;
+        }
+    }
+    return write_output(fin, wk.h, wk.w, wk.c, out_hwc, st);
+}
+
+}  // namespace ss

@@ -1,0 +1,308 @@
+"""GPU parity: the sm_100a path through the C ABI against the reference's golden
+vectors (tests/golden, produced by the reference itself) and the CPU oracle.
+
+Bars: bit-exact for warp, masks, occlusion, blends, Laplacian, the solver on
+identical inputs and the divergence iteration; exp-derived weights within
+2 ulp (CUDA expf vs numpy expf); stabilized outputs within 1e-5 max-abs (the
+north star allows 1e-3 for the fp32 path).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from conftest import stream_case
+
+pytestmark = pytest.mark.gpu
+
+OUT_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ss():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2301_00750_b200 as m
+
+    return m
+
+
+def ulp_close(a, b, ulps=2):
+    a = np.asarray(a, np.float32)
+    b = np.asarray(b, np.float32)
+    gap = np.abs(a.astype(np.float64) - b.astype(np.float64))
+    tol = ulps * np.spacing(np.maximum(np.abs(a), np.abs(b))).astype(np.float64)
+    return bool(np.all(gap <= tol))
+
+
+# ---------------------------------------------------------------- known answers
+class TestKnownAnswers:
+    """The reference's own hand-value tests (test_flow.py, test_consistency.py)."""
+
+    def test_zero_flow_identity(self, ss, random_frame):
+        warped, mask = ss.backward_warp(random_frame, ss.FlowField.zero(12, 10))
+        assert np.array_equal(warped, random_frame)
+        assert np.all(mask == 1.0)
+
+    def test_ramp_shift(self, ss):
+        image = np.array([[0.1, 0.2, 0.3, 0.4]], np.float32)[:, :, None]
+        uv = np.zeros((1, 4, 2), np.float32)
+        uv[:, :, 0] = 1.0
+        warped, mask = ss.backward_warp(image, ss.FlowField(uv))
+        assert warped[0, :, 0] == pytest.approx([0.2, 0.3, 0.4, 0.4], abs=1e-7)
+        assert mask[0].tolist() == [1.0, 1.0, 1.0, 0.0]
+
+    def test_far_oob_clamped(self, ss, random_frame):
+        uv = np.zeros((12, 10, 2), np.float32)
+        uv[:, :, 0] = 1e6
+        warped, mask = ss.backward_warp(random_frame, ss.FlowField(uv))
+        assert np.all(mask == 0.0)
+        assert np.allclose(warped, random_frame[:, -1:, :])
+
+    def test_resolution_mismatch(self, ss, random_frame):
+        with pytest.raises(ss.ResolutionMismatch):
+            ss.backward_warp(random_frame, ss.FlowField.zero(5, 5))
+
+    def test_occlusion_cases(self, ss):
+        def uni(h, w, u, v):
+            uv = np.empty((h, w, 2), np.float32)
+            uv[:, :, 0], uv[:, :, 1] = u, v
+            return ss.FlowField(uv)
+
+        assert np.all(ss.occlusion_mask(uni(8, 8, 2, 0), uni(8, 8, -2, 0))[:, :6] == 1.0)
+        assert np.all(ss.occlusion_mask(uni(8, 8, 5, 0), uni(8, 8, 0, 0)) == 0.0)
+        assert np.all(ss.occlusion_mask(ss.FlowField.zero(6, 6), ss.FlowField.zero(6, 6)) == 1)
+
+    def test_weight_hand_values(self, ss, random_frame):
+        import math
+
+        assert np.all(ss.warp_weight(random_frame, random_frame, 6.5e3, 0.3) == np.float32(0.3))
+        ref = np.full((1, 1, 1), 0.5, np.float32)
+        warped = np.full((1, 1, 1), 0.5 + math.sqrt(1e-4), np.float32)
+        assert ss.warp_weight(ref, warped, 6.5e3, 0.9)[0, 0] == pytest.approx(math.exp(-0.65),
+                                                                            rel=1e-4)
+        a = np.full((1, 1, 1), 0.2, np.float32)
+        b = np.full((1, 1, 1), 0.2 + math.sqrt(1e-4), np.float32)
+        assert ss.consistency_weight(a, b, 6.5e3, 2.0)[0, 0] == pytest.approx(
+            2.0 * math.exp(-0.65), rel=1e-4)
+
+    def test_blend_hand_values(self, ss):
+        cur = np.full((1, 1, 1), 0.5, np.float32)
+        prev = np.full((1, 1, 1), 0.3, np.float32)
+        nxt = np.full((1, 1, 1), 0.7, np.float32)
+        wp = np.full((1, 1), 0.3, np.float32)
+        wn = np.full((1, 1), 0.5, np.float32)
+        assert ss.local_blend(cur, prev, nxt, wp, wn)[0, 0, 0] == pytest.approx(0.54, abs=1e-6)
+        g = np.zeros((12, 10, 3), np.float32)
+        l = np.ones((12, 10, 3), np.float32)
+        w = np.full((12, 10), 0.3, np.float32)
+        assert ss.adaptive_blend(g, l, w)[0, 0, 0] == pytest.approx(0.7, abs=1e-6)
+
+    def test_solver_fixed_point_bitwise(self, ss, rng):
+        p = rng.random((16, 12, 3)).astype(np.float32)
+        wc = rng.uniform(0.0, 2.0, (16, 12)).astype(np.float32)
+        for iters in (1, 15, 150, 600):
+            out = ss.solve_screened_poisson(p, p, wc, ss.ConsistencyParams(iterations=iters), p)
+            assert out.tobytes() == p.tobytes()
+
+
+# ------------------------------------------------------------- golden vectors
+@pytest.mark.parametrize("tag", ["c3", "c1", "gray2d"])
+def test_backward_warp_golden_bitwise(ss, golden, tag):
+    g = golden("warp.npz")
+    field = ss.FlowField(g[f"{tag}_uv"], g[f"{tag}_valid"])
+    warped, mask = ss.backward_warp(g[f"{tag}_img"], field)
+    assert np.array_equal(warped, g[f"{tag}_warped"])
+    assert np.array_equal(mask, g[f"{tag}_mask"])
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_occlusion_golden_bitwise(ss, golden, tag):
+    g = golden("occlusion.npz")
+    m = ss.occlusion_mask(ss.FlowField(g[f"{tag}_fuv"], g[f"{tag}_fvalid"]),
+                          ss.FlowField(g[f"{tag}_buv"], g[f"{tag}_bvalid"]))
+    assert np.array_equal(m, g[f"{tag}_mask"])
+
+
+@pytest.mark.parametrize("c", [3, 1])
+def test_weights_blends_golden(ss, golden, c):
+    g = golden("weights.npz")
+    k = f"c{c}_"
+    assert ulp_close(ss.warp_weight(g[k + "ref"], g[k + "warped"], 6.5e3, 0.3, g[k + "validity"]),
+                     g[k + "wp"])
+    assert ulp_close(ss.warp_weight(g[k + "ref"], np.ascontiguousarray(g[k + "warped"][::-1]),
+                                    1.0e3, 0.5), g[k + "wn"])
+    assert np.array_equal(ss.local_blend(g[k + "ref"], g[k + "prev"], g[k + "next"], g[k + "wp"],
+                                         g[k + "wn"]), g[k + "L"])
+    assert np.array_equal(ss.adaptive_blend(g[k + "G"], g[k + "L"], g[k + "wp"]), g[k + "A"])
+    assert ulp_close(ss.consistency_weight(g[k + "ref"], g[k + "warped"], 6.5e3, 2.0), g[k + "wc"])
+    assert np.array_equal(ss.laplacian(g[k + "ref"]), g[k + "lap"])
+
+
+def _cp(ss, arr):
+    k1, k2, alpha, lam, eta, kappa, iters = arr.tolist()
+    return ss.ConsistencyParams(k1=k1, k2=k2, alpha=alpha, lam=lam, eta=eta, kappa=kappa,
+                                iterations=int(iters))
+
+
+@pytest.mark.parametrize("tag", ["default", "gray", "unscreened", "long"])
+def test_solver_golden_bitwise(ss, golden, tag):
+    g = golden("solver.npz")
+    o = ss.solve_screened_poisson(g[f"{tag}_P"], g[f"{tag}_A"], g[f"{tag}_wc"],
+                                  _cp(ss, g[f"{tag}_params"]), g[f"{tag}_A"])
+    assert np.array_equal(o, g[f"{tag}_O"])
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_solver_divergence_iteration(ss, golden, i):
+    g = golden("solver.npz")
+    with pytest.raises(ss.SolverDivergence) as err:
+        ss.solve_screened_poisson(g[f"div{i}_P"], g[f"div{i}_A"], g[f"div{i}_wc"],
+                                  ss.ConsistencyParams(iterations=int(g[f"div{i}_iters"])),
+                                  g[f"div{i}_A"])
+    assert err.value.iteration == int(g[f"div{i}_iteration"])
+
+
+@pytest.mark.parametrize("tag", ["int", "subpix", "dis", "gray", "two", "sched"])
+def test_stream_golden(ss, golden, tag):
+    g = golden("streams.npz")
+    inputs, processed, outputs, flows, params = stream_case(g, tag)
+    n = len(inputs)
+    provider = ss.ReplayFlow(flows)
+    if params is None:
+        got = dict(ss.stabilize_stream(zip(inputs, processed), ss.preset("default"), provider))
+    else:
+        state = ss.SessionState(params=_cp(ss, params[0]))
+        got = {}
+        for pos in range(1, n + 1):
+            state.push_pair(pos, inputs[pos - 1], processed[pos - 1])
+            if pos == 1:
+                got[1] = state.prev_output
+            elif pos >= 3:
+                state.params = _cp(ss, params[pos - 2])
+                got[pos - 1] = ss.stabilize_step(state, provider)
+        state.params = _cp(ss, params[n - 1])
+        got[n] = ss.stream_end_step(state, provider)
+    assert sorted(got) == list(range(1, n + 1))
+    assert np.array_equal(got[1], outputs[1])
+    worst = max(float(np.abs(got[t] - outputs[t]).max()) for t in got)
+    assert worst <= OUT_TOL, worst
+    if tag in ("int", "gray", "two"):
+        # integer flows: exp never differs -> bit-identical to the reference
+        for t in got:
+            assert np.array_equal(got[t], outputs[t]), t
+
+
+def test_constant_flow_provider_on_device(ss, golden):
+    """ConstantFlow fills the flow slots on device; same outputs as replay."""
+    g = golden("streams.npz")
+    inputs, processed, outputs, _, _ = stream_case(g, "subpix")
+    got = dict(ss.stabilize_stream(zip(inputs, processed), ss.preset("default"),
+                                   ss.ConstantFlow(2.37, 1.13)))
+    assert max(float(np.abs(got[t] - outputs[t]).max()) for t in got) <= OUT_TOL
+
+
+# -------------------------------------------------------------- session logic
+class TestSession:
+    def test_step_errors(self, ss):
+        state = ss.SessionState(params=ss.preset("default"))
+        f = np.random.default_rng(0).random((16, 16, 3)).astype(np.float32)
+        flow = ss.ConstantFlow(0, 0)
+        with pytest.raises(ValueError, match="no buffered"):
+            ss.stabilize_step(state, flow)
+        state.push_pair(1, f, f)
+        state.push_pair(2, f, f)
+        with pytest.raises(ValueError, match="missing next"):
+            ss.stabilize_step(state, flow)
+        state.push_pair(3, f, f)
+        with pytest.raises(ValueError, match="next frame is available"):
+            ss.stream_end_step(state, flow)
+        ss.stabilize_step(state, flow)
+        ss.stream_end_step(state, flow)
+        assert state.solved_through == 3
+
+    def test_resolution_drift_and_positions(self, ss):
+        rng = np.random.default_rng(0)
+        state = ss.SessionState(params=ss.preset("default"))
+        state.push_pair(1, rng.random((8, 8, 3)), rng.random((8, 8, 3)))
+        with pytest.raises(ss.ResolutionMismatch):
+            state.push_pair(2, rng.random((9, 8, 3)), rng.random((9, 8, 3)))
+        with pytest.raises(ValueError, match="non-consecutive"):
+            state.push_pair(3, rng.random((8, 8, 3)), rng.random((8, 8, 3)))
+        with pytest.raises(ss.ResolutionMismatch):
+            state.push_pair(2, rng.random((8, 8, 3)), rng.random((8, 9, 3)))
+
+    def test_first_frame_is_processed_object(self, ss):
+        f = np.random.default_rng(5).random((24, 20, 3)).astype(np.float32)
+        out = list(ss.stabilize_stream(iter([(f, f * 0.5)]), ss.preset("default"),
+                                       ss.ConstantFlow(0, 0)))
+        assert len(out) == 1 and np.array_equal(out[0][1], f * 0.5)
+
+    def test_divergence_does_not_advance(self, ss):
+        rng = np.random.default_rng(1)
+        state = ss.SessionState(params=ss.ConsistencyParams(eta=0.9999, lam=1e6, alpha=0.0,
+                                                            iterations=300, k1=0.1, k2=0.1))
+        frames = [rng.random((12, 12, 3)).astype(np.float32) for _ in range(3)]
+        for i, f in enumerate(frames, 1):
+            state.push_pair(i, f, frames[(i + 1) % 3])
+        before = state.prev_output.copy()
+        with pytest.raises(ss.SolverDivergence) as err:
+            ss.stabilize_step(state, ss.ConstantFlow(0.5, 0))
+        assert err.value.iteration >= 1
+        assert state.solved_through == 1
+        assert np.array_equal(state.prev_output, before)
+        # the oracle reports the same iteration
+        p = state.params
+        with pytest.raises(orc.OracleDivergence) as e2:
+            orc.run_step(frames[0], frames[2], frames[1], frames[0], frames[2], frames[1],
+                         frames[2], orc.constant_flow(12, 12, 0.5, 0, -1),
+                         orc.constant_flow(12, 12, 0.5, 0, 1),
+                         orc.Params(k1=p.k1, k2=p.k2, alpha=p.alpha, lam=p.lam, eta=p.eta,
+                                    kappa=p.kappa, iterations=p.iterations))
+        assert e2.value.iteration == err.value.iteration
+
+
+# ------------------------------------------------------- larger sizes / props
+@pytest.mark.parametrize("shape", [(37, 301, 3), (129, 250, 1), (200, 113, 3), (5, 7, 3)])
+def test_solver_matches_oracle_bitwise_odd_shapes(ss, shape):
+    """Blocked tiles, image borders inside strips/pairs, partial tiles."""
+    rng = np.random.default_rng(sum(shape))
+    p = rng.random(shape).astype(np.float32)
+    a = rng.random(shape).astype(np.float32)
+    wc = rng.uniform(0, 2, shape[:2]).astype(np.float32)
+    for iters in (1, 7, 8, 9, 150):
+        prm = ss.ConsistencyParams(iterations=iters)
+        got = ss.solve_screened_poisson(p, a, wc, prm, a)
+        want = orc.solve_screened_poisson(p, a, wc, orc.Params(iterations=iters))
+        assert np.array_equal(got, want), (shape, iters)
+
+
+def test_step_720p_matches_oracle(ss):
+    from paper_2301_00750_b200 import synthetic
+
+    seq = synthetic.translating_sequence(frames=3, height=720, width=1280, step=(2, 1), seed=11)
+    flow = ss.ConstantFlow(2.37, 1.13)
+    got = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"), flow))
+
+    def flow_fn(a, fa, b, fb):
+        f = flow.flow_between(a, fa, b, fb)
+        return f.uv, f.valid
+
+    want = dict(orc.stabilize_stream(seq.inputs, seq.processed, orc.Params(), flow_fn))
+    for t in want:
+        assert float(np.abs(got[t] - want[t]).max()) <= OUT_TOL, t
+
+
+def test_1080p_fixed_point_and_range(ss):
+    """Size-independent properties at the benchmark resolution: A = P = init is
+    a bitwise fixed point; outputs stay in [0, 1]."""
+    torch = pytest.importorskip("torch")
+    g = torch.Generator(device="cuda").manual_seed(0)
+    p = torch.rand((1080, 1920, 3), device="cuda", generator=g)
+    wc = torch.rand((1080, 1920), device="cuda", generator=g) * 2
+    out = ss.solve_screened_poisson(p, p, wc, ss.ConsistencyParams(), p)
+    assert torch.equal(out, p)
+    a = torch.rand((1080, 1920, 3), device="cuda", generator=g)
+    out = ss.solve_screened_poisson(p, a, wc, ss.ConsistencyParams(), a)
+    assert float(out.min()) >= 0.0 and float(out.max()) <= 1.0
