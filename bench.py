@@ -350,7 +350,7 @@ def run_e2e(args, L, state, seq, torch, dist):
         host_p.append(p.cpu().pin_memory())
     out = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
     sess = state.handle
-    pos = [int(L.ss_solved_through(sess)) + 2]
+    pos = [int(L.ss_solved_through(sess)) + 1]  # last pushed position
 
     def step(k):
         pos[0] += 1

@@ -75,6 +75,8 @@ def to_dev(x, dtype=None):
     if is_torch(x):
         return x.to(device=dev, dtype=dtype).contiguous()
     arr = np.ascontiguousarray(x)
+    if not arr.flags.writeable:
+        arr = arr.copy()
     return t.from_numpy(arr).to(device=dev, dtype=dtype, non_blocking=False).contiguous()
 
 

@@ -109,9 +109,6 @@ static int session_alloc(ss_session *s)
     SS_CUDA_TRY(cudaMalloc(&s->lapP, px * s->cp * sizeof(float)));
     SS_CUDA_TRY(cudaMalloc(&s->wc, px * sizeof(float)));
     for (auto &e : s->ev) SS_CUDA_TRY(cudaEventCreate(&e));
-    s->solver.h = s->h;
-    s->solver.w = s->w;
-    s->solver.c = s->cp;
     return s->solver.ensure(s->h, s->w, s->cp, 150) == SS_OK ? SS_OK : SS_NO_MEMORY;
 }
 
@@ -305,7 +302,6 @@ int ss_solve_screened_poisson(const float *processed, const float *target, const
     SS_CUDA_TRY(cudaMalloc(&tA.p, n * sizeof(float)));
     SS_CUDA_TRY(cudaMalloc(&tL.p, n * sizeof(float)));
     if (init && init != target) SS_CUDA_TRY(cudaMalloc(&tI.p, n * sizeof(float)));
-    wk.h = h; wk.w = w; wk.c = c;
     if (int rc = wk.ensure(h, w, c, p->iterations)) return rc;
     if (int rc = launch_hwc_to_planar(target, h, w, c, tA.p, st)) return rc;
     if (int rc = launch_laplacian(processed, h, w, c, tL.p, true, st)) return rc;

@@ -246,7 +246,10 @@ __global__ void __launch_bounds__(blk::THREADS, 1) k_sgd_blocked(BlockedArgs a)
     // row/column (-1, RH / RW) bounds the region edges
     const int lo_r = max(-ry0, -1), hi_r = min(h - 1 - ry0, RH);
     const int lo_c = max(-rx0, -1), hi_c = min(w - 1 - rx0, RW);
-    const bool fast = gx0 >= 1 && gx0 + 2 <= w - 1 && gy0 >= 1 && gy0 + R <= h - 1;
+    // the fast path must be warp-uniform: __syncthreads (bar.sync.aligned)
+    // inside blk_run must be reached at the same PC by every lane of a warp
+    const bool fast = __all_sync(0xffffffffu, gx0 >= 1 && gx0 + 2 <= w - 1 && gy0 >= 1 &&
+                                                  gy0 + R <= h - 1);
     float mx = 0.0f;
     if (fast)
         blk_run<true>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters, a.eta,
@@ -456,7 +459,7 @@ SolverWork::~SolverWork()
 
 int SolverWork::ensure(int h_, int w_, int c_, int iterations)
 {
-    if (h_ != h || w_ != w || c_ != c) {
+    if (h_ != h || w_ != w || c_ != c || O[0][0] == nullptr) {
         for (auto &s : O)
             for (auto &b : s) {
                 cudaFree(b);
