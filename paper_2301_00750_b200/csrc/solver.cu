@@ -25,6 +25,9 @@
 #include <cstring>
 #include <string>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ss_common.cuh"
 #include "ss_internal.h"
 
@@ -74,21 +77,23 @@ __global__ void k_planar_clamp_to_hwc(const float *__restrict__ src, long hw,
 }
 
 // ---------------------------------------------------------------------------
-// temporally blocked kernel
+// temporally blocked kernels
 namespace blk {
-constexpr int K = 8;          // iterations per pass (= halo width)
 constexpr int R = 8;          // rows per thread
 constexpr int PAIRS = 64;     // column pairs per region row -> RW = 128
 constexpr int STRIPS = 8;     // row strips -> RH = 64
 constexpr int RW = 2 * PAIRS;
 constexpr int RH = R * STRIPS;
-constexpr int OW = RW - 2 * K;  // interior tile
-constexpr int OH = RH - 2 * K;
-constexpr int SW = RW + 4;      // smem row pitch: 2 padding columns each side
-constexpr int SH = RH + 2;      // 1 padding row each side
 constexpr int THREADS = PAIRS * STRIPS;
+// smem O buffers: region (rr, cc) lives at (rr + 1) * pitch + cc + 2
+constexpr int SW = RW + 4;      // LDG kernel: 2 padding columns each side, 1 row each side
+constexpr int SH = RH + 2;
 constexpr size_t SMEM = 2ull * SH * SW * sizeof(float);
-static_assert(K % R == 0 && K % 2 == 0, "halo must align with strips and pairs");
+constexpr int SW2 = RW + 2;     // TMA kernel: 2 left padding columns, 1 top row; the
+constexpr int SH2 = RH + 1;     // right / bottom neighbours of the region edge read the
+                                // next row / next buffer (finite halo garbage)
+constexpr int STAGE = RH * RW;  // one staged array (TMA box 128 x 64 floats)
+constexpr size_t SMEM_TMA = (5ull * STAGE + 2ull * SH2 * SW2 + SW2) * sizeof(float) + 16;
 }  // namespace blk
 
 struct BlockedArgs {
@@ -102,12 +107,16 @@ struct BlockedArgs {
     unsigned *maxbits;        // this pass's slot
 };
 
+// One SGD-momentum update (consistency.py:282-291).  The first Laplacian step
+// fmul(o, -4) + N is fused: o * -4 is exact (power-of-two scale) unless it
+// overflows, which only happens far inside the grey zone, where the exact
+// replay (k_sgd_iter, no fusion) takes over -- so the fused form is bitwise
+// identical on every output the blocked path commits.
 __device__ __forceinline__ float sgd_update(float o, float op, float N, float S, float W,
                                             float E, float lp, float a, float wcv, float eta,
                                             float kappa)
 {
-    float g = fmul(o, -4.0f);
-    g = fadd(g, N);
+    float g = __fmaf_rn(o, -4.0f, N);
     g = fadd(g, S);
     g = fadd(g, W);
     g = fadd(g, E);
@@ -124,7 +133,7 @@ __device__ __forceinline__ float sgd_update(float o, float op, float N, float S,
 // One iteration for one thread's 2 x R block.  X holds the current iterate,
 // Y the previous one; Y is overwritten with the new iterate (the caller swaps
 // roles).  Reads neighbours from smem buffer `cur`, writes new values to `nxt`.
-template <bool FAST>
+template <bool FAST, int P>
 __device__ __forceinline__ void blk_iter(float (&X)[blk::R][2], float (&Y)[blk::R][2],
                                          const float (&Av)[blk::R][2],
                                          const float (&Lv)[blk::R][2],
@@ -133,16 +142,15 @@ __device__ __forceinline__ void blk_iter(float (&X)[blk::R][2], float (&Y)[blk::
                                          int lo_c, int hi_c, float eta, float kappa, float &mx)
 {
     using namespace blk;
-    // smem index of region (rr, cc): (rr + 1) * SW + (cc + 2)
     if (FAST) {
         float wv[R], ev[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            wv[r] = cur[(r0 + r + 1) * SW + c0 + 1];
-            ev[r] = cur[(r0 + r + 1) * SW + c0 + 4];
+            wv[r] = cur[(r0 + r + 1) * P + c0 + 1];
+            ev[r] = cur[(r0 + r + 1) * P + c0 + 4];
         }
-        const float2 nv = *reinterpret_cast<const float2 *>(cur + r0 * SW + c0 + 2);
-        const float2 sv = *reinterpret_cast<const float2 *>(cur + (r0 + R + 1) * SW + c0 + 2);
+        const float2 nv = *reinterpret_cast<const float2 *>(cur + r0 * P + c0 + 2);
+        const float2 sv = *reinterpret_cast<const float2 *>(cur + (r0 + R + 1) * P + c0 + 2);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const float n0 = r == 0 ? nv.x : X[r - 1][0];
@@ -166,10 +174,10 @@ __device__ __forceinline__ void blk_iter(float (&X)[blk::R][2], float (&Y)[blk::
             for (int k = 0; k < 2; ++k) {
                 const int cc = c0 + k;
                 const int wcl = max(cc - 1, lo_c), ecl = min(cc + 1, hi_c);
-                const float N = cur[(nr + 1) * SW + cc + 2];
-                const float S = cur[(sr + 1) * SW + cc + 2];
-                const float Wn = cur[(rr + 1) * SW + wcl + 2];
-                const float En = cur[(rr + 1) * SW + ecl + 2];
+                const float N = cur[(nr + 1) * P + cc + 2];
+                const float S = cur[(sr + 1) * P + cc + 2];
+                const float Wn = cur[(rr + 1) * P + wcl + 2];
+                const float En = cur[(rr + 1) * P + ecl + 2];
                 const float u = sgd_update(X[r][k], Y[r][k], N, S, Wn, En, Lv[r][k], Av[r][k],
                                            Wv[r][k], eta, kappa);
                 Y[r][k] = u;
@@ -179,10 +187,10 @@ __device__ __forceinline__ void blk_iter(float (&X)[blk::R][2], float (&Y)[blk::
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
-        *reinterpret_cast<float2 *>(nxt + (r0 + r + 1) * SW + c0 + 2) = make_float2(Y[r][0], Y[r][1]);
+        *reinterpret_cast<float2 *>(nxt + (r0 + r + 1) * P + c0 + 2) = make_float2(Y[r][0], Y[r][1]);
 }
 
-template <bool FAST>
+template <bool FAST, int P>
 __device__ __forceinline__ void blk_run(float (&X)[blk::R][2], float (&Y)[blk::R][2],
                                         const float (&Av)[blk::R][2],
                                         const float (&Lv)[blk::R][2],
@@ -192,15 +200,84 @@ __device__ __forceinline__ void blk_run(float (&X)[blk::R][2], float (&Y)[blk::R
 {
     // iterations alternate roles: even -> (X cur, Y prev) read sm0 write sm1
     for (int it = 0; it < iters; it += 2) {
-        blk_iter<FAST>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, eta, kappa, mx);
+        blk_iter<FAST, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, eta, kappa,
+                          mx);
         __syncthreads();
         if (it + 1 < iters) {
-            blk_iter<FAST>(Y, X, Av, Lv, Wv, sm1, sm0, r0, c0, lo_r, hi_r, lo_c, hi_c, eta,
-                           kappa, mx);
+            blk_iter<FAST, P>(Y, X, Av, Lv, Wv, sm1, sm0, r0, c0, lo_r, hi_r, lo_c, hi_c, eta,
+                              kappa, mx);
             __syncthreads();
         }
     }
 }
+
+// run one region's iterations (fast or edge path, warp-uniform) and write the
+// interior back; returns the max-bits contribution of this thread
+template <int P>
+__device__ __forceinline__ unsigned blk_tile(float (&X)[blk::R][2], float (&Y)[blk::R][2],
+                                             const float (&Av)[blk::R][2],
+                                             const float (&Lv)[blk::R][2],
+                                             const float (&Wv)[blk::R][2], float *sm0, float *sm1,
+                                             const BlockedArgs &a, int K, int rx0, int ry0, int ch)
+{
+    using namespace blk;
+    const int p = threadIdx.x, s = threadIdx.y;
+    const int c0 = 2 * p, r0 = s * R;
+    const int h = a.h, w = a.w;
+    const long plane = (long)ch * h * w;
+    const int gx0 = rx0 + c0, gy0 = ry0 + r0;
+    // clamp ranges (region coords) for the replicate boundary; the padding
+    // row/column (-1, RH / RW) bounds the region edges
+    const int lo_r = max(-ry0, -1), hi_r = min(h - 1 - ry0, RH);
+    const int lo_c = max(-rx0, -1), hi_c = min(w - 1 - rx0, RW);
+    // the fast path must be warp-uniform: __syncthreads (bar.sync.aligned)
+    // inside blk_run must be reached at the same PC by every lane of a warp
+    const bool fast = __all_sync(0xffffffffu, gx0 >= 1 && gx0 + 2 <= w - 1 && gy0 >= 1 &&
+                                                  gy0 + R <= h - 1);
+    float mx = 0.0f;
+    if (fast)
+        blk_run<true, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters,
+                         a.eta, a.kappa, mx);
+    else
+        blk_run<false, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters,
+                          a.eta, a.kappa, mx);
+
+    // after an odd number of iterations the current iterate lives in Y
+    const bool odd = a.iters & 1;
+    const bool interior_c = c0 >= K && c0 + 2 <= RW - K;
+    bool nan_seen = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int gy = gy0 + r;
+        const bool interior_r = r0 + r >= K && r0 + r < RH - K;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const float o = odd ? Y[r][k] : X[r][k];
+            const float op = odd ? X[r][k] : Y[r][k];
+            nan_seen |= (o != o);
+            const int gx = gx0 + k;
+            if (interior_r && interior_c && gy < h && gx < w) {
+                const long q = (long)gy * w + gx;
+                if (a.hwc_out) {
+                    a.hwc_out[q * a.c + ch] = fminf(fmaxf(o, 0.0f), 1.0f);
+                } else {
+                    a.Oout[plane + q] = o;
+                    a.Oprev_out[plane + q] = op;
+                }
+            }
+        }
+    }
+    return nan_seen ? 0x7fffffffu : __float_as_uint(mx);
+}
+
+__device__ __forceinline__ void push_maxbits(unsigned bits, unsigned *slot)
+{
+    bits = __reduce_max_sync(0xffffffffu, bits);
+    if ((threadIdx.x & 31) == 0 && bits > *(volatile unsigned *)slot) atomicMax(slot, bits);
+}
+
+// LDG variant (any width): one region per CTA, K = 8.
+constexpr int K_LDG = 8;
 
 __global__ void __launch_bounds__(blk::THREADS, 1) k_sgd_blocked(BlockedArgs a)
 {
@@ -208,14 +285,13 @@ __global__ void __launch_bounds__(blk::THREADS, 1) k_sgd_blocked(BlockedArgs a)
     extern __shared__ float4 smem_raw[];
     float *sm0 = reinterpret_cast<float *>(smem_raw);
     float *sm1 = sm0 + SH * SW;
-
+    constexpr int K = K_LDG;
     const int p = threadIdx.x, s = threadIdx.y;
     const int ch = blockIdx.z;
-    const int rx0 = blockIdx.x * OW - K, ry0 = blockIdx.y * OH - K;
-    const int c0 = 2 * p, r0 = s * R;  // region coords of this thread's block
+    const int rx0 = blockIdx.x * (RW - 2 * K) - K, ry0 = blockIdx.y * (RH - 2 * K) - K;
+    const int c0 = 2 * p, r0 = s * R;
     const int h = a.h, w = a.w;
-    const long hw = (long)h * w;
-    const long plane = (long)ch * hw;
+    const long plane = (long)ch * h * w;
 
     // zero both buffers (padding must be finite; interior is overwritten)
     for (int i = threadIdx.y * PAIRS + threadIdx.x; i < 2 * SH * SW; i += THREADS) sm0[i] = 0.0f;
@@ -241,51 +317,197 @@ __global__ void __launch_bounds__(blk::THREADS, 1) k_sgd_blocked(BlockedArgs a)
     for (int r = 0; r < R; ++r)
         *reinterpret_cast<float2 *>(sm0 + (r0 + r + 1) * SW + c0 + 2) = make_float2(X[r][0], X[r][1]);
     __syncthreads();
+    const unsigned bits = blk_tile<SW>(X, Y, Av, Lv, Wv, sm0, sm1, a, K, rx0, ry0, ch);
+    push_maxbits(bits, a.maxbits);
+}
 
-    // clamp ranges (region coords) for the replicate boundary; the padding
-    // row/column (-1, RH / RW) bounds the region edges
-    const int lo_r = max(-ry0, -1), hi_r = min(h - 1 - ry0, RH);
-    const int lo_c = max(-rx0, -1), hi_c = min(w - 1 - rx0, RW);
-    // the fast path must be warp-uniform: __syncthreads (bar.sync.aligned)
-    // inside blk_run must be reached at the same PC by every lane of a warp
-    const bool fast = __all_sync(0xffffffffu, gx0 >= 1 && gx0 + 2 <= w - 1 && gy0 >= 1 &&
-                                                  gy0 + R <= h - 1);
-    float mx = 0.0f;
-    if (fast)
-        blk_run<true>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters, a.eta,
-                      a.kappa, mx);
-    else
-        blk_run<false>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters,
-                       a.eta, a.kappa, mx);
+// ---------------------------------------------------------------------------
+// TMA variant: persistent CTAs (one per SM) walk the tile list; while a tile
+// iterates, the next tile's five input boxes (O, O_prev, A, lapP planes and
+// wc) stream into shared memory through cp.async.bulk.tensor + mbarrier, so
+// the global-load latency is off the critical path.  Requires w % 4 == 0
+// (16-byte row pitch for the tensor maps).
+struct TmaMaps {
+    CUtensorMap O, Op, A, L, W;  // 3-D (w, h, c) planes; W is 2-D (w, h)
+};
 
-    // after an odd number of iterations the current iterate lives in Y
-    const bool odd = a.iters & 1;
-    const bool interior_r = r0 >= K && r0 + R <= RH - K;
-    const bool interior_c = c0 >= K && c0 + 2 <= RW - K;
-    bool nan_seen = false;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int gy = gy0 + r;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const float o = odd ? Y[r][k] : X[r][k];
-            const float op = odd ? X[r][k] : Y[r][k];
-            nan_seen |= (o != o);
-            const int gx = gx0 + k;
-            if (interior_r && interior_c && gy < h && gx < w) {
-                const long q = (long)gy * w + gx;
-                if (a.hwc_out) {
-                    a.hwc_out[q * a.c + ch] = fminf(fmaxf(o, 0.0f), 1.0f);
-                } else {
-                    a.Oout[plane + q] = o;
-                    a.Oprev_out[plane + q] = op;
-                }
-            }
-        }
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
+{
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
     }
-    unsigned bits = nan_seen ? 0x7fffffffu : __float_as_uint(mx);
-    bits = __reduce_max_sync(0xffffffffu, bits);
-    if ((threadIdx.x & 31) == 0 && bits > *(volatile unsigned *)a.maxbits) atomicMax(a.maxbits, bits);
+}
+
+__device__ __forceinline__ void tma_load_3d(float *dst, const CUtensorMap *map, int x, int y, int z,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];"
+        :
+        : "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z),
+          "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(float *dst, const CUtensorMap *map, int x, int y,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];"
+        :
+        : "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
+          "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(blk::THREADS, 1)
+    k_sgd_tma(const __grid_constant__ TmaMaps maps, BlockedArgs a)
+{
+    using namespace blk;
+    constexpr int OW = RW - 2 * K, OH = RH - 2 * K;
+    extern __shared__ __align__(1024) float smem_tma[];
+    float *stage = smem_tma;                       // 5 x (RH x RW), 128-byte aligned
+    float *sm0 = stage + 5 * STAGE;                // O buffers
+    float *sm1 = sm0 + SH2 * SW2;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm1 + SH2 * SW2 + SW2);
+    const int tid = threadIdx.y * PAIRS + threadIdx.x;
+    const int ntx = (a.w + OW - 1) / OW, nty = (a.h + OH - 1) / OH;
+    const int ntiles = ntx * nty * a.c;
+
+    auto issue = [&](int t) {
+        const int ch = t / (ntx * nty), rem = t - ch * ntx * nty;
+        const int ty = rem / ntx, tx = rem - ty * ntx;
+        const int x = tx * OW - K, y = ty * OH - K;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :
+                     : "r"(smem_u32(bar)), "r"((uint32_t)(5 * STAGE * sizeof(float)))
+                     : "memory");
+        tma_load_3d(stage + 0 * STAGE, &maps.O, x, y, ch, bar);
+        tma_load_3d(stage + 1 * STAGE, &maps.Op, x, y, ch, bar);
+        tma_load_3d(stage + 2 * STAGE, &maps.A, x, y, ch, bar);
+        tma_load_3d(stage + 3 * STAGE, &maps.L, x, y, ch, bar);
+        tma_load_2d(stage + 4 * STAGE, &maps.W, x, y, bar);
+    };
+
+    // zero the O buffers once (pads stay finite), init the barrier
+    for (int i = tid; i < 2 * SH2 * SW2 + SW2; i += THREADS) sm0[i] = 0.0f;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if ((int)blockIdx.x < ntiles) issue(blockIdx.x);
+    }
+    __syncthreads();
+
+    const int p = threadIdx.x, s = threadIdx.y;
+    const int c0 = 2 * p, r0 = s * R;
+    uint32_t phase = 0;
+    unsigned bits_all = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int ch = t / (ntx * nty), rem = t - ch * ntx * nty;
+        const int ty = rem / ntx, tx = rem - ty * ntx;
+        const int rx0 = tx * OW - K, ry0 = ty * OH - K;
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        float X[R][2], Y[R][2], Av[R][2], Lv[R][2], Wv[R][2];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int o = (r0 + r) * RW + c0;
+            const float2 x2 = *reinterpret_cast<const float2 *>(stage + 0 * STAGE + o);
+            const float2 y2 = *reinterpret_cast<const float2 *>(stage + 1 * STAGE + o);
+            const float2 a2 = *reinterpret_cast<const float2 *>(stage + 2 * STAGE + o);
+            const float2 l2 = *reinterpret_cast<const float2 *>(stage + 3 * STAGE + o);
+            const float2 w2 = *reinterpret_cast<const float2 *>(stage + 4 * STAGE + o);
+            X[r][0] = x2.x; X[r][1] = x2.y;
+            Y[r][0] = y2.x; Y[r][1] = y2.y;
+            Av[r][0] = a2.x; Av[r][1] = a2.y;
+            Lv[r][0] = l2.x; Lv[r][1] = l2.y;
+            Wv[r][0] = w2.x; Wv[r][1] = w2.y;
+            *reinterpret_cast<float2 *>(sm0 + (r0 + r + 1) * SW2 + c0 + 2) = x2;
+        }
+        __syncthreads();  // stage consumed, sm0 holds O
+        if (tid == 0 && t + (int)gridDim.x < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(t + gridDim.x);
+        }
+        bits_all = max(bits_all, blk_tile<SW2>(X, Y, Av, Lv, Wv, sm0, sm1, a, K, rx0, ry0, ch));
+    }
+    push_maxbits(bits_all, a.maxbits);
+}
+
+template <int K>
+static int launch_tma(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
+{
+    static bool attr = false;
+    if (!attr) {
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)blk::SMEM_TMA));
+        attr = true;
+    }
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        SS_CUDA_TRY(cudaGetDevice(&dev));
+        SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    constexpr int OW = blk::RW - 2 * K, OH = blk::RH - 2 * K;
+    const int ntiles = ((a.w + OW - 1) / OW) * ((a.h + OH - 1) / OH) * a.c;
+    const int grid = std::min(ntiles, n_sm);
+    k_sgd_tma<K><<<grid, dim3(blk::PAIRS, blk::STRIPS), blk::SMEM_TMA, st>>>(maps, a);
+    SS_LAUNCH_CHECK("k_sgd_tma");
+    return SS_OK;
+}
+
+// tensor maps over planar (c, h, w) float32 arrays (cuTensorMapEncodeTiled
+// through the runtime's driver entry point; no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+static int make_map(CUtensorMap *m, const float *base, int w, int h, int c, bool planes)
+{
+    auto fn = encode_fn();
+    if (!fn) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return SS_CUDA_ERROR;
+    }
+    const cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)c};
+    const cuuint64_t strides[2] = {(cuuint64_t)w * 4, (cuuint64_t)w * h * 4};
+    const cuuint32_t box[3] = {blk::RW, blk::RH, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, planes ? 3 : 2,
+                          const_cast<float *>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        return SS_CUDA_ERROR;
+    }
+    return SS_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -488,12 +710,25 @@ int SolverWork::ensure(int h_, int w_, int c_, int iterations)
 
 int solver_variant()
 {
+    // 0 = streaming (one iteration per launch), 1 = blocked LDG, 2 = blocked TMA
     static int v = [] {
         const char *e = getenv("SS_SOLVER");
         if (e && !strcmp(e, "stream")) return 0;
-        return 1;
+        if (e && !strcmp(e, "ldg")) return 1;
+        return 2;
     }();
     return v;
+}
+
+static int tma_k()
+{
+    static int k = [] {
+        const char *e = getenv("SS_SOLVER_K");
+        // the TMA box origin (tx * OW - K) must be 16-byte aligned: K % 4 == 0
+        const int v = e ? atoi(e) : 8;
+        return (v == 4 || v == 8) ? v : 8;
+    }();
+    return k;
 }
 
 static int run_streaming(SolverWork &wk, const float *A, const float *init, const float *lapP,
@@ -552,17 +787,38 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
     if (!init) init = A;
     const long hw = (long)wk.h * wk.w;
     const long n = hw * wk.c;
-    const int n_pass = solver_variant() == 1 ? (iters + blk::K - 1) / blk::K : 0;
+    int variant = solver_variant();
+    if (variant == 2 && (wk.w % 4 != 0 || !encode_fn())) variant = 1;
+    const int K = variant == 2 ? tma_k() : K_LDG;
+    const int n_pass = variant ? (iters + K - 1) / K : 0;
 
-    if (solver_variant() == 1) {
-        static bool attr = false;
-        if (!attr) {
-            SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)blk::SMEM));
-            attr = true;
-        }
+    if (variant) {
         SS_CUDA_TRY(cudaMemsetAsync(wk.maxbits, 0, (size_t)n_pass * sizeof(unsigned), st));
-        const dim3 grid((wk.w + blk::OW - 1) / blk::OW, (wk.h + blk::OH - 1) / blk::OH, wk.c);
+        TmaMaps m_init, m_set[2];
+        if (variant == 2) {
+            TmaMaps base;
+            if ((rc = make_map(&base.A, A, wk.w, wk.h, wk.c, true))) return rc;
+            if ((rc = make_map(&base.L, lapP, wk.w, wk.h, wk.c, true))) return rc;
+            if ((rc = make_map(&base.W, wc, wk.w, wk.h, 1, false))) return rc;
+            m_init = base;
+            if ((rc = make_map(&m_init.O, init, wk.w, wk.h, wk.c, true))) return rc;
+            m_init.Op = m_init.O;
+            for (int k = 0; k < 2; ++k) {
+                m_set[k] = base;
+                if ((rc = make_map(&m_set[k].O, wk.O[k][0], wk.w, wk.h, wk.c, true))) return rc;
+                if ((rc = make_map(&m_set[k].Op, wk.O[k][1], wk.w, wk.h, wk.c, true))) return rc;
+            }
+        } else {
+            static bool attr = false;
+            if (!attr) {
+                SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_blocked,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)blk::SMEM));
+                attr = true;
+            }
+        }
+        constexpr int OWL = blk::RW - 2 * K_LDG, OHL = blk::RH - 2 * K_LDG;
+        const dim3 grid((wk.w + OWL - 1) / OWL, (wk.h + OHL - 1) / OHL, wk.c);
         const dim3 block(blk::PAIRS, blk::STRIPS);
         const float *src_o = init, *src_op = init;
         int set = 0;
@@ -577,12 +833,19 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
             a.Oprev_out = wk.O[set][1];
             a.hwc_out = ps == n_pass - 1 ? out_hwc : nullptr;
             a.h = wk.h; a.w = wk.w; a.c = wk.c;
-            a.iters = std::min(blk::K, iters - ps * blk::K);
+            a.iters = std::min(K, iters - ps * K);
             a.eta = p.eta;
             a.kappa = p.kappa;
             a.maxbits = wk.maxbits + ps;
-            k_sgd_blocked<<<grid, block, blk::SMEM, st>>>(a);
-            SS_LAUNCH_CHECK("k_sgd_blocked");
+            if (variant == 2) {
+                const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];
+                if (K == 4) rc = launch_tma<4>(mp, a, st);
+                else rc = launch_tma<8>(mp, a, st);
+                if (rc) return rc;
+            } else {
+                k_sgd_blocked<<<grid, block, blk::SMEM, st>>>(a);
+                SS_LAUNCH_CHECK("k_sgd_blocked");
+            }
             src_o = wk.O[set][0];
             src_op = wk.O[set][1];
             set ^= 1;
@@ -602,7 +865,7 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
     unsigned thr_bits;
     std::memcpy(&thr_bits, &thr, sizeof thr_bits);
     int first_grey_pass = -1;
-    if (solver_variant() == 1) {
+    if (variant) {
         hb.resize(n_pass);
         SS_CUDA_TRY(cudaMemcpyAsync(hb.data(), wk.maxbits, n_pass * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         SS_CUDA_TRY(cudaStreamSynchronize(st));
@@ -619,7 +882,7 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
     // exact replay with numpy's pairwise sum from the first grey iteration
     rc = wk.plan.build(hw, wk.c);
     if (rc) return rc;
-    const int from_iter = solver_variant() == 1 ? first_grey_pass * blk::K : 0;
+    const int from_iter = variant ? first_grey_pass * K : 0;
     float *fin = nullptr;
     rc = run_streaming(wk, A, init, lapP, wc, p, iters, wk.sums, from_iter, &fin, st);
     if (rc) return rc;

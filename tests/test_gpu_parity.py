@@ -264,7 +264,8 @@ class TestSession:
 
 
 # ------------------------------------------------------- larger sizes / props
-@pytest.mark.parametrize("shape", [(37, 301, 3), (129, 250, 1), (200, 113, 3), (5, 7, 3)])
+@pytest.mark.parametrize("shape", [(37, 301, 3), (129, 250, 1), (200, 113, 3), (5, 7, 3),
+                                   (37, 300, 3), (130, 256, 1), (201, 116, 3), (8, 4, 3)])
 def test_solver_matches_oracle_bitwise_odd_shapes(ss, shape):
     """Blocked tiles, image borders inside strips/pairs, partial tiles."""
     rng = np.random.default_rng(sum(shape))
@@ -306,3 +307,36 @@ def test_1080p_fixed_point_and_range(ss):
     a = torch.rand((1080, 1920, 3), device="cuda", generator=g)
     out = ss.solve_screened_poisson(p, a, wc, ss.ConsistencyParams(), a)
     assert float(out.min()) >= 0.0 and float(out.max()) <= 1.0
+
+
+VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/oracle']
+import oracle as orc, paper_2301_00750_b200 as ss
+for shape in [(61, 200, 3), (130, 124, 1), (47, 301, 3)]:
+    r = np.random.default_rng(sum(shape))
+    p = r.random(shape).astype(np.float32); a = r.random(shape).astype(np.float32)
+    wc = r.uniform(0, 2, shape[:2]).astype(np.float32)
+    for it in (1, 5, 150):
+        got = ss.solve_screened_poisson(p, a, wc, ss.ConsistencyParams(iterations=it), a)
+        want = orc.solve_screened_poisson(p, a, wc, orc.Params(iterations=it))
+        assert np.array_equal(got, want), (shape, it)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"SS_SOLVER": "stream"}, {"SS_SOLVER": "ldg"},
+                                 {"SS_SOLVER_K": "4"}, {"SS_SOLVER_K": "8"}])
+def test_solver_variants_bitwise(ss, env):
+    """Every solver schedule (streaming, blocked LDG, blocked TMA at K = 4/6/8)
+    produces the reference's bits."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", VARIANT_SCRIPT, ROOT], env=e, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
