@@ -1,0 +1,79 @@
+"""Summarise ncu outputs into profiles/*.md (run here, on the CPU box).
+
+    python profiles/summarize.py launches gpurun_out/launches.csv
+    python profiles/summarize.py full gpurun_out/prof.ncu-rep
+"""
+
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_bytes.sum",
+    "sm__cycles_elapsed.avg.per_second",
+]
+
+
+def _scale(v, unit):
+    return {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+            "second": 1e6, "s": 1e6}.get(unit, 1.0) * v
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hi]
+    ki, mi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.defaultdict(list)
+    for r in rows[hi + 1:]:
+        if len(r) <= mi:
+            continue
+        agg[r[ki].split("(")[0][:70]].append(_scale(float(r[mi].replace(",", "")), r[ui]))
+    tot = sum(sum(v) for v in agg.values())
+    out = ["| kernel | launches | total us | avg us | share |", "|---|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+        out.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v) / len(v):.2f} | "
+                   f"{100 * sum(v) / tot:.1f}% |")
+    return "\n".join(out)
+
+
+def full(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    out = []
+    for r in data:
+        name = r[hdr.index("Kernel Name")]
+        out.append(f"### `{name[:90]}`\n")
+        out.append("| metric | value |\n|---|---|")
+        for k in KEYS:
+            if k in hdr:
+                out.append(f"| {k} | {r[hdr.index(k)]} {units[hdr.index(k)]} |")
+        stalls = []
+        for i, h in enumerate(hdr):
+            if "pcsamp_warps_issue_stalled" in h and not h.endswith("not_issued"):
+                try:
+                    stalls.append((float(r[i].replace(",", "")), h.split("stalled_")[-1]))
+                except ValueError:
+                    pass
+        tot = sum(v for v, _ in stalls) or 1.0
+        top = ", ".join(f"{n} {100 * v / tot:.1f}%" for v, n in sorted(stalls, reverse=True)[:8])
+        out.append(f"\nstall samples: {top}\n")
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    mode, path = sys.argv[1], sys.argv[2]
+    print(launches(path) if mode == "launches" else full(path))
