@@ -144,6 +144,27 @@ SS_API int ss_last_timing(const ss_session *s, ss_timing *t);
 /* Copy the flows used by the last step (for feeding back into the
  * reference's FloDirFlow / FlowProvider seam). */
 SS_API int ss_flows(const ss_session *s, int which, float *uv_dst, uint8_t *valid_dst, int where);
+
+/* ---- lite flow network (north star (a); architecture in liteflownet.py) --- */
+typedef struct ss_flownet ss_flownet;
+/* Number of float32 parameters the network expects (liteflownet.n_params). */
+SS_API int64_t ss_flownet_num_params(void);
+/* Upload weights (host float32, liteflownet.flatten_weights layout) to the
+ * current device.  precision: SS_FLOW_FP32 (CUDA-core FFMA) or SS_FLOW_BF16
+ * (tcgen05 tensor cores, bf16 operands, fp32 accumulation). */
+enum ss_flow_precision { SS_FLOW_FP32 = 0, SS_FLOW_BF16 = 1 };
+SS_API int ss_flownet_create(const float *weights, int64_t n, int precision, ss_flownet **out);
+SS_API int ss_flownet_destroy(ss_flownet *net);
+/* Stateless: flow from frame_a toward frame_b ((h, w, c) HWC float32 device
+ * pointers) into uv (h, w, 2) and valid (h, w) (may be NULL); stream-ordered. */
+SS_API int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b, int h,
+                           int w, int c, float *uv, uint8_t *valid, void *stream);
+/* Attach the network to a session: it computes the step's flows itself,
+ * caching each ring frame's feature pyramid (FlowProvider.flow_between(t, I_t,
+ * t-/+1, I_t-/+1), consistency.py:380, :384). */
+SS_API int ss_session_attach_flownet(ss_session *s, ss_flownet *net);
+/* Compute flow slot `which` (0: t -> t-1, 1: t -> t+1) for the pending step. */
+SS_API int ss_session_compute_flow(ss_session *s, int which);
 SS_API void *ss_session_stream(const ss_session *s);
 
 #ifdef __cplusplus

@@ -4,8 +4,11 @@
 // positions, one-frame latency, error texts) follows consistency.py:321-353
 // exactly; the per-frame math is K1 (k_presolve) + K2 (solve_planar).
 #include <cstring>
+#include <map>
+#include <memory>
 #include <string>
 
+#include "flownet.h"
 #include "ss_common.cuh"
 #include "ss_internal.h"
 
@@ -89,6 +92,18 @@ struct ss_session {
     SolverWork solver;
     cudaEvent_t ev[3];
     ss_timing timing;
+    // lite flow network (optional): pyramid slot i follows ring slot i
+    ss_flownet *net = nullptr;
+    std::unique_ptr<fn::Run> run;
+    cudaEvent_t fev[2] = {nullptr, nullptr};
+    bool flow_timed = false;
+};
+
+struct ss_flownet {
+    int device;
+    int precision;
+    fn::Weights wts;
+    std::map<std::pair<int, int>, std::unique_ptr<fn::Run>> runs;  // stateless calls
 };
 
 static int session_alloc(ss_session *s)
@@ -109,6 +124,7 @@ static int session_alloc(ss_session *s)
     SS_CUDA_TRY(cudaMalloc(&s->lapP, px * s->cp * sizeof(float)));
     SS_CUDA_TRY(cudaMalloc(&s->wc, px * sizeof(float)));
     for (auto &e : s->ev) SS_CUDA_TRY(cudaEventCreate(&e));
+    for (auto &e : s->fev) SS_CUDA_TRY(cudaEventCreate(&e));
     return s->solver.ensure(s->h, s->w, s->cp, 150) == SS_OK ? SS_OK : SS_NO_MEMORY;
 }
 
@@ -129,6 +145,9 @@ static void session_free(ss_session *s)
     cudaFree(s->wc);
     for (auto &e : s->ev)
         if (e) cudaEventDestroy(e);
+    for (auto &e : s->fev)
+        if (e) cudaEventDestroy(e);
+    s->run.reset();
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
 
@@ -396,6 +415,7 @@ int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, 
         s->order[2] = idx;
     }
     auto &sl = s->slot[idx];
+    if (s->run) s->run->slots[idx].key = -1;  // the frame's cached pyramid is stale
     if (int rc = copy_frame(s, sl.I, I, s->ci, dtype, where)) return rc;
     if (int rc = copy_frame(s, sl.P, P, s->cp, dtype, where)) return rc;
     sl.pos = position;
@@ -529,6 +549,11 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
     cudaEventElapsedTime(&t_solve, s->ev[1], s->ev[2]);
     s->timing.warp_blend_ms = t_blend;
     s->timing.solve_ms = t_solve;
+    s->timing.flow_ms = 0.f;
+    if (s->flow_timed) {  // device time of the flow network for this step
+        cudaEventElapsedTime(&s->timing.flow_ms, s->fev[0], s->fev[1]);
+        s->flow_timed = false;
+    }
     float *tmp = s->O;  // commit (consistency.py:410-412)
     s->O = s->O_new;
     s->O_new = tmp;
@@ -579,6 +604,95 @@ int ss_flows(const ss_session *s, int which, float *uv_dst, uint8_t *valid_dst, 
     if (uv_dst) SS_CUDA_TRY(cudaMemcpyAsync(uv_dst, s->uv[which], px * 2 * sizeof(float), kind, s->stream));
     if (valid_dst) SS_CUDA_TRY(cudaMemcpyAsync(valid_dst, s->valid[which], px, kind, s->stream));
     SS_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return SS_OK;
+}
+
+// ---- lite flow network ----------------------------------------------------------
+int64_t ss_flownet_num_params(void) { return fn::Weights::expected_params(); }
+
+int ss_flownet_create(const float *weights, int64_t n, int precision, ss_flownet **out)
+{
+    if (precision != SS_FLOW_FP32 && precision != SS_FLOW_BF16) {
+        set_error("precision must be SS_FLOW_FP32 or SS_FLOW_BF16");
+        return SS_VALUE_ERROR;
+    }
+    std::unique_ptr<ss_flownet> net(new (std::nothrow) ss_flownet());
+    if (!net) return SS_NO_MEMORY;
+    SS_CUDA_TRY(cudaGetDevice(&net->device));
+    net->precision = precision;
+    if (int rc = net->wts.upload(weights, n)) return rc;
+    *out = net.release();
+    return SS_OK;
+}
+
+int ss_flownet_destroy(ss_flownet *net)
+{
+    if (net) {
+        cudaDeviceSynchronize();
+        delete net;
+    }
+    return SS_OK;
+}
+
+int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b, int h, int w,
+                    int c, float *uv, uint8_t *valid, void *stream)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    if (int rc = check_c(c)) return rc;
+    auto &run = net->runs[{h, w}];
+    if (!run) {
+        run.reset(new fn::Run());
+        if (int rc = run->init(&net->wts, h, w)) {
+            run.reset();
+            return rc;
+        }
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = run->pyramid(0, -1, frame_a, c, st)) return rc;
+    if (int rc = run->pyramid(1, -1, frame_b, c, st)) return rc;
+    return run->flow(0, 1, uv, valid, st);
+}
+
+int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
+{
+    if (s->net == net && s->run) return SS_OK;
+    s->net = net;
+    s->run.reset(new fn::Run());
+    if (int rc = s->run->init(&net->wts, s->h, s->w)) {
+        s->run.reset();
+        s->net = nullptr;
+        return rc;
+    }
+    return SS_OK;
+}
+
+int ss_session_compute_flow(ss_session *s, int which)
+{
+    if (which != 0 && which != 1) {
+        set_error("which must be 0 (to previous) or 1 (to next)");
+        return SS_VALUE_ERROR;
+    }
+    if (!s->run) {
+        set_error("no flow network attached to the session");
+        return SS_VALUE_ERROR;
+    }
+    const int64_t t = s->solved_through + 1, other = which == 0 ? t - 1 : t + 1;
+    const auto *a = find_pos(s, t), *b = find_pos(s, other);
+    if (!a || !b) {
+        set_error("frames " + std::to_string(t) + " and " + std::to_string(other) +
+                  " are not buffered");
+        return SS_VALUE_ERROR;
+    }
+    const int ia = (int)(a - s->slot), ib = (int)(b - s->slot);
+    if (which == 0 || !s->flow_timed) {
+        SS_CUDA_TRY(cudaEventRecord(s->fev[0], s->stream));
+    }
+    if (int rc = s->run->pyramid(ia, t, a->I, s->ci, s->stream)) return rc;
+    if (int rc = s->run->pyramid(ib, other, b->I, s->ci, s->stream)) return rc;
+    if (int rc = s->run->flow(ia, ib, s->uv[which], s->valid[which], s->stream)) return rc;
+    SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->stream));
+    s->flow_timed = true;
+    s->flow_for[which] = t;
     return SS_OK;
 }
 

@@ -1,0 +1,255 @@
+// Native runner of the lite flow network: weight upload in the layout of
+// liteflownet.layer_table(), per-resolution buffers, pyramid cache, and the
+// estimator / refinement schedule (liteflownet.py docstring).
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "flownet.h"
+#include "ss_common.cuh"
+
+namespace ss {
+namespace fn {
+
+static const int PYR_CH[6] = {16, 32, 64, 96, 128, 196};
+static inline int pad4(int c) { return (c + 3) / 4 * 4; }
+static inline int est_in(int lvl) { return lvl == 6 ? 84 : 88 + PYR_CH[lvl - 1]; }
+constexpr int E_LD = 196;  // [flow 2 | 0 0 | e5 32 | e4 64 | e3 96]
+
+// layer indices (same order as liteflownet.layer_table())
+static inline int pyr_idx(int lvl, int j) { return (lvl - 1) * 3 + j; }          // j: 0 a, 1 b, 2 c
+static inline int est_idx(int lvl, int j) { return 18 + (6 - lvl) * 6 + (j - 1); }  // j: 1..6
+static inline int ref_idx(int i, bool pw) { return 42 + (i - 1) * 2 + (pw ? 1 : 0); }  // i: 1..6
+constexpr int REF7 = 54;
+
+static std::vector<LayerDev> table()
+{
+    std::vector<LayerDev> L;
+    auto conv = [&](int cin, int cout, int k, int stride, int dil, int act) {
+        LayerDev d;
+        d.cin = cin; d.cout = cout; d.cout_pad = pad4(cout); d.k = k; d.stride = stride;
+        d.dil = dil; d.act = act; d.dw = false;
+        L.push_back(d);
+    };
+    int cin = 4;
+    for (int l = 1; l <= 6; ++l) {
+        conv(cin, PYR_CH[l - 1], 3, 2, 1, 1);
+        conv(pad4(PYR_CH[l - 1]), PYR_CH[l - 1], 3, 1, 1, 1);
+        conv(pad4(PYR_CH[l - 1]), PYR_CH[l - 1], 3, 1, 1, 1);
+        cin = pad4(PYR_CH[l - 1]);
+    }
+    for (int lvl = 6; lvl >= 3; --lvl) {
+        conv(est_in(lvl), 128, 3, 1, 1, 1);
+        conv(128, 128, 3, 1, 1, 1);
+        conv(128, 96, 3, 1, 1, 1);
+        conv(96, 64, 3, 1, 1, 1);
+        conv(64 + 96, 32, 3, 1, 1, 1);
+        conv(32 + 64, 2, 3, 1, 1, 0);
+    }
+    const int sep[6][3] = {{100, 128, 1}, {128, 128, 2}, {128, 128, 4},
+                           {128, 96, 8},  {96, 64, 16},  {64, 32, 1}};
+    for (auto &s : sep) {
+        LayerDev d;
+        d.cin = s[0]; d.cout = s[0]; d.cout_pad = s[0]; d.k = 3; d.stride = 1; d.dil = s[2];
+        d.act = 0; d.dw = true;
+        L.push_back(d);
+        conv(s[0], s[1], 1, 1, 1, 1);
+    }
+    conv(32, 2, 3, 1, 1, 0);
+    return L;
+}
+
+Weights::~Weights() { cudaFree(block); }
+
+int Weights::expected_params()
+{
+    long n = 0;
+    for (auto &l : table()) n += l.dw ? 9L * l.cin + l.cin : (long)l.k * l.k * l.cin * l.cout + l.cout;
+    return (int)n;
+}
+
+int Weights::upload(const float *host, int64_t n)
+{
+    layers = table();
+    if (n != expected_params()) {
+        set_error("flow network expects " + std::to_string(expected_params()) +
+                  " parameters, got " + std::to_string(n));
+        return SS_VALUE_ERROR;
+    }
+    // device layout: conv W [k*k*cin][cout_pad] + b [cout_pad]; dw W [9][cin] + b [cin]
+    size_t total = 0;
+    for (auto &l : layers)
+        total += l.dw ? (size_t)10 * l.cin : (size_t)(l.k * l.k * l.cin + 1) * l.cout_pad;
+    std::vector<float> dev(total, 0.0f);
+    size_t off = 0, src = 0;
+    std::vector<size_t> woff(layers.size()), boff(layers.size());
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) {
+            woff[i] = off;
+            std::memcpy(&dev[off], host + src, sizeof(float) * 9 * l.cin);
+            off += 9 * l.cin;
+            src += 9 * l.cin;
+            boff[i] = off;
+            std::memcpy(&dev[off], host + src, sizeof(float) * l.cin);
+            off += l.cin;
+            src += l.cin;
+        } else {
+            const int K = l.k * l.k * l.cin;
+            woff[i] = off;
+            for (int r = 0; r < K; ++r)
+                std::memcpy(&dev[off + (size_t)r * l.cout_pad], host + src + (size_t)r * l.cout,
+                            sizeof(float) * l.cout);
+            off += (size_t)K * l.cout_pad;
+            src += (size_t)K * l.cout;
+            boff[i] = off;
+            std::memcpy(&dev[off], host + src, sizeof(float) * l.cout);
+            off += l.cout_pad;
+            src += l.cout;
+        }
+    }
+    cudaFree(block);
+    block = nullptr;
+    SS_CUDA_TRY(cudaMalloc(&block, total * sizeof(float)));
+    SS_CUDA_TRY(cudaMemcpy(block, dev.data(), total * sizeof(float), cudaMemcpyHostToDevice));
+    for (size_t i = 0; i < layers.size(); ++i) {
+        layers[i].w = block + woff[i];
+        layers[i].b = block + boff[i];
+    }
+    return SS_OK;
+}
+
+Run::~Run()
+{
+    for (void *p : allocs) cudaFree(p);
+}
+
+int Run::init(const Weights *wt, int h_, int w_)
+{
+    wts = wt;
+    h = h_;
+    w = w_;
+    H[0] = (h + 63) / 64 * 64;
+    W[0] = (w + 63) / 64 * 64;
+    for (int l = 1; l <= 6; ++l) {
+        H[l] = H[l - 1] / 2;
+        W[l] = W[l - 1] / 2;
+    }
+    auto alloc = [&](float **p, size_t floats) -> int {
+        SS_CUDA_TRY(cudaMalloc(p, floats * sizeof(float)));
+        SS_CUDA_TRY(cudaMemset(*p, 0, floats * sizeof(float)));
+        allocs.push_back(*p);
+        return SS_OK;
+    };
+    const size_t px1 = (size_t)H[1] * W[1];
+    int rc;
+    if ((rc = alloc(&prep, (size_t)H[0] * W[0] * 4))) return rc;
+    if ((rc = alloc(&s0, px1 * 16))) return rc;
+    if ((rc = alloc(&s1, px1 * 16))) return rc;
+    for (auto &sl : slots)
+        for (int l = 3; l <= 6; ++l)
+            if ((rc = alloc(&sl.lvl[l], (size_t)H[l] * W[l] * PYR_CH[l - 1]))) return rc;
+    for (int l = 3; l <= 6; ++l) {
+        const size_t px = (size_t)H[l] * W[l];
+        if ((rc = alloc(&x[l], px * est_in(l)))) return rc;
+        if ((rc = alloc(&e1[l], px * 128))) return rc;
+        if ((rc = alloc(&e2[l], px * 128))) return rc;
+        if ((rc = alloc(&E[l], px * E_LD))) return rc;
+        if ((rc = alloc(&w2[l], px * PYR_CH[l - 1]))) return rc;
+    }
+    const size_t px3 = (size_t)H[3] * W[3];
+    if ((rc = alloc(&ra, px3 * 128))) return rc;
+    if ((rc = alloc(&rb, px3 * 128))) return rc;
+    if ((rc = alloc(&rr, px3 * 4))) return rc;
+    return SS_OK;
+}
+
+static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, float *out,
+                int out_ld, cudaStream_t st)
+{
+    ConvParams p;
+    p.in = in;
+    p.in_ld = in_ld;
+    p.H = Hi;
+    p.W = Wi;
+    p.Cin = L.cin;
+    p.wgt = L.w;
+    p.bias = L.b;
+    p.Cout = L.cout;
+    p.Cout_pad = L.cout_pad;
+    p.out = out;
+    p.out_ld = out_ld;
+    p.k = L.k;
+    p.stride = L.stride;
+    p.dil = L.dil;
+    p.pad = L.dil * (L.k / 2);
+    p.Ho = (Hi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
+    p.Wo = (Wi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
+    p.act = L.act;
+    return launch_conv_ffma(p, st);
+}
+
+int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st)
+{
+    Slot &sl = slots[slot];
+    if (key >= 0 && sl.key == key) return SS_OK;  // key < 0: never cached
+    sl.key = -1;
+    int rc;
+    if ((rc = launch_prep(img, h, w, c, H[0], W[0], prep, st))) return rc;
+    const float *in = prep;
+    int in_ld = 4;
+    for (int l = 1; l <= 6; ++l) {
+        const int C = PYR_CH[l - 1];
+        float *a = l <= 2 ? (in == s0 ? s1 : s0) : (in == s0 ? s1 : s0);
+        if ((rc = conv(wts->L(pyr_idx(l, 0)), in, in_ld, H[l - 1], W[l - 1], a, C, st))) return rc;
+        float *b = a == s0 ? s1 : s0;
+        if ((rc = conv(wts->L(pyr_idx(l, 1)), a, C, H[l], W[l], b, C, st))) return rc;
+        float *c3 = l <= 2 ? a : sl.lvl[l];
+        if ((rc = conv(wts->L(pyr_idx(l, 2)), b, C, H[l], W[l], c3, C, st))) return rc;
+        in = c3;
+        in_ld = C;
+    }
+    sl.key = key >= 0 ? key : -1;
+    return SS_OK;
+}
+
+int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
+{
+    int rc;
+    for (int l = 6; l >= 3; --l) {
+        const int C = PYR_CH[l - 1], X = est_in(l);
+        const float *f1 = slots[a].lvl[l], *f2 = slots[b].lvl[l];
+        if (l == 6) {
+            if ((rc = launch_corr(f1, f2, C, H[l], W[l], x[l], X, false, st))) return rc;
+        } else {
+            if ((rc = launch_up2_warp(E[l + 1], E_LD, H[l + 1], W[l + 1], f2, C, H[l], W[l], x[l], X,
+                                      w2[l], st)))
+                return rc;
+            if ((rc = launch_corr(f1, w2[l], C, H[l], W[l], x[l], X, true, st))) return rc;
+        }
+        const int hh = H[l], ww = W[l];
+        if ((rc = conv(wts->L(est_idx(l, 1)), x[l], X, hh, ww, e1[l], 128, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 2)), e1[l], 128, hh, ww, e2[l], 128, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 3)), e2[l], 128, hh, ww, E[l] + 100, E_LD, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 4)), E[l] + 100, E_LD, hh, ww, E[l] + 36, E_LD, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 5)), E[l] + 36, E_LD, hh, ww, E[l] + 4, E_LD, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 6)), E[l] + 4, E_LD, hh, ww, E[l], E_LD, st))) return rc;
+    }
+    // separable refinement at level 3: r_in = E[3][0:100]
+    const int hh = H[3], ww = W[3];
+    const float *in = E[3];
+    int in_ld = E_LD;
+    const int cin[6] = {100, 128, 128, 128, 96, 64};
+    for (int i = 1; i <= 6; ++i) {
+        const LayerDev &dw = wts->L(ref_idx(i, false));
+        if ((rc = launch_depthwise(in, in_ld, hh, ww, cin[i - 1], dw.w, dw.dil, ra, 128, st))) return rc;
+        if ((rc = conv(wts->L(ref_idx(i, true)), ra, 128, hh, ww, rb, 128, st))) return rc;
+        in = rb;
+        in_ld = 128;
+    }
+    if ((rc = conv(wts->L(REF7), rb, 128, hh, ww, rr, 4, st))) return rc;
+    return launch_flow_final(E[3], E_LD, rr, 4, hh, ww, h, w, uv, valid, st);
+}
+
+}  // namespace fn
+}  // namespace ss

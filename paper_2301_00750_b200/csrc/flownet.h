@@ -1,0 +1,77 @@
+// Lite flow network: kernel launchers and the native runner (see
+// paper_2301_00750_b200/liteflownet.py for the architecture table).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <memory>
+#include <utility>
+#include <vector>
+
+namespace ss {
+namespace fn {
+
+struct ConvParams {
+    const float *in;
+    int in_ld, H, W, Cin;       // input NHWC slice (Cin % 4 == 0, 16-byte aligned)
+    const float *wgt, *bias;    // wgt [k*k*Cin][Cout_pad], bias [Cout_pad]
+    int Cout, Cout_pad;
+    float *out;
+    int out_ld, Ho, Wo;
+    int k, stride, dil, pad, act;
+};
+
+int launch_conv_ffma(const ConvParams &p, cudaStream_t st);
+int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,
+                     float *out, int ld_out, cudaStream_t st);
+int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st);
+int launch_up2_warp(const float *coarse, int cld, int Hc, int Wc, const float *f2, int C, int H,
+                    int W, float *x, int xld, float *w2, cudaStream_t st);
+int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x, int xld,
+                bool copy_f1, cudaStream_t st);
+int launch_flow_final(const float *f3, int ld3, const float *r, int ldr, int Hc, int Wc, int h,
+                      int w, float *uv, uint8_t *valid, cudaStream_t st);
+
+struct LayerDev {
+    int cin, cout, cout_pad, k, stride, dil, act;
+    bool dw;
+    float *w = nullptr, *b = nullptr;
+};
+
+// Weights on one device, in liteflownet.layer_table() order.
+struct Weights {
+    std::vector<LayerDev> layers;
+    float *block = nullptr;
+    ~Weights();
+    static int expected_params();
+    int upload(const float *host, int64_t n);
+    const LayerDev &L(int i) const { return layers[i]; }
+};
+
+// Resolution-specific buffers + a 3-slot pyramid cache (slots follow the
+// session's frame ring: the pyramid of a frame is computed once and reused by
+// the two steps that see it as a neighbour and the one that sees it as I_t).
+struct Run {
+    const Weights *wts = nullptr;
+    int h = 0, w = 0, H[7] = {0}, W[7] = {0};
+    float *prep = nullptr, *s0 = nullptr, *s1 = nullptr;
+    struct Slot {
+        int64_t key = -1;
+        float *lvl[7] = {nullptr};
+    } slots[3];
+    float *x[7] = {nullptr}, *e1[7] = {nullptr}, *e2[7] = {nullptr}, *E[7] = {nullptr},
+          *w2[7] = {nullptr};
+    float *ra = nullptr, *rb = nullptr, *rr = nullptr;
+    std::vector<void *> allocs;
+    ~Run();
+    int init(const Weights *w, int h, int w_);
+    // pyramid of img (h, w, c) into slot (skipped if key matches)
+    int pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st);
+    // flow from the frame in slot a toward the frame in slot b (both computed)
+    int flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st);
+};
+
+}  // namespace fn
+}  // namespace ss

@@ -1,0 +1,409 @@
+// Lite flow network kernels (fp32 path), sm_100a.  Architecture:
+// paper_2301_00750_b200/liteflownet.py.  NHWC activations, every channel count
+// padded to a multiple of 4 (16-byte rows).  This TU uses FMA freely: the
+// flow network has no reference bits to reproduce (parity is a tolerance vs.
+// the CPU restatement).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "flownet.h"
+#include "ss_common.cuh"
+
+namespace ss {
+namespace fn {
+
+__device__ __forceinline__ float leaky(float v) { return v >= 0.f ? v : 0.1f * v; }
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred)
+{
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const int n = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---------------------------------------------------------------------------
+// Implicit-GEMM convolution on CUDA cores (FFMA), fp32.
+//   M = Ho*Wo output pixels (tile BM = 128), N = Cout (tile BN), K = k*k*Cin
+//   (tile BK = 16, float4 groups never straddle a tap because Cin % 4 == 0).
+// Thread tile 8 pixels x 4 output channels; A staged [m][k] so one LDS.128
+// yields 4 k-values of a pixel, B staged [k][n].  cp.async double buffering
+// with zero-fill for padding / tails.
+constexpr int BM = 128, BK = 16, AS = BK + 4;
+
+template <int BN>
+__global__ void __launch_bounds__(16 * (BN / 4)) k_conv_ffma(ConvParams p)
+{
+    constexpr int NT = BN / 4;       // channel groups
+    constexpr int THREADS = 16 * NT; // 16 pixel groups
+    __shared__ __align__(16) float As[2][BM][AS];
+    __shared__ __align__(16) float Bs[2][BK][BN];
+    const int tid = threadIdx.x;
+    const int tm = tid % 16, tn = tid / 16;
+    const int M = p.Ho * p.Wo;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int Ktot = p.k * p.k * p.Cin;
+    const int nk = (Ktot + BK - 1) / BK;
+
+    // A slots of this thread: BM*BK/4 float4 = 512 per stage
+    constexpr int A_SLOTS = (BM * BK / 4) / THREADS;
+    int a_m[A_SLOTS], a_oy[A_SLOTS], a_ox[A_SLOTS], a_kq[A_SLOTS];
+#pragma unroll
+    for (int s = 0; s < A_SLOTS; ++s) {
+        const int f = tid + s * THREADS;
+        a_m[s] = f >> 2;
+        a_kq[s] = f & 3;
+        const int pix = m0 + a_m[s];
+        a_oy[s] = pix < M ? pix / p.Wo : -100000;
+        a_ox[s] = pix < M ? pix - (pix / p.Wo) * p.Wo : 0;
+    }
+    // B slots: BK*BN/4 float4
+    constexpr int B_SLOTS = (BK * BN / 4 + THREADS - 1) / THREADS;
+
+    auto load_stage = [&](int st, int kt) {
+        const int k0 = kt * BK;
+#pragma unroll
+        for (int s = 0; s < A_SLOTS; ++s) {
+            const int k = k0 + a_kq[s] * 4;
+            const int tap = k / p.Cin, ci = k - tap * p.Cin;
+            const int ky = tap / p.k, kx = tap - ky * p.k;
+            const int iy = a_oy[s] * p.stride + ky * p.dil - p.pad;
+            const int ix = a_ox[s] * p.stride + kx * p.dil - p.pad;
+            const bool ok = k < Ktot && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W;
+            const float *src = ok ? p.in + ((long)iy * p.W + ix) * p.in_ld + ci : p.in;
+            cp_async16(&As[st][a_m[s]][a_kq[s] * 4], src, ok);
+        }
+#pragma unroll
+        for (int s = 0; s < B_SLOTS; ++s) {
+            const int f = tid + s * THREADS;
+            if (f < BK * BN / 4) {
+                const int kr = f / (BN / 4), nc = (f - kr * (BN / 4)) * 4;
+                const int k = k0 + kr, n = n0 + nc;
+                const bool ok = k < Ktot && n < p.Cout_pad;
+                const float *src = ok ? p.wgt + (long)k * p.Cout_pad + n : p.wgt;
+                cp_async16(&Bs[st][kr][nc], src, ok);
+            }
+        }
+        cp_async_commit();
+    };
+
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+    load_stage(0, 0);
+    for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt & 1;
+        if (kt + 1 < nk) {
+            load_stage(st ^ 1, kt + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            float4 a[8], b[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(&As[st][i * 16 + tm][kk]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const float4 *>(&Bs[st][kk + j][tn * 4]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float av[4] = {a[i].x, a[i].y, a[i].z, a[i].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[i][0] = fmaf(av[j], b[j].x, acc[i][0]);
+                    acc[i][1] = fmaf(av[j], b[j].y, acc[i][1]);
+                    acc[i][2] = fmaf(av[j], b[j].z, acc[i][2]);
+                    acc[i][3] = fmaf(av[j], b[j].w, acc[i][3]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    const int n = n0 + tn * 4;
+    if (n >= p.Cout) return;
+    float bias[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bias[j] = n + j < p.Cout ? p.bias[n + j] : 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int pix = m0 + i * 16 + tm;
+        if (pix >= M) continue;
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v[j] = acc[i][j] + bias[j];
+            if (p.act) v[j] = leaky(v[j]);
+        }
+        float *dst = p.out + (long)pix * p.out_ld + n;
+        if (n + 4 <= p.Cout) {
+            *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+            for (int j = 0; j < p.Cout - n; ++j) dst[j] = v[j];
+        }
+    }
+}
+
+int launch_conv_ffma(const ConvParams &p, cudaStream_t st)
+{
+    const int M = p.Ho * p.Wo;
+    const int gx = (M + BM - 1) / BM;
+    if (p.Cout > 32) {
+        k_conv_ffma<64><<<dim3(gx, (p.Cout + 63) / 64), 256, 0, st>>>(p);
+    } else if (p.Cout > 16) {
+        k_conv_ffma<32><<<dim3(gx, 1), 128, 0, st>>>(p);
+    } else {
+        k_conv_ffma<16><<<dim3(gx, 1), 64, 0, st>>>(p);
+    }
+    SS_LAUNCH_CHECK("k_conv_ffma");
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// depthwise 3x3 (dilated), NHWC, zero padding, no bias / activation
+__global__ void k_depthwise(const float *__restrict__ in, int ld, int H, int W, int C,
+                            const float *__restrict__ w, int dil, float *__restrict__ out,
+                            int ld_out)
+{
+    const int C4 = C / 4;
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)H * W * C4) return;
+    const int c = (int)(i % C4) * 4;
+    const long pix = i / C4;
+    const int y = (int)(pix / W), x = (int)(pix - (long)y * W);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky) {
+        const int iy = y + (ky - 1) * dil;
+        if (iy < 0 || iy >= H) continue;
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+            const int ix = x + (kx - 1) * dil;
+            if (ix < 0 || ix >= W) continue;
+            const float4 v = *reinterpret_cast<const float4 *>(in + ((long)iy * W + ix) * ld + c);
+            const float4 k = *reinterpret_cast<const float4 *>(w + (ky * 3 + kx) * C + c);
+            acc.x = fmaf(v.x, k.x, acc.x);
+            acc.y = fmaf(v.y, k.y, acc.y);
+            acc.z = fmaf(v.z, k.z, acc.z);
+            acc.w = fmaf(v.w, k.w, acc.w);
+        }
+    }
+    *reinterpret_cast<float4 *>(out + pix * ld_out + c) = acc;
+}
+
+int launch_depthwise(const float *in, int ld, int H, int W, int C, const float *w, int dil,
+                     float *out, int ld_out, cudaStream_t st)
+{
+    const long n = (long)H * W * (C / 4);
+    k_depthwise<<<blocks_for(n, 256), 256, 0, st>>>(in, ld, H, W, C, w, dil, out, ld_out);
+    SS_LAUNCH_CHECK("k_depthwise");
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// network input: (h, w, c) HWC in [0,1] -> (H64, W64, 4) NHWC, RGB - 0.5,
+// replicate padding, zero 4th channel; grey input is replicated to RGB
+__global__ void k_prep(const float *__restrict__ img, int h, int w, int c, int H, int W,
+                       float *__restrict__ out)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)H * W) return;
+    const int y = (int)(i / W), x = (int)(i - (long)y * W);
+    const long q = (long)min(y, h - 1) * w + min(x, w - 1);
+    float r, g, b;
+    if (c == 3) {
+        r = img[q * 3];
+        g = img[q * 3 + 1];
+        b = img[q * 3 + 2];
+    } else {
+        r = g = b = img[q];
+    }
+    reinterpret_cast<float4 *>(out)[i] = make_float4(r - 0.5f, g - 0.5f, b - 0.5f, 0.f);
+}
+
+int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st)
+{
+    k_prep<<<blocks_for((long)H * W, 256), 256, 0, st>>>(img, h, w, c, H, W, out);
+    SS_LAUNCH_CHECK("k_prep");
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// bilinear (align_corners=False) source coordinate with negative clamp
+__device__ __forceinline__ void src_coord(int d, float inv_scale, int n, int &i0, int &i1, float &f)
+{
+    float s = fmaxf((d + 0.5f) * inv_scale - 0.5f, 0.f);
+    i0 = (int)floorf(s);
+    if (i0 > n - 1) i0 = n - 1;
+    i1 = min(i0 + 1, n - 1);
+    f = s - (float)i0;
+}
+
+// up = 2 * bilinear_x2(coarse flow) -> x[:, 84:86]; w2 = warp_zero(f2, up)
+__global__ void k_up2_warp(const float *__restrict__ coarse, int cld, int Hc, int Wc,
+                           const float *__restrict__ f2, int C, int H, int W,
+                           float *__restrict__ x, int xld, float *__restrict__ w2)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)H * W) return;
+    const int y = (int)(i / W), xx = (int)(i - (long)y * W);
+    int y0, y1, x0, x1;
+    float fy, fx;
+    src_coord(y, 0.5f, Hc, y0, y1, fy);
+    src_coord(xx, 0.5f, Wc, x0, x1, fx);
+    float up[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float a = coarse[((long)y0 * Wc + x0) * cld + k], b = coarse[((long)y0 * Wc + x1) * cld + k];
+        const float c = coarse[((long)y1 * Wc + x0) * cld + k], d = coarse[((long)y1 * Wc + x1) * cld + k];
+        const float top = a * (1.f - fx) + b * fx, bot = c * (1.f - fx) + d * fx;
+        up[k] = 2.f * (top * (1.f - fy) + bot * fy);
+    }
+    x[i * xld + 84] = up[0];
+    x[i * xld + 85] = up[1];
+    const float sx = (float)xx + up[0], sy = (float)y + up[1];
+    const float gx0 = floorf(sx), gy0 = floorf(sy);
+    const int ix = (int)gx0, iy = (int)gy0;
+    const float ax = sx - gx0, ay = sy - gy0;
+    const float wt[4] = {(1.f - ay) * (1.f - ax), (1.f - ay) * ax, ay * (1.f - ax), ay * ax};
+    const int ty[4] = {iy, iy, iy + 1, iy + 1}, tx[4] = {ix, ix + 1, ix, ix + 1};
+    bool ok[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) ok[t] = ty[t] >= 0 && ty[t] < H && tx[t] >= 0 && tx[t] < W;
+    for (int c = 0; c < C; c += 4) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (!ok[t]) continue;
+            const float4 v = *reinterpret_cast<const float4 *>(f2 + ((long)ty[t] * W + tx[t]) * C + c);
+            acc.x = fmaf(wt[t], v.x, acc.x);
+            acc.y = fmaf(wt[t], v.y, acc.y);
+            acc.z = fmaf(wt[t], v.z, acc.z);
+            acc.w = fmaf(wt[t], v.w, acc.w);
+        }
+        *reinterpret_cast<float4 *>(w2 + i * C + c) = acc;
+    }
+}
+
+int launch_up2_warp(const float *coarse, int cld, int Hc, int Wc, const float *f2, int C, int H,
+                    int W, float *x, int xld, float *w2, cudaStream_t st)
+{
+    k_up2_warp<<<blocks_for((long)H * W, 128), 128, 0, st>>>(coarse, cld, Hc, Wc, f2, C, H, W, x,
+                                                              xld, w2);
+    SS_LAUNCH_CHECK("k_up2_warp");
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cost volume: x[:, d] = leaky(sum_c f1_c * w2_c(p + d) / C), d in [-4,4]^2;
+// also copies f1 into x[:, 88:88+C] (l < 6).  16x16 pixel tile, channels
+// staged 16 at a time with a 4-pixel halo of w2.
+constexpr int CT = 16, CH = 8, HALO = 4, CW = CT + 2 * HALO;
+
+__global__ void __launch_bounds__(CT *CT) k_corr(const float *__restrict__ f1,
+                                                 const float *__restrict__ w2, int C, int H,
+                                                 int W, float *__restrict__ x, int xld,
+                                                 int copy_f1)
+{
+    __shared__ float s1[CT * CT][CH + 1];
+    __shared__ float s2[CW * CW][CH + 1];
+    const int tx = threadIdx.x % CT, ty = threadIdx.x / CT;
+    const int bx = blockIdx.x * CT, by = blockIdx.y * CT;
+    const int y = by + ty, xx = bx + tx;
+    const bool inb = y < H && xx < W;
+    float acc[81];
+#pragma unroll
+    for (int d = 0; d < 81; ++d) acc[d] = 0.f;
+    for (int c0 = 0; c0 < C; c0 += CH) {
+        for (int i = threadIdx.x; i < CT * CT * CH; i += CT * CT) {
+            const int px = i / CH, c = i - px * CH;
+            const int py = by + px / CT, pxx = bx + px % CT;
+            s1[px][c] = (py < H && pxx < W && c0 + c < C) ? f1[((long)py * W + pxx) * C + c0 + c] : 0.f;
+        }
+        for (int i = threadIdx.x; i < CW * CW * CH; i += CT * CT) {
+            const int px = i / CH, c = i - px * CH;
+            const int py = by - HALO + px / CW, pxx = bx - HALO + px % CW;
+            s2[px][c] = (py >= 0 && py < H && pxx >= 0 && pxx < W && c0 + c < C)
+                            ? w2[((long)py * W + pxx) * C + c0 + c]
+                            : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int c = 0; c < CH; ++c) {
+            const float a = s1[ty * CT + tx][c];
+#pragma unroll
+            for (int dy = 0; dy < 9; ++dy)
+#pragma unroll
+                for (int dx = 0; dx < 9; ++dx)
+                    acc[dy * 9 + dx] = fmaf(a, s2[(ty + dy) * CW + tx + dx][c], acc[dy * 9 + dx]);
+        }
+        __syncthreads();
+    }
+    if (!inb) return;
+    const long pix = (long)y * W + xx;
+    const float inv = 1.f / (float)C;
+    float *dst = x + pix * xld;
+#pragma unroll
+    for (int d = 0; d < 81; ++d) dst[d] = leaky(acc[d] * inv);
+    if (copy_f1)
+        for (int c = 0; c < C; c += 4)
+            *reinterpret_cast<float4 *>(dst + 88 + c) = *reinterpret_cast<const float4 *>(f1 + pix * C + c);
+}
+
+int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x, int xld,
+                bool copy_f1, cudaStream_t st)
+{
+    const dim3 grid((W + CT - 1) / CT, (H + CT - 1) / CT);
+    k_corr<<<grid, CT * CT, 0, st>>>(f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
+    SS_LAUNCH_CHECK("k_corr");
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// full-resolution flow: 8 * bilinear_x8(flow3 + r), cropped; writes the
+// session's (h, w, 2) flow slot and validity = 1
+__global__ void k_flow_final(const float *__restrict__ f3, int ld3, const float *__restrict__ r,
+                             int ldr, int Hc, int Wc, int h, int w, float *__restrict__ uv,
+                             uint8_t *__restrict__ valid)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)h * w) return;
+    const int y = (int)(i / w), x = (int)(i - (long)y * w);
+    int y0, y1, x0, x1;
+    float fy, fx;
+    src_coord(y, 0.125f, Hc, y0, y1, fy);
+    src_coord(x, 0.125f, Wc, x0, x1, fx);
+    float o[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        auto at = [&](int yy, int xq) {
+            const long q = (long)yy * Wc + xq;
+            return f3[q * ld3 + k] + r[q * ldr + k];
+        };
+        const float top = at(y0, x0) * (1.f - fx) + at(y0, x1) * fx;
+        const float bot = at(y1, x0) * (1.f - fx) + at(y1, x1) * fx;
+        o[k] = 8.f * (top * (1.f - fy) + bot * fy);
+    }
+    reinterpret_cast<float2 *>(uv)[i] = make_float2(o[0], o[1]);
+    if (valid) valid[i] = 1;
+}
+
+int launch_flow_final(const float *f3, int ld3, const float *r, int ldr, int Hc, int Wc, int h,
+                      int w, float *uv, uint8_t *valid, cudaStream_t st)
+{
+    k_flow_final<<<blocks_for((long)h * w, 256), 256, 0, st>>>(f3, ld3, r, ldr, Hc, Wc, h, w, uv,
+                                                               valid);
+    SS_LAUNCH_CHECK("k_flow_final");
+    return SS_OK;
+}
+
+}  // namespace fn
+}  // namespace ss

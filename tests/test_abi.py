@@ -73,6 +73,30 @@ def test_params_validate_matches_reference_messages(lib, changes, msg):
     assert lib.ss_params_validate(ctypes.byref(params_struct(ConsistencyParams()))) == 0
 
 
+def test_flownet_param_count_matches_layer_table(lib):
+    from paper_2301_00750_b200 import liteflownet as lf
+
+    w = lf.make_weights(0)
+    assert lib.ss_flownet_num_params() == lf.n_params() == lf.flatten_weights(w).size
+    # padding rows are exactly zero; live rows are not
+    w1, _ = w["est5_1"]
+    assert not w1[:, :, 81:84].any() and not w1[:, :, 86:88].any() and w1[:, :, 88:].any()
+
+
+def test_flownet_oracle_shapes():
+    import numpy as np
+
+    import flownet_oracle as fo
+    from paper_2301_00750_b200 import liteflownet as lf
+
+    w = lf.make_weights(1)
+    rng = np.random.default_rng(0)
+    a = rng.random((40, 70, 3)).astype(np.float32)
+    f = fo.flow(w, a, np.roll(a, 2, axis=1))
+    assert f.shape == (40, 70, 2) and f.dtype == np.float32 and np.isfinite(f).all()
+    assert 0.01 < float(np.abs(f).mean()) < 20.0
+
+
 def test_product_has_no_oracle_dependency():
     """The shipped package never imports or links the CPU oracle."""
     pkg = os.path.join(ROOT, "paper_2301_00750_b200")

@@ -1,0 +1,86 @@
+"""GPU parity of the lite flow network (north star (a)) against its CPU
+restatement (oracle/flownet_oracle.py, float64 accumulation).
+
+The reference has no flow CNN, so these pins are to the restatement of the
+architecture in liteflownet.py with the same seeded random-init weights:
+  * fp32 path: flow max |GPU - CPU| <= 2e-3 px, mean EPE <= 1e-4 px;
+  * full step with CNN flows: O_t within 1e-3 max-abs (the north star's fp32
+    bar) of the CPU oracle fed the CPU network's flows.
+"""
+
+import numpy as np
+import pytest
+
+import flownet_oracle as fo
+import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ss():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2301_00750_b200 as m
+
+    return m
+
+
+@pytest.fixture(scope="module")
+def net(ss):
+    return ss.LiteFlowNet(seed=0)
+
+
+def _epe(a, b):
+    return np.sqrt(((a - b) ** 2).sum(axis=2))
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 3), (120, 200, 3), (72, 130, 1), (200, 130, 3)])
+def test_flow_fp32_matches_cpu(ss, net, shape):
+    from paper_2301_00750_b200 import synthetic
+
+    seq = synthetic.translating_sequence(frames=2, height=shape[0], width=shape[1], seed=4)
+    a, b = seq.inputs[1], seq.inputs[0]
+    if shape[2] == 1:
+        a, b = a.mean(axis=2, keepdims=True), b.mean(axis=2, keepdims=True)
+    got = net.flow_between(2, a, 1, b)
+    want = fo.flow(net.weights, a, b)
+    assert got.uv.shape == want.shape and got.valid.all()
+    e = _epe(got.uv, want)
+    assert float(e.max()) <= 2e-3 and float(e.mean()) <= 1e-4, (float(e.max()), float(e.mean()))
+    assert float(np.abs(want).mean()) > 0.05  # the random net emits non-trivial flow
+
+
+def test_session_cnn_step_within_1e3(ss, net):
+    """The full step (CNN flows + consistency) vs the CPU oracle end to end."""
+    from paper_2301_00750_b200 import synthetic
+
+    seq = synthetic.translating_sequence(frames=4, height=96, width=160, seed=6)
+    got = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"), net))
+
+    def flow_fn(a, fa, b, fb):
+        uv = fo.flow(net.weights, fa, fb)
+        return uv, np.ones(uv.shape[:2], bool)
+
+    want = dict(orc.stabilize_stream(seq.inputs, seq.processed, orc.Params(), flow_fn))
+    worst = max(float(np.abs(got[t] - want[t]).max()) for t in want)
+    assert worst <= 1e-3, worst
+
+
+def test_session_flows_match_stateless(ss, net):
+    """Pyramid caching inside the session does not change the flows."""
+    import ctypes
+
+    from paper_2301_00750_b200 import _lib, synthetic
+
+    seq = synthetic.translating_sequence(frames=3, height=64, width=128, seed=2)
+    state = ss.SessionState(params=ss.preset("default"))
+    for i in range(3):
+        state.push_pair(i + 1, seq.inputs[i], seq.processed[i])
+    ss.stabilize_step(state, net)
+    for which, other in ((0, 1), (1, 3)):
+        uv = np.empty((64, 128, 2), np.float32)
+        _lib.lib().ss_flows(state.handle, which, uv.ctypes.data, None, _lib.SS_HOST)
+        ref = net.flow_between(2, seq.inputs[1], other, seq.inputs[other - 1])
+        assert np.array_equal(uv, ref.uv)
