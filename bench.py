@@ -1,21 +1,26 @@
 #!/usr/bin/env python
-"""Benchmark: 1080p frames/s of the per-frame temporal-consistency step.
+"""Benchmark: 1080p frames/s of the per-frame temporal-consistency step
+(flow + warp + blend + solve), BASELINE.json's metric.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--flow fp32|bf16|constant] [--height H --width W]
 
 One process per GPU (torchrun for N > 1).  Streams are independent (SURVEY
-§8(e)): every rank runs its own 1080p stream, no collective on the data path
-(torch.distributed is used only for the timing barrier and the max over
-ranks) -> "scaling": "weak".
+§8(e)): every rank runs its own 1080p stream; torch.distributed is used only
+for the timing barrier and the max over ranks, never on the data path ->
+"scaling": "weak".
 
-A step = one stabilize_step of a 1920x1080 RGB stream: push the next
-(input, processed) pair, provide the two flows, fused warp/weights/blend (K1),
-150-iteration screened-Poisson solve (K2), commit.  The consistency params
-alternate per frame (k1 0.3/0.5 with k2 0.5/0.3, lambda 2.0/0.5), the
-"interactive local/global blend" of BASELINE config 2.
+A step = one stabilize_step of a 1920x1080 RGB stream with the lite flow CNN
+(BASELINE config 2: fp32 flow, interactive local/global blend): push the next
+(input, processed) pair; the network computes the new frame's feature pyramid
+and the two flows t->t-1, t->t+1 into the session's flow slots; the fused
+warp/weights/blend pass (K1); the 150-iteration screened-Poisson solve (K2);
+commit.  The consistency params alternate per frame (k1/k2 0.3/0.5 <-> 0.5/0.3,
+lambda 2.0 <-> 0.5).
 
-`value` is device-timed with inputs resident in HBM; `e2e` is the same step
-through the C ABI from pinned host buffers (H2D of the pair + D2H of O_t inside
+`value` is device-timed (CUDA events on the session stream, per step, L2
+flushed between steps) with the frames already in HBM; `e2e` is the same step
+through the C ABI from pinned host buffers (H2D of the pair and D2H of O_t in
 the timed region).  `--impl reference` times the CPU restatement of the
 reference step (oracle/, all host threads) on a bounded sample.
 """
@@ -37,6 +42,7 @@ sys.path.insert(0, ROOT)
 
 H, W = 1080, 1920
 METRIC = "1080p frames/s (flow+warp+blend), per stream and box aggregate at 1/2/4/8 GPU"
+SOLVER_K = 8  # iterations per temporally-blocked solver pass (csrc/solver.cu)
 
 
 def parse():
@@ -45,6 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--flow", default="fp32", choices=["fp32", "bf16", "constant"])
     ap.add_argument("--height", type=int, default=H)
     ap.add_argument("--width", type=int, default=W)
     ap.add_argument("--no-e2e", action="store_true")
@@ -53,10 +60,8 @@ def parse():
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def params_for(t):
@@ -65,6 +70,13 @@ def params_for(t):
     if t % 2 == 0:
         return ConsistencyParams(k1=0.3, k2=0.5, lam=2.0)
     return ConsistencyParams(k1=0.5, k2=0.3, lam=0.5)
+
+
+def flow_kernel_launches():
+    """Kernels the flow network launches per steady-state step: one new
+    pyramid (prep + 18 convs) and two estimator passes (L6: corr + 6 convs;
+    L5..L3: warp + corr + 6 convs; refinement 6 dw + 6 pw + 1 conv + final)."""
+    return 19 + 2 * (7 + 3 * 8 + 14)
 
 
 class ClockSampler:
@@ -85,8 +97,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
 
@@ -97,6 +108,7 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -122,59 +134,18 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def run_reference(args, rank, world):
-    """CPU restatement of the reference step (oracle/, test infrastructure)
-    timed on the host cores: the reference arm.  Rank 0 only."""
-    if rank != 0:
-        return
+# CPU restatement (oracle/): the reference arm and the cpu_baseline leg
+def _cpu_step_seconds(h, w, flow_kind, budget_s):
+    """Seconds per full step of the CPU restatement on all host threads:
+    consistency step (C, OpenMP) timed in full; the flow CNN (numpy restatement)
+    timed on a 1/16-area crop and scaled by pixel count (one new pyramid + two
+    estimator passes per step, like the GPU step)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
 
+    import flownet_oracle as fo
     import oracle as orc
-    from paper_2301_00750_b200 import synthetic
-
-    orc.build()
-    cores = os.cpu_count() or 1
-    orc.set_threads(cores)
-    h, w = args.height, args.width
-    seq = synthetic.translating_sequence(frames=3, height=h, width=w, step=(2, 1), seed=0)
-    fp = orc.constant_flow(h, w, 2, 1, -1)
-    fn = orc.constant_flow(h, w, 2, 1, 1)
-    prm = orc.Params()
-    steps = max(1, min(args.steps, 20))
-    times = []
-    for i in range(max(0, min(args.warmup, 1)) + steps):
-        t0 = time.perf_counter()
-        orc.run_step(seq.inputs[0], seq.processed[0], seq.inputs[1], seq.processed[1],
-                     seq.inputs[2], seq.processed[2], seq.processed[0], fp, fn, prm)
-        dt = time.perf_counter() - t0
-        if i >= min(args.warmup, 1):
-            times.append(dt)
-        if sum(times) > 60.0:
-            break
-    sec = sum(times) / len(times)
-    fps = 1.0 / sec
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(fps, 4), "unit": "frames/s",
-        "n_gpus": world, "steps": len(times), "warmup": min(args.warmup, 1),
-        "ms_per_step": round(sec * 1e3, 2), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{w}x{h} single-stream consistency step (default preset, "
-                               f"150 iterations, ConstantFlow(2,1) flows)",
-                   "flow": "constant (provider seam)"},
-        "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": cores,
-                         "kind": "port",
-                         "sample": f"{len(times)} full {w}x{h} steps of the C restatement "
-                                   f"(oracle/streamstab_oracle.c, OpenMP {cores} threads)"},
-        "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def cpu_baseline_sample(h, w, budget_s=20.0):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as orc
+    from paper_2301_00750_b200 import liteflownet as lf
     from paper_2301_00750_b200 import synthetic
 
     orc.build()
@@ -183,16 +154,57 @@ def cpu_baseline_sample(h, w, budget_s=20.0):
     seq = synthetic.translating_sequence(frames=3, height=h, width=w, step=(2, 1), seed=0)
     fp = orc.constant_flow(h, w, 2, 1, -1)
     fn = orc.constant_flow(h, w, 2, 1, 1)
-    times = []
-    while not times or (sum(times) < budget_s and len(times) < 3):
+    cons = []
+    while not cons or (sum(cons) < budget_s and len(cons) < 3):
         t0 = time.perf_counter()
         orc.run_step(seq.inputs[0], seq.processed[0], seq.inputs[1], seq.processed[1],
                      seq.inputs[2], seq.processed[2], seq.processed[0], fp, fn, orc.Params())
-        times.append(time.perf_counter() - t0)
-    sec = sum(times) / len(times)
-    return {"value": round(1.0 / sec, 4), "unit": "frames/s", "cores": cores, "kind": "port",
-            "sample": f"{len(times)} full {w}x{h} consistency steps, C restatement "
-                      f"(oracle/streamstab_oracle.c) on {cores} host threads"}
+        cons.append(time.perf_counter() - t0)
+    t_cons = sum(cons) / len(cons)
+    t_flow = 0.0
+    sample = f"{len(cons)} full {w}x{h} consistency steps (oracle/streamstab_oracle.c, {cores} threads)"
+    if flow_kind != "constant":
+        ch, cw = max(64, h // 4), max(64, w // 4)
+        scale = (math.ceil(h / 64) * math.ceil(w / 64)) / (math.ceil(ch / 64) * math.ceil(cw / 64))
+        wts = lf.make_weights(0)
+        a = np.ascontiguousarray(seq.inputs[1][:ch, :cw])
+        b = np.ascontiguousarray(seq.inputs[0][:ch, :cw])
+        t0 = time.perf_counter()
+        pa = fo.pyramid(wts, a)
+        t_pyr = time.perf_counter() - t0
+        pb = fo.pyramid(wts, b)
+        t0 = time.perf_counter()
+        fo.flow(wts, a, b, pyr1=pa, pyr2=pb)
+        t_est = time.perf_counter() - t0
+        t_flow = scale * (t_pyr + 2 * t_est)
+        sample += (f" + flow CNN restatement (oracle/flownet_oracle.py, numpy) timed on a "
+                   f"{cw}x{ch} crop and scaled x{scale:.1f} by area")
+    return t_cons + t_flow, cores, sample
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    h, w = args.height, args.width
+    steps = max(1, min(args.steps, 3))
+    secs, cores, sample = [], 0, ""
+    for _ in range(steps):
+        s, cores, sample = _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
+        secs.append(s)
+    sec = sum(secs) / len(secs)
+    fps = 1.0 / sec
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(fps, 5), "unit": "frames/s",
+        "n_gpus": world, "steps": len(secs), "warmup": 0, "ms_per_step": round(sec * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{w}x{h} single stream, default preset, 150 iterations, "
+                               f"flow={args.flow}"},
+        "cpu_baseline": {"value": round(fps, 5), "unit": "frames/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(fps, 5), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -219,13 +231,14 @@ def main():
     h, w = args.height, args.width
     L = _lib.lib()
     seq = DeviceSequence(h, w, step=(2, 1), seed=rank)
-    flow = ss.ConstantFlow(2, 1)
+    flow = ss.ConstantFlow(2, 1) if args.flow == "constant" else ss.LiteFlowNet(
+        seed=0, precision=args.flow)
     state = ss.SessionState(params=params_for(0))
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    # the stream's frames are generated in HBM before any timed region (a pool
-    # cycled by position; the consistency step never sees the generator)
+    # frames are generated in HBM before any timed region (a pool cycled by
+    # position; the consistency step never sees the generator)
     pool_n = 16
     pool = [seq.frame(k + 1) for k in range(pool_n)]
     torch.cuda.synchronize()
@@ -249,21 +262,22 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---- device-timed region (inputs generated in HBM) -------------------
+    # ---- device-timed region -------------------------------------------------
     sampler = ClockSampler(local)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    blend_ms, solve_ms = [], []
+    flow_ms, blend_ms, solve_ms = [], [], []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     sampler.start()
     for k in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
+        flush.zero_()  # L2 flush between timed steps, outside the events
         ev[k][0].record(stream)
         step()
         ev[k][1].record(stream)
         tm = state.last_timing
+        flow_ms.append(tm.flow_ms)
         blend_ms.append(tm.warp_blend_ms)
         solve_ms.append(tm.solve_ms)
     torch.cuda.synchronize()
@@ -276,22 +290,16 @@ def main():
     ms_per_step = total_ms / args.steps
     value = world * 1e3 / ms_per_step  # frames/s over all ranks (one stream each)
 
-    # ---- e2e through the C ABI from pinned host buffers --------------------
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(args, L, state, seq, torch, dist)
+    e2e = None if args.no_e2e else run_e2e(args, L, state, pool, flow, torch, dist)
 
-    # ---- roofline of the dominant kernel (solver pass) ---------------------
-    # stage times come from CUDA events on the session stream inside ss_step:
-    # warp_blend = K1 alone, solve = the solver passes back to back
-    n_pass = math.ceil(150 / 8)
-    med_solve = sorted(solve_ms)[len(solve_ms) // 2]
-    med_blend = sorted(blend_ms)[len(blend_ms) // 2]
+    # ---- roofline: stage times are CUDA events on the session stream ----------
+    med = lambda xs: sorted(xs)[len(xs) // 2]  # noqa: E731
+    med_flow, med_blend, med_solve = med(flow_ms), med(blend_ms), med(solve_ms)
+    n_pass = math.ceil(150 / SOLVER_K)
     per_pass_ms = med_solve / n_pass
-    flops_per_pass = 14.0 * h * w * 3 * 8  # algorithmic FP32 ops, no halo redundancy
-    fp32_peak = 148 * 128 * 1.965e9 / 1e12  # non-FMA FP32 op rate at max SM clock, TOP/s
+    flops_per_pass = 14.0 * h * w * 3 * SOLVER_K  # algorithmic FP32 ops, SURVEY 8(d)
+    fp32_peak = 148 * 128 * 1.965e9 / 1e12
     achieved = flops_per_pass / (per_pass_ms * 1e-3) / 1e12
-    k1_bytes = 130.0 * h * w  # K1 algorithmic bytes per launch
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -299,9 +307,9 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    k1_gbs = k1_bytes / (med_blend * 1e-3) / 1e9
+    k1_gbs = 130.0 * h * w / (med_blend * 1e-3) / 1e9
     roofline = {
-        "kernel": "k_sgd_blocked (solver pass = 8 SGD-momentum iterations)",
+        "kernel": f"k_sgd_tma<{SOLVER_K}> (solver pass = {SOLVER_K} SGD-momentum iterations)",
         "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 2),
         "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": None,
         "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1965 MHz non-FMA op rate "
@@ -315,24 +323,30 @@ def main():
     }
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(h, w)
-    launches_per_step = 2 + 1 + n_pass  # 2 flow fills, K1, solver passes
+        sec, cores, sample = _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
+        cpu = {"value": round(1.0 / sec, 5), "unit": "frames/s", "cores": cores, "kind": "port",
+               "sample": sample}
+    launches = 1 + n_pass + (2 if args.flow == "constant" else flow_kernel_launches())
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"{w}x{h} single stream per GPU, default preset with per-frame "
-                               "interactive k1/k2/lambda schedule, 150 solver iterations",
-                   "flow": "ConstantFlow(2,1) on device (provider seam; lite flow CNN not yet "
-                           "in the step)",
+        "config": {"workload": f"{w}x{h} single stream per GPU, lite flow CNN ({args.flow}) + "
+                               "default preset with per-frame interactive k1/k2/lambda schedule, "
+                               "150 solver iterations",
+                   "flow": {"fp32": "lite flow CNN, fp32 (CUDA-core FFMA convs), random-init "
+                                    "seeded weights",
+                            "bf16": "lite flow CNN, bf16 tcgen05 convs, random-init seeded "
+                                    "weights",
+                            "constant": "ConstantFlow(2,1) on device"}[args.flow],
                    "streams_per_gpu": 1, "l2": "flushed between timed steps (256 MiB write)",
-                   "stage_ms_median": {"warp_blend": round(med_blend, 4),
+                   "stage_ms_median": {"flow": round(med_flow, 4), "warp_blend": round(med_blend, 4),
                                        "solve": round(med_solve, 4)}},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches * args.steps,
         "clocks": clocks,
     }
     if rank == 0:
@@ -341,29 +355,33 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(args, L, state, seq, torch, dist):
+def run_e2e(args, L, state, pool, flow, torch, dist):
     """The same step through the C ABI from pinned host memory."""
     from paper_2301_00750_b200 import _lib
     from paper_2301_00750_b200._dev import params_struct
 
     h, w = args.height, args.width
     n_host = 4
-    host_i, host_p = [], []
-    for k in range(n_host):
-        i, p = seq.frame(1000 + k)
-        host_i.append(i.cpu().pin_memory())
-        host_p.append(p.cpu().pin_memory())
+    host_i = [pool[k][0].cpu().pin_memory() for k in range(n_host)]
+    host_p = [pool[k][1].cpu().pin_memory() for k in range(n_host)]
     out = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
     sess = state.handle
     pos = [int(L.ss_solved_through(sess)) + 1]  # last pushed position
+    use_cnn = args.flow != "constant"
+    if use_cnn:
+        _check(L.ss_session_attach_flownet(sess, flow.handle()), L)
 
     def step(k):
         pos[0] += 1
         _check(L.ss_push_pair(sess, pos[0], host_i[k % n_host].data_ptr(),
                               host_p[k % n_host].data_ptr(), _lib.SS_F32, _lib.SS_HOST), L)
         t = int(L.ss_solved_through(sess)) + 1
-        _check(L.ss_set_constant_flow(sess, 0, 2.0, 1.0, -1), L)
-        _check(L.ss_set_constant_flow(sess, 1, 2.0, 1.0, 1), L)
+        if use_cnn:
+            _check(L.ss_session_compute_flow(sess, 0), L)
+            _check(L.ss_session_compute_flow(sess, 1), L)
+        else:
+            _check(L.ss_set_constant_flow(sess, 0, 2.0, 1.0, -1), L)
+            _check(L.ss_set_constant_flow(sess, 1, 2.0, 1.0, 1), L)
         prm = params_struct(params_for(t))
         it = ctypes.c_int(0)
         _check(L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)), L)
@@ -386,9 +404,9 @@ def run_e2e(args, L, state, seq, torch, dist):
     world = dist.get_world_size() if dist else 1
     return {"value": round(world * args.steps / dt, 3), "unit": "frames/s",
             "h2d_bytes_per_step": 2 * h * w * 3 * 4, "d2h_bytes_per_step": h * w * 3 * 4,
-            "path": "C ABI: ss_push_pair(host pinned f32) + ss_set_constant_flow x2 + ss_step "
-                    "+ ss_output(host)", "timer": "host wall clock around K steps, "
-                                                  "device synchronised at both ends"}
+            "path": "C ABI: ss_push_pair(host pinned f32) + ss_session_compute_flow x2 + ss_step "
+                    "+ ss_output(host pinned)",
+            "timer": "host wall clock around K steps, device synchronised at both ends"}
 
 
 def _check(rc, L):

@@ -429,8 +429,13 @@ def _run_step(state: SessionState, flow_backend, with_next: bool, return_host: b
     _lib.lib().ss_last_timing(state.handle, ctypes.byref(tm))
     state._first_output = None
     state._out_cache = None
-    state.last_timing = StepTiming(flow_ms=flow_ms, solve_ms=solve_ms,
-                                   warp_blend_ms=float(tm.warp_blend_ms))
+    # device (CUDA-event) times when available: the flow network's kernels
+    # run asynchronously, so the host clock around the provider calls would
+    # only see the launches
+    state.last_timing = StepTiming(
+        flow_ms=float(tm.flow_ms) if tm.flow_ms > 0 else flow_ms,
+        solve_ms=float(tm.solve_ms) if tm.solve_ms > 0 else solve_ms,
+        warp_blend_ms=float(tm.warp_blend_ms))
     if not return_host:
         return state.output_device()
     out = state.output_host()
