@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-PYR_CH = (16, 32, 64, 96, 128, 196)
+PYR_CH = (16, 32, 64, 96, 128, 192)
 MD = 4
 LEAKY = 0.1
 
@@ -24,7 +24,7 @@ def _leaky(x):
 
 
 def prep(img):
-    """(H, W, C) in [0, 1] -> (H64, W64, 4): RGB - 0.5, replicate pad, zero 4th ch."""
+    """(H, W, C) in [0, 1] -> (H64, W64, 8): RGB - 0.5, replicate pad, zero ch 3..7."""
     img = np.asarray(img, np.float32)
     if img.ndim == 2:
         img = img[:, :, None]
@@ -34,7 +34,7 @@ def prep(img):
     H, W = -(-h // 64) * 64, -(-w // 64) * 64
     ys = np.minimum(np.arange(H), h - 1)
     xs = np.minimum(np.arange(W), w - 1)
-    out = np.zeros((H, W, 4), np.float32)
+    out = np.zeros((H, W, 8), np.float32)
     out[:, :, :3] = img[ys][:, xs] - np.float32(0.5)
     return out
 
@@ -145,15 +145,15 @@ def flow(weights, img1, img2, pyr1=None, pyr2=None):
         f1, f2 = p1[lvl - 1], p2[lvl - 1]
         H, W, C = f1.shape
         if lvl == 6:
-            x = np.zeros((H, W, 84), np.float32)
+            x = np.zeros((H, W, 88), np.float32)
             x[:, :, :81] = _leaky(corr(f1, f2))
         else:
             up = (2.0 * _bilinear_resize(fl, H, W)).astype(np.float32)
             w2 = warp_zero(f2, up)
-            x = np.zeros((H, W, 88 + C), np.float32)
+            x = np.zeros((H, W, 96 + C), np.float32)
             x[:, :, :81] = _leaky(corr(f1, w2))
-            x[:, :, 84:86] = up
-            x[:, :, 88:] = f1
+            x[:, :, 88:90] = up
+            x[:, :, 96:] = f1
         e1 = conv(x, *weights[f"est{lvl}_1"])
         e2 = conv(e1, *weights[f"est{lvl}_2"])
         e3 = conv(e2, *weights[f"est{lvl}_3"])
@@ -162,7 +162,7 @@ def flow(weights, img1, img2, pyr1=None, pyr2=None):
         w6, b6 = weights[f"est{lvl}_6"]
         fl = conv(np.concatenate([e5, e4], axis=2), w6, b6, act=False)
     # separable refinement at level 3
-    r = np.concatenate([fl, np.zeros(fl.shape[:2] + (2,), np.float32), e5, e4], axis=2)
+    r = np.concatenate([fl, np.zeros(fl.shape[:2] + (6,), np.float32), e5, e4], axis=2)
     for i, d in enumerate((1, 2, 4, 8, 16, 1), start=1):
         wd, _ = weights[f"ref{i}_dw"]
         r = depthwise(r, wd, d)

@@ -11,10 +11,11 @@
 namespace ss {
 namespace fn {
 
-static const int PYR_CH[6] = {16, 32, 64, 96, 128, 196};
-static inline int pad4(int c) { return (c + 3) / 4 * 4; }
-static inline int est_in(int lvl) { return lvl == 6 ? 84 : 88 + PYR_CH[lvl - 1]; }
-constexpr int E_LD = 196;  // [flow 2 | 0 0 | e5 32 | e4 64 | e3 96]
+static const int PYR_CH[6] = {16, 32, 64, 96, 128, 192};
+static inline int pad16(int c) { return (c + 15) / 16 * 16; }
+static inline int est_in(int lvl) { return lvl == 6 ? 88 : 96 + PYR_CH[lvl - 1]; }
+// estimator features: [flow 2 | 0 x6 | e5 32 | e4 64 | e3 96]
+constexpr int E_LD = 200, E5_OFF = 8, E4_OFF = 40, E3_OFF = 104;
 
 // layer indices (same order as liteflownet.layer_table())
 static inline int pyr_idx(int lvl, int j) { return (lvl - 1) * 3 + j; }          // j: 0 a, 1 b, 2 c
@@ -27,16 +28,16 @@ static std::vector<LayerDev> table()
     std::vector<LayerDev> L;
     auto conv = [&](int cin, int cout, int k, int stride, int dil, int act) {
         LayerDev d;
-        d.cin = cin; d.cout = cout; d.cout_pad = pad4(cout); d.k = k; d.stride = stride;
+        d.cin = cin; d.cout = cout; d.cout_pad = pad16(cout); d.k = k; d.stride = stride;
         d.dil = dil; d.act = act; d.dw = false;
         L.push_back(d);
     };
-    int cin = 4;
+    int cin = 8;
     for (int l = 1; l <= 6; ++l) {
         conv(cin, PYR_CH[l - 1], 3, 2, 1, 1);
-        conv(pad4(PYR_CH[l - 1]), PYR_CH[l - 1], 3, 1, 1, 1);
-        conv(pad4(PYR_CH[l - 1]), PYR_CH[l - 1], 3, 1, 1, 1);
-        cin = pad4(PYR_CH[l - 1]);
+        conv(PYR_CH[l - 1], PYR_CH[l - 1], 3, 1, 1, 1);
+        conv(PYR_CH[l - 1], PYR_CH[l - 1], 3, 1, 1, 1);
+        cin = PYR_CH[l - 1];
     }
     for (int lvl = 6; lvl >= 3; --lvl) {
         conv(est_in(lvl), 128, 3, 1, 1, 1);
@@ -46,7 +47,7 @@ static std::vector<LayerDev> table()
         conv(64 + 96, 32, 3, 1, 1, 1);
         conv(32 + 64, 2, 3, 1, 1, 0);
     }
-    const int sep[6][3] = {{100, 128, 1}, {128, 128, 2}, {128, 128, 4},
+    const int sep[6][3] = {{104, 128, 1}, {128, 128, 2}, {128, 128, 4},
                            {128, 96, 8},  {96, 64, 16},  {64, 32, 1}};
     for (auto &s : sep) {
         LayerDev d;
@@ -143,7 +144,7 @@ int Run::init(const Weights *wt, int h_, int w_)
     };
     const size_t px1 = (size_t)H[1] * W[1];
     int rc;
-    if ((rc = alloc(&prep, (size_t)H[0] * W[0] * 4))) return rc;
+    if ((rc = alloc(&prep, (size_t)H[0] * W[0] * 8))) return rc;
     if ((rc = alloc(&s0, px1 * 16))) return rc;
     if ((rc = alloc(&s1, px1 * 16))) return rc;
     for (auto &sl : slots)
@@ -197,7 +198,7 @@ int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st
     int rc;
     if ((rc = launch_prep(img, h, w, c, H[0], W[0], prep, st))) return rc;
     const float *in = prep;
-    int in_ld = 4;
+    int in_ld = 8;
     for (int l = 1; l <= 6; ++l) {
         const int C = PYR_CH[l - 1];
         float *a = l <= 2 ? (in == s0 ? s1 : s0) : (in == s0 ? s1 : s0);
@@ -230,16 +231,16 @@ int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
         const int hh = H[l], ww = W[l];
         if ((rc = conv(wts->L(est_idx(l, 1)), x[l], X, hh, ww, e1[l], 128, st))) return rc;
         if ((rc = conv(wts->L(est_idx(l, 2)), e1[l], 128, hh, ww, e2[l], 128, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 3)), e2[l], 128, hh, ww, E[l] + 100, E_LD, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 4)), E[l] + 100, E_LD, hh, ww, E[l] + 36, E_LD, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 5)), E[l] + 36, E_LD, hh, ww, E[l] + 4, E_LD, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 6)), E[l] + 4, E_LD, hh, ww, E[l], E_LD, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 3)), e2[l], 128, hh, ww, E[l] + E3_OFF, E_LD, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 4)), E[l] + E3_OFF, E_LD, hh, ww, E[l] + E4_OFF, E_LD, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 5)), E[l] + E4_OFF, E_LD, hh, ww, E[l] + E5_OFF, E_LD, st))) return rc;
+        if ((rc = conv(wts->L(est_idx(l, 6)), E[l] + E5_OFF, E_LD, hh, ww, E[l], E_LD, st))) return rc;
     }
-    // separable refinement at level 3: r_in = E[3][0:100]
+    // separable refinement at level 3: r_in = E[3][0:104]
     const int hh = H[3], ww = W[3];
     const float *in = E[3];
     int in_ld = E_LD;
-    const int cin[6] = {100, 128, 128, 128, 96, 64};
+    const int cin[6] = {104, 128, 128, 128, 96, 64};
     for (int i = 1; i <= 6; ++i) {
         const LayerDev &dw = wts->L(ref_idx(i, false));
         if ((rc = launch_depthwise(in, in_ld, hh, ww, cin[i - 1], dw.w, dw.dil, ra, 128, st))) return rc;

@@ -209,8 +209,8 @@ int launch_depthwise(const float *in, int ld, int H, int W, int C, const float *
 }
 
 // ---------------------------------------------------------------------------
-// network input: (h, w, c) HWC in [0,1] -> (H64, W64, 4) NHWC, RGB - 0.5,
-// replicate padding, zero 4th channel; grey input is replicated to RGB
+// network input: (h, w, c) HWC in [0,1] -> (H64, W64, 8) NHWC, RGB - 0.5,
+// replicate padding, zero channels 3..7; grey input is replicated to RGB
 __global__ void k_prep(const float *__restrict__ img, int h, int w, int c, int H, int W,
                        float *__restrict__ out)
 {
@@ -226,7 +226,8 @@ __global__ void k_prep(const float *__restrict__ img, int h, int w, int c, int H
     } else {
         r = g = b = img[q];
     }
-    reinterpret_cast<float4 *>(out)[i] = make_float4(r - 0.5f, g - 0.5f, b - 0.5f, 0.f);
+    reinterpret_cast<float4 *>(out)[2 * i] = make_float4(r - 0.5f, g - 0.5f, b - 0.5f, 0.f);
+    reinterpret_cast<float4 *>(out)[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st)
@@ -247,7 +248,7 @@ __device__ __forceinline__ void src_coord(int d, float inv_scale, int n, int &i0
     f = s - (float)i0;
 }
 
-// up = 2 * bilinear_x2(coarse flow) -> x[:, 84:86]; w2 = warp_zero(f2, up)
+// up = 2 * bilinear_x2(coarse flow) -> x[:, 88:90]; w2 = warp_zero(f2, up)
 __global__ void k_up2_warp(const float *__restrict__ coarse, int cld, int Hc, int Wc,
                            const float *__restrict__ f2, int C, int H, int W,
                            float *__restrict__ x, int xld, float *__restrict__ w2)
@@ -267,8 +268,8 @@ __global__ void k_up2_warp(const float *__restrict__ coarse, int cld, int Hc, in
         const float top = a * (1.f - fx) + b * fx, bot = c * (1.f - fx) + d * fx;
         up[k] = 2.f * (top * (1.f - fy) + bot * fy);
     }
-    x[i * xld + 84] = up[0];
-    x[i * xld + 85] = up[1];
+    x[i * xld + 88] = up[0];
+    x[i * xld + 89] = up[1];
     const float sx = (float)xx + up[0], sy = (float)y + up[1];
     const float gx0 = floorf(sx), gy0 = floorf(sy);
     const int ix = (int)gx0, iy = (int)gy0;
@@ -304,7 +305,7 @@ int launch_up2_warp(const float *coarse, int cld, int Hc, int Wc, const float *f
 
 // ---------------------------------------------------------------------------
 // cost volume: x[:, d] = leaky(sum_c f1_c * w2_c(p + d) / C), d in [-4,4]^2;
-// also copies f1 into x[:, 88:88+C] (l < 6).  16x16 pixel tile, channels
+// also copies f1 into x[:, 96:96+C] (l < 6).  16x16 pixel tile, channels
 // staged 16 at a time with a 4-pixel halo of w2.
 constexpr int CT = 16, CH = 8, HALO = 4, CW = CT + 2 * HALO;
 
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(CT *CT) k_corr(const float *__restrict__ f1,
     for (int d = 0; d < 81; ++d) dst[d] = leaky(acc[d] * inv);
     if (copy_f1)
         for (int c = 0; c < C; c += 4)
-            *reinterpret_cast<float4 *>(dst + 88 + c) = *reinterpret_cast<const float4 *>(f1 + pix * C + c);
+            *reinterpret_cast<float4 *>(dst + 96 + c) = *reinterpret_cast<const float4 *>(f1 + pix * C + c);
 }
 
 int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x, int xld,

@@ -9,29 +9,29 @@ two estimator layers ("light"), the quarter-resolution estimator removed
 down once here and restated independently by the CPU checker:
 
 Feature pyramid (shared by both frames), 3x3 convs + LeakyReLU(0.1):
-    L1  4->16 s2, 16->16, 16->16          (input RGB - 0.5, zero 4th channel)
+    L1  8->16 s2, 16->16, 16->16          (input RGB - 0.5, zero channels 3..7)
     L2 16->32 s2, 32->32, 32->32
     L3 32->64 s2, 64->64, 64->64
     L4 64->96 s2, 96->96, 96->96
     L5 96->128 s2, 128->128, 128->128
-    L6 128->196 s2, 196->196, 196->196
+    L6 128->192 s2, 192->192, 192->192   (PWC-Net uses 196; 192 keeps every width a multiple of 16)
 Estimator at level l in (6, 5, 4, 3):
     up   = 2 * bilinear_x2(flow_{l+1})             (l < 6)
     w2   = bilinear warp of f2_l by up (zeros outside)
-    x    = [LeakyReLU(corr(f1_l, w2)) 81 | 0 0 0 | up 2 | 0 0 | f1_l C_l]  (l = 6: corr only)
+    x    = [LeakyReLU(corr(f1_l, w2)) 81 | 0 x7 | up 2 | 0 x6 | f1_l C_l]  (l = 6: corr | 0 x7)
     e1 = conv(x, 128); e2 = conv(e1, 128); e3 = conv(e2, 96); e4 = conv(e3, 64)
     e5 = conv([e4, e3], 32);  flow_l = conv([e5, e4], 2)  (no activation)
 Refinement at level 3 (depthwise-separable, dilations 1 2 4 8 16 1):
-    r_in = [flow_3 2 | 0 0 | e5 32 | e4 64]
-    sep(100->128,d1) sep(128->128,d2) sep(128->128,d4) sep(128->96,d8)
+    r_in = [flow_3 2 | 0 x6 | e5 32 | e4 64]
+    sep(104->128,d1) sep(128->128,d2) sep(128->128,d4) sep(128->96,d8)
     sep(96->64,d16) sep(64->32,d1), conv3x3(32->2); flow_3 += r
 Output: 8 * bilinear_x8(flow_3), cropped to the frame (network input is the
 frame replicate-padded to a multiple of 64).  corr(a, b)[d] = sum_c a_c b_c(x+d)
 / C over the 9x9 displacements d in [-4, 4]^2 (row-major dy, dx), zeros
 outside; bilinear sampling is at pixel centres (align_corners=False).
 
-Channel counts are padded to multiples of 4 (zero weights), so every NHWC
-buffer row is 16-byte aligned.  Weights are random-init (no checkpoint is
+Channel groups are padded to multiples of 8 (zero weights), so a 16-byte chunk
+of fp32 (4 ch) or bf16 (8 ch) activations never straddles a filter tap.  Weights are random-init (no checkpoint is
 available offline) from a seeded generator; ``layer_table()`` fixes the order
 in which they are flattened for the C ABI.
 """
@@ -42,22 +42,22 @@ from dataclasses import dataclass
 
 import numpy as np
 
-PYR_CH = (16, 32, 64, 96, 128, 196)
+PYR_CH = (16, 32, 64, 96, 128, 192)
 EST_LEVELS = (6, 5, 4, 3)
 MD = 4
 N_DISP = (2 * MD + 1) ** 2
 LEAKY = 0.1
 
 
-def pad4(c: int) -> int:
-    return (c + 3) // 4 * 4
+def pad8(c: int) -> int:
+    return (c + 7) // 8 * 8
 
 
 def est_in_channels(level: int) -> int:
     """Padded channel count of the estimator input x at ``level``."""
     if level == 6:
-        return pad4(N_DISP)  # 84
-    return pad4(N_DISP) + 4 + PYR_CH[level - 1]
+        return pad8(N_DISP)  # 88
+    return pad8(N_DISP) + 8 + PYR_CH[level - 1]
 
 
 @dataclass(frozen=True)
@@ -84,12 +84,12 @@ class Layer:
 
 def layer_table() -> list[Layer]:
     L = []
-    cin = 4
+    cin = 8
     for lvl, c in enumerate(PYR_CH, start=1):
         L.append(Layer(f"pyr{lvl}a", "conv", cin, c, stride=2))
-        L.append(Layer(f"pyr{lvl}b", "conv", pad4(c), c))
-        L.append(Layer(f"pyr{lvl}c", "conv", pad4(c), c))
-        cin = pad4(c)
+        L.append(Layer(f"pyr{lvl}b", "conv", c, c))
+        L.append(Layer(f"pyr{lvl}c", "conv", c, c))
+        cin = c
     for lvl in EST_LEVELS:
         x = est_in_channels(lvl)
         L.append(Layer(f"est{lvl}_1", "conv", x, 128))
@@ -98,7 +98,7 @@ def layer_table() -> list[Layer]:
         L.append(Layer(f"est{lvl}_4", "conv", 96, 64))
         L.append(Layer(f"est{lvl}_5", "conv", 64 + 96, 32))
         L.append(Layer(f"est{lvl}_6", "conv", 32 + 64, 2, act=False))
-    sep = [(100, 128, 1), (128, 128, 2), (128, 128, 4), (128, 96, 8), (96, 64, 16), (64, 32, 1)]
+    sep = [(104, 128, 1), (128, 128, 2), (128, 128, 4), (128, 96, 8), (96, 64, 16), (64, 32, 1)]
     for i, (ci, co, d) in enumerate(sep, start=1):
         L.append(Layer(f"ref{i}_dw", "dw", ci, ci, dil=d, act=False))
         L.append(Layer(f"ref{i}_pw", "conv", ci, co, k=1))
@@ -118,11 +118,11 @@ def _live_rows(layer: Layer) -> np.ndarray:
     elif n.startswith("pyr") and n[-1] == "a":
         live[PYR_CH[int(n[3]) - 2]:] = False
     elif n.endswith("_1"):
-        live[N_DISP:pad4(N_DISP)] = False
+        live[N_DISP:pad8(N_DISP)] = False
         if n != "est6_1":
-            live[pad4(N_DISP) + 2:pad4(N_DISP) + 4] = False
+            live[pad8(N_DISP) + 2:pad8(N_DISP) + 8] = False
     elif n in ("ref1_dw", "ref1_pw"):
-        live[2:4] = False
+        live[2:8] = False
     return live
 
 

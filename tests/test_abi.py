@@ -80,7 +80,8 @@ def test_flownet_param_count_matches_layer_table(lib):
     assert lib.ss_flownet_num_params() == lf.n_params() == lf.flatten_weights(w).size
     # padding rows are exactly zero; live rows are not
     w1, _ = w["est5_1"]
-    assert not w1[:, :, 81:84].any() and not w1[:, :, 86:88].any() and w1[:, :, 88:].any()
+    assert not w1[:, :, 81:88].any() and not w1[:, :, 90:96].any() and w1[:, :, 96:].any()
+    assert w1[:, :, 88:90].any()
 
 
 def test_flownet_oracle_shapes():
