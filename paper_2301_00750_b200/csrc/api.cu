@@ -608,6 +608,15 @@ int ss_flows(const ss_session *s, int which, float *uv_dst, uint8_t *valid_dst, 
 }
 
 // ---- lite flow network ----------------------------------------------------------
+// fp32 -> 3xTF32 on tcgen05 (fp32-class accuracy); bf16 -> bf16 tcgen05;
+// SS_FLOW_CONV=ffma forces the CUDA-core FFMA implicit GEMM (cross-check)
+static int conv_mode_for(int precision)
+{
+    const char *e = getenv("SS_FLOW_CONV");
+    if (e && !strcmp(e, "ffma")) return fn::CONV_FFMA;
+    return precision == SS_FLOW_BF16 ? fn::CONV_TC_BF16 : fn::CONV_TC_TF32X3;
+}
+
 int64_t ss_flownet_num_params(void) { return fn::Weights::expected_params(); }
 
 int ss_flownet_create(const float *weights, int64_t n, int precision, ss_flownet **out)
@@ -648,6 +657,7 @@ int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b,
         }
     }
     cudaStream_t st = (cudaStream_t)stream;
+    run->conv_mode = conv_mode_for(net->precision);
     if (int rc = run->pyramid(0, -1, frame_a, c, st)) return rc;
     if (int rc = run->pyramid(1, -1, frame_b, c, st)) return rc;
     return run->flow(0, 1, uv, valid, st);
@@ -663,6 +673,7 @@ int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
         s->net = nullptr;
         return rc;
     }
+    s->run->conv_mode = conv_mode_for(net->precision);
     return SS_OK;
 }
 

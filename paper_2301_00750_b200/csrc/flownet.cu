@@ -60,7 +60,11 @@ static std::vector<LayerDev> table()
     return L;
 }
 
-Weights::~Weights() { cudaFree(block); }
+Weights::~Weights()
+{
+    cudaFree(block);
+    cudaFree(tc_block);
+}
 
 int Weights::expected_params()
 {
@@ -117,6 +121,59 @@ int Weights::upload(const float *host, int64_t n)
         layers[i].w = block + woff[i];
         layers[i].b = block + boff[i];
     }
+
+    // tensor-core weight stages (flownet_tc.cu): per K stage, N = cout_pad rows
+    // of 128 bytes of K in the core-matrix layout
+    //   byte(n, kb) = (n / 8) * 1024 + (kb / 16) * 128 + (n % 8) * 16 + kb % 16
+    // bf16: 64 K per stage; 3xTF32: 32 K per stage, (hi, lo) blocks
+    auto core_off = [](int n, int kb) {
+        return (size_t)(n / 8) * 1024 + (size_t)(kb / 16) * 128 + (size_t)(n % 8) * 16 + kb % 16;
+    };
+    std::vector<size_t> obf(layers.size(), 0), otf(layers.size(), 0);
+    size_t tc_total = 0;
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        const int K = l.k * l.k * l.cin, N = l.cout_pad;
+        obf[i] = tc_total;
+        tc_total += (size_t)((K + 63) / 64) * N * 128;
+        otf[i] = tc_total;
+        tc_total += (size_t)((K + 31) / 32) * 2 * N * 128;
+    }
+    std::vector<uint8_t> tch(tc_total, 0);
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        const int K = l.k * l.k * l.cin, N = l.cout_pad;
+        const float *wl = dev.data() + woff[i];  // [K][cout_pad]
+        for (int k = 0; k < K; ++k) {
+            for (int n = 0; n < l.cout; ++n) {
+                const float f = wl[(size_t)k * N + n];
+                uint32_t u;
+                std::memcpy(&u, &f, 4);
+                // bf16, round to nearest even
+                const uint16_t bf = (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+                std::memcpy(&tch[obf[i] + (size_t)(k / 64) * N * 128 + core_off(n, (k % 64) * 2)], &bf, 2);
+                // tf32 hi (truncated) / lo (exact remainder)
+                const uint32_t hu = u & 0xffffe000u;
+                float hi, lo;
+                std::memcpy(&hi, &hu, 4);
+                lo = f - hi;
+                const size_t st = otf[i] + (size_t)(k / 32) * 2 * N * 128;
+                std::memcpy(&tch[st + core_off(n, (k % 32) * 4)], &hi, 4);
+                std::memcpy(&tch[st + (size_t)N * 128 + core_off(n, (k % 32) * 4)], &lo, 4);
+            }
+        }
+    }
+    cudaFree(tc_block);
+    tc_block = nullptr;
+    SS_CUDA_TRY(cudaMalloc(&tc_block, tc_total));
+    SS_CUDA_TRY(cudaMemcpy(tc_block, tch.data(), tc_total, cudaMemcpyHostToDevice));
+    for (size_t i = 0; i < layers.size(); ++i) {
+        if (layers[i].dw) continue;
+        layers[i].tc_bf16 = static_cast<uint8_t *>(tc_block) + obf[i];
+        layers[i].tc_tf32 = static_cast<uint8_t *>(tc_block) + otf[i];
+    }
     return SS_OK;
 }
 
@@ -165,10 +222,13 @@ int Run::init(const Weights *wt, int h_, int w_)
     return SS_OK;
 }
 
+static thread_local int conv_mode_ = CONV_TC_TF32X3;  // set by the Run issuing the convs
+
 static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, float *out,
                 int out_ld, cudaStream_t st)
 {
     ConvParams p;
+    p.wtc = conv_mode_ == CONV_TC_BF16 ? L.tc_bf16 : L.tc_tf32;
     p.in = in;
     p.in_ld = in_ld;
     p.H = Hi;
@@ -187,7 +247,8 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
     p.Ho = (Hi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.Wo = (Wi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.act = L.act;
-    return launch_conv_ffma(p, st);
+    if (conv_mode_ == CONV_FFMA) return launch_conv_ffma(p, st);
+    return launch_conv_tc(p, conv_mode_ == CONV_TC_BF16 ? 0 : 1, st);
 }
 
 int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st)
@@ -195,6 +256,7 @@ int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st
     Slot &sl = slots[slot];
     if (key >= 0 && sl.key == key) return SS_OK;  // key < 0: never cached
     sl.key = -1;
+    conv_mode_ = conv_mode;
     int rc;
     if ((rc = launch_prep(img, h, w, c, H[0], W[0], prep, st))) return rc;
     const float *in = prep;
@@ -216,6 +278,7 @@ int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st
 
 int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
 {
+    conv_mode_ = conv_mode;
     int rc;
     for (int l = 6; l >= 3; --l) {
         const int C = PYR_CH[l - 1], X = est_in(l);

@@ -21,9 +21,14 @@ struct ConvParams {
     float *out;
     int out_ld, Ho, Wo;
     int k, stride, dil, pad, act;
+    const void *wtc;            // tensor-core weight stages (flownet_tc.cu layout)
 };
 
+enum ConvMode { CONV_FFMA = 0, CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
+
 int launch_conv_ffma(const ConvParams &p, cudaStream_t st);
+// kind 0: bf16 operands (kind::f16); kind 1: 3xTF32 (kind::tf32)
+int launch_conv_tc(const ConvParams &p, int kind, cudaStream_t st);
 int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,
                      float *out, int ld_out, cudaStream_t st);
 int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st);
@@ -38,12 +43,14 @@ struct LayerDev {
     int cin, cout, cout_pad, k, stride, dil, act;
     bool dw;
     float *w = nullptr, *b = nullptr;
+    const void *tc_bf16 = nullptr, *tc_tf32 = nullptr;  // tensor-core stage layouts
 };
 
 // Weights on one device, in liteflownet.layer_table() order.
 struct Weights {
     std::vector<LayerDev> layers;
     float *block = nullptr;
+    void *tc_block = nullptr;
     ~Weights();
     static int expected_params();
     int upload(const float *host, int64_t n);
@@ -55,6 +62,7 @@ struct Weights {
 // the two steps that see it as a neighbour and the one that sees it as I_t).
 struct Run {
     const Weights *wts = nullptr;
+    int conv_mode = CONV_TC_TF32X3;
     int h = 0, w = 0, H[7] = {0}, W[7] = {0};
     float *prep = nullptr, *s0 = nullptr, *s1 = nullptr;
     struct Slot {

@@ -42,6 +42,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib as _lib_mod
+
 PYR_CH = (16, 32, 64, 96, 128, 192)
 EST_LEVELS = (6, 5, 4, 3)
 MD = 4
@@ -198,13 +200,12 @@ class LiteFlowNet:
         return self._nets[dev.index]
 
     def __del__(self):
-        from . import _lib
-
-        if _lib._lib is None:
+        lib = _lib_mod._lib
+        if lib is None:
             return
         for h in getattr(self, "_nets", {}).values():
             try:
-                _lib.lib().ss_flownet_destroy(h)
+                lib.ss_flownet_destroy(h)
             except Exception:
                 pass
 
