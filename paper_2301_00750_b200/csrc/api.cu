@@ -674,7 +674,8 @@ int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
         return rc;
     }
     s->run->conv_mode = conv_mode_for(net->precision);
-    return SS_OK;
+    s->run->use_graphs = getenv("SS_FLOW_GRAPHS") == nullptr || strcmp(getenv("SS_FLOW_GRAPHS"), "0");
+    return fn::prepare_conv_tc();
 }
 
 int ss_session_compute_flow(ss_session *s, int which)

@@ -179,6 +179,10 @@ int Weights::upload(const float *host, int64_t n)
 
 Run::~Run()
 {
+    for (auto &g : pyr_graphs)
+        if (g.second) cudaGraphExecDestroy(g.second);
+    for (auto &g : flow_graphs)
+        if (g.second) cudaGraphExecDestroy(g.second);
     for (void *p : allocs) cudaFree(p);
 }
 
@@ -219,16 +223,66 @@ int Run::init(const Weights *wt, int h_, int w_)
     if ((rc = alloc(&ra, px3 * 128))) return rc;
     if ((rc = alloc(&rb, px3 * 128))) return rc;
     if ((rc = alloc(&rr, px3 * 4))) return rc;
+    ws_floats = 6u << 20;  // 24 MB of split-K partials
+    if ((rc = alloc(&ws, ws_floats))) return rc;
     return SS_OK;
 }
 
 static thread_local int conv_mode_ = CONV_TC_TF32X3;  // set by the Run issuing the convs
+static thread_local float *ws_ = nullptr;
+static thread_local size_t ws_floats_ = 0;
+
+// SS_FLOW_PROFILE=1: per-launch device times of the network (CUDA events),
+// printed to stderr after every pyramid / flow call (diagnostics only)
+namespace {
+struct Prof {
+    bool on = getenv("SS_FLOW_PROFILE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    void mark(const std::string &name, cudaStream_t st)
+    {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        marks.emplace_back(name, e);
+    }
+    void dump(const char *what)
+    {
+        if (!on || marks.size() < 2) return;
+        cudaEventSynchronize(marks.back().second);
+        float total = 0.f;
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+            total += ms;
+            fprintf(stderr, "[flow-prof] %s %-12s %8.1f us\n", what, marks[i].first.c_str(), ms * 1e3f);
+        }
+        fprintf(stderr, "[flow-prof] %s total %.3f ms\n", what, total);
+        for (auto &m : marks) cudaEventDestroy(m.second);
+        marks.clear();
+    }
+};
+thread_local Prof prof;
+}  // namespace
+
+static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, float *out,
+                int out_ld, cudaStream_t st);
+
+static int convp(const char *name, const LayerDev &L, const float *in, int in_ld, int Hi, int Wi,
+                 float *out, int out_ld, cudaStream_t st)
+{
+    const int rc = conv(L, in, in_ld, Hi, Wi, out, out_ld, st);
+    prof.mark(name, st);
+    return rc;
+}
 
 static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, float *out,
                 int out_ld, cudaStream_t st)
 {
     ConvParams p;
     p.wtc = conv_mode_ == CONV_TC_BF16 ? L.tc_bf16 : L.tc_tf32;
+    p.ws = ws_;
+    p.ws_floats = ws_floats_;
     p.in = in;
     p.in_ld = in_ld;
     p.H = Hi;
@@ -251,26 +305,40 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
     return launch_conv_tc(p, conv_mode_ == CONV_TC_BF16 ? 0 : 1, st);
 }
 
+// capture fn(st) into a graph (thread-local capture mode) and instantiate it
+template <class F>
+static int capture(cudaStream_t st, cudaGraphExec_t *exec, F &&fn)
+{
+    SS_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const int rc = fn();
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(st, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_status(e, "cudaStreamEndCapture");
+    const cudaError_t e2 = cudaGraphInstantiate(exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e2 != cudaSuccess) return cuda_status(e2, "cudaGraphInstantiate");
+    return SS_OK;
+}
+
 int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st)
 {
     Slot &sl = slots[slot];
     if (key >= 0 && sl.key == key) return SS_OK;  // key < 0: never cached
     sl.key = -1;
-    conv_mode_ = conv_mode;
     int rc;
-    if ((rc = launch_prep(img, h, w, c, H[0], W[0], prep, st))) return rc;
-    const float *in = prep;
-    int in_ld = 8;
-    for (int l = 1; l <= 6; ++l) {
-        const int C = PYR_CH[l - 1];
-        float *a = l <= 2 ? (in == s0 ? s1 : s0) : (in == s0 ? s1 : s0);
-        if ((rc = conv(wts->L(pyr_idx(l, 0)), in, in_ld, H[l - 1], W[l - 1], a, C, st))) return rc;
-        float *b = a == s0 ? s1 : s0;
-        if ((rc = conv(wts->L(pyr_idx(l, 1)), a, C, H[l], W[l], b, C, st))) return rc;
-        float *c3 = l <= 2 ? a : sl.lvl[l];
-        if ((rc = conv(wts->L(pyr_idx(l, 2)), b, C, H[l], W[l], c3, C, st))) return rc;
-        in = c3;
-        in_ld = C;
+    if (use_graphs && !prof.on) {
+        auto &g = pyr_graphs[std::make_tuple(slot, (const void *)img, c)];
+        if (!g && (rc = capture(st, &g, [&] { return pyramid_impl(slot, img, c, st); }))) {
+            pyr_graphs.erase(std::make_tuple(slot, (const void *)img, c));
+            return rc;
+        }
+        SS_CUDA_TRY(cudaGraphLaunch(g, st));
+    } else if ((rc = pyramid_impl(slot, img, c, st))) {
+        return rc;
     }
     sl.key = key >= 0 ? key : -1;
     return SS_OK;
@@ -278,10 +346,58 @@ int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st
 
 int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
 {
+    if (use_graphs && !prof.on) {
+        const auto k = std::make_tuple(a, b, (void *)uv, (void *)valid);
+        auto &g = flow_graphs[k];
+        int rc;
+        if (!g && (rc = capture(st, &g, [&] { return flow_impl(a, b, uv, valid, st); }))) {
+            flow_graphs.erase(k);
+            return rc;
+        }
+        SS_CUDA_TRY(cudaGraphLaunch(g, st));
+        return SS_OK;
+    }
+    return flow_impl(a, b, uv, valid, st);
+}
+
+int Run::pyramid_impl(int slot, const float *img, int c, cudaStream_t st)
+{
+    Slot &sl = slots[slot];
     conv_mode_ = conv_mode;
+    ws_ = ws;
+    ws_floats_ = ws_floats;
     int rc;
+    prof.mark("start", st);
+    if ((rc = launch_prep(img, h, w, c, H[0], W[0], prep, st))) return rc;
+    prof.mark("prep", st);
+    const float *in = prep;
+    int in_ld = 8;
+    for (int l = 1; l <= 6; ++l) {
+        const int C = PYR_CH[l - 1];
+        const std::string tag = "pyr" + std::to_string(l);
+        float *a = in == s0 ? s1 : s0;
+        if ((rc = convp((tag + "a").c_str(), wts->L(pyr_idx(l, 0)), in, in_ld, H[l - 1], W[l - 1], a, C, st))) return rc;
+        float *b = a == s0 ? s1 : s0;
+        if ((rc = convp((tag + "b").c_str(), wts->L(pyr_idx(l, 1)), a, C, H[l], W[l], b, C, st))) return rc;
+        float *c3 = l <= 2 ? a : sl.lvl[l];
+        if ((rc = convp((tag + "c").c_str(), wts->L(pyr_idx(l, 2)), b, C, H[l], W[l], c3, C, st))) return rc;
+        in = c3;
+        in_ld = C;
+    }
+    prof.dump("pyramid");
+    return SS_OK;
+}
+
+int Run::flow_impl(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
+{
+    conv_mode_ = conv_mode;
+    ws_ = ws;
+    ws_floats_ = ws_floats;
+    int rc;
+    prof.mark("start", st);
     for (int l = 6; l >= 3; --l) {
         const int C = PYR_CH[l - 1], X = est_in(l);
+        const std::string tag = "est" + std::to_string(l) + "_";
         const float *f1 = slots[a].lvl[l], *f2 = slots[b].lvl[l];
         if (l == 6) {
             if ((rc = launch_corr(f1, f2, C, H[l], W[l], x[l], X, false, st))) return rc;
@@ -289,15 +405,17 @@ int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
             if ((rc = launch_up2_warp(E[l + 1], E_LD, H[l + 1], W[l + 1], f2, C, H[l], W[l], x[l], X,
                                       w2[l], st)))
                 return rc;
+            prof.mark(tag + "warp", st);
             if ((rc = launch_corr(f1, w2[l], C, H[l], W[l], x[l], X, true, st))) return rc;
         }
+        prof.mark(tag + "corr", st);
         const int hh = H[l], ww = W[l];
-        if ((rc = conv(wts->L(est_idx(l, 1)), x[l], X, hh, ww, e1[l], 128, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 2)), e1[l], 128, hh, ww, e2[l], 128, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 3)), e2[l], 128, hh, ww, E[l] + E3_OFF, E_LD, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 4)), E[l] + E3_OFF, E_LD, hh, ww, E[l] + E4_OFF, E_LD, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 5)), E[l] + E4_OFF, E_LD, hh, ww, E[l] + E5_OFF, E_LD, st))) return rc;
-        if ((rc = conv(wts->L(est_idx(l, 6)), E[l] + E5_OFF, E_LD, hh, ww, E[l], E_LD, st))) return rc;
+        if ((rc = convp((tag + "1").c_str(), wts->L(est_idx(l, 1)), x[l], X, hh, ww, e1[l], 128, st))) return rc;
+        if ((rc = convp((tag + "2").c_str(), wts->L(est_idx(l, 2)), e1[l], 128, hh, ww, e2[l], 128, st))) return rc;
+        if ((rc = convp((tag + "3").c_str(), wts->L(est_idx(l, 3)), e2[l], 128, hh, ww, E[l] + E3_OFF, E_LD, st))) return rc;
+        if ((rc = convp((tag + "4").c_str(), wts->L(est_idx(l, 4)), E[l] + E3_OFF, E_LD, hh, ww, E[l] + E4_OFF, E_LD, st))) return rc;
+        if ((rc = convp((tag + "5").c_str(), wts->L(est_idx(l, 5)), E[l] + E4_OFF, E_LD, hh, ww, E[l] + E5_OFF, E_LD, st))) return rc;
+        if ((rc = convp((tag + "6").c_str(), wts->L(est_idx(l, 6)), E[l] + E5_OFF, E_LD, hh, ww, E[l], E_LD, st))) return rc;
     }
     // separable refinement at level 3: r_in = E[3][0:104]
     const int hh = H[3], ww = W[3];
@@ -307,12 +425,16 @@ int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
     for (int i = 1; i <= 6; ++i) {
         const LayerDev &dw = wts->L(ref_idx(i, false));
         if ((rc = launch_depthwise(in, in_ld, hh, ww, cin[i - 1], dw.w, dw.dil, ra, 128, st))) return rc;
-        if ((rc = conv(wts->L(ref_idx(i, true)), ra, 128, hh, ww, rb, 128, st))) return rc;
+        prof.mark("ref" + std::to_string(i) + "_dw", st);
+        if ((rc = convp(("ref" + std::to_string(i) + "_pw").c_str(), wts->L(ref_idx(i, true)), ra, 128, hh, ww, rb, 128, st))) return rc;
         in = rb;
         in_ld = 128;
     }
-    if ((rc = conv(wts->L(REF7), rb, 128, hh, ww, rr, 4, st))) return rc;
-    return launch_flow_final(E[3], E_LD, rr, 4, hh, ww, h, w, uv, valid, st);
+    if ((rc = convp("ref7", wts->L(REF7), rb, 128, hh, ww, rr, 4, st))) return rc;
+    rc = launch_flow_final(E[3], E_LD, rr, 4, hh, ww, h, w, uv, valid, st);
+    prof.mark("final", st);
+    prof.dump("flow");
+    return rc;
 }
 
 }  // namespace fn

@@ -7,6 +7,7 @@
 
 #include <map>
 #include <memory>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -22,6 +23,9 @@ struct ConvParams {
     int out_ld, Ho, Wo;
     int k, stride, dil, pad, act;
     const void *wtc;            // tensor-core weight stages (flownet_tc.cu layout)
+    float *ws = nullptr;        // split-K workspace (tensor-core path), may be null
+    size_t ws_floats = 0;
+    int k_per_split = 0;        // set by the launcher
 };
 
 enum ConvMode { CONV_FFMA = 0, CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
@@ -29,6 +33,7 @@ enum ConvMode { CONV_FFMA = 0, CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
 int launch_conv_ffma(const ConvParams &p, cudaStream_t st);
 // kind 0: bf16 operands (kind::f16); kind 1: 3xTF32 (kind::tf32)
 int launch_conv_tc(const ConvParams &p, int kind, cudaStream_t st);
+int prepare_conv_tc();  // one-time kernel attributes (call outside stream capture)
 int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,
                      float *out, int ld_out, cudaStream_t st);
 int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st);
@@ -72,13 +77,24 @@ struct Run {
     float *x[7] = {nullptr}, *e1[7] = {nullptr}, *e2[7] = {nullptr}, *E[7] = {nullptr},
           *w2[7] = {nullptr};
     float *ra = nullptr, *rb = nullptr, *rr = nullptr;
+    float *ws = nullptr;  // split-K partial sums
+    size_t ws_floats = 0;
     std::vector<void *> allocs;
+    // CUDA graphs (sessions: every buffer is fixed per ring slot, so the
+    // ~60 launches of a pyramid / flow replay as one graph launch)
+    bool use_graphs = false;
+    std::map<std::tuple<int, const void *, int>, cudaGraphExec_t> pyr_graphs;
+    std::map<std::tuple<int, int, void *, void *>, cudaGraphExec_t> flow_graphs;
     ~Run();
     int init(const Weights *w, int h, int w_);
     // pyramid of img (h, w, c) into slot (skipped if key matches)
     int pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st);
     // flow from the frame in slot a toward the frame in slot b (both computed)
     int flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st);
+
+  private:
+    int pyramid_impl(int slot, const float *img, int c, cudaStream_t st);
+    int flow_impl(int a, int b, float *uv, uint8_t *valid, cudaStream_t st);
 };
 
 }  // namespace fn

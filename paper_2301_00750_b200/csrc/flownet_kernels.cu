@@ -305,65 +305,79 @@ int launch_up2_warp(const float *coarse, int cld, int Hc, int Wc, const float *f
 
 // ---------------------------------------------------------------------------
 // cost volume: x[:, d] = leaky(sum_c f1_c * w2_c(p + d) / C), d in [-4,4]^2;
-// also copies f1 into x[:, 96:96+C] (l < 6).  16x16 pixel tile, channels
-// staged 16 at a time with a 4-pixel halo of w2.
-constexpr int CT = 16, CH = 8, HALO = 4, CW = CT + 2 * HALO;
+// also copies f1 into x[:, 96:96+C] (l < 6).  One CTA per (16 x 8 pixel tile,
+// dy): each thread owns one pixel and the 9 dx displacements of that dy row,
+// channels staged 16 at a time ([pixel][channel] smem, w2 rows y + dy with a
+// +-4 column halo).  Grid z = 9 keeps even the 17 x 30 coarsest level spread
+// over dozens of SMs.
+constexpr int CTW = 16, CTH = 8, CHK = 16, HALO = 4, CWW = CTW + 2 * HALO;
 
-__global__ void __launch_bounds__(CT *CT) k_corr(const float *__restrict__ f1,
-                                                 const float *__restrict__ w2, int C, int H,
-                                                 int W, float *__restrict__ x, int xld,
-                                                 int copy_f1)
+__global__ void __launch_bounds__(CTW *CTH) k_corr(const float *__restrict__ f1,
+                                                   const float *__restrict__ w2, int C, int H,
+                                                   int W, float *__restrict__ x, int xld,
+                                                   int copy_f1)
 {
-    __shared__ float s1[CT * CT][CH + 1];
-    __shared__ float s2[CW * CW][CH + 1];
-    const int tx = threadIdx.x % CT, ty = threadIdx.x / CT;
-    const int bx = blockIdx.x * CT, by = blockIdx.y * CT;
+    __shared__ __align__(16) float s1[CTW * CTH][CHK + 4];
+    __shared__ __align__(16) float s2[CTH * CWW][CHK + 4];
+    const int tx = threadIdx.x % CTW, ty = threadIdx.x / CTW;
+    const int bx = blockIdx.x * CTW, by = blockIdx.y * CTH;
+    const int dy = (int)blockIdx.z - HALO;
     const int y = by + ty, xx = bx + tx;
     const bool inb = y < H && xx < W;
-    float acc[81];
+    float acc[9];
 #pragma unroll
-    for (int d = 0; d < 81; ++d) acc[d] = 0.f;
-    for (int c0 = 0; c0 < C; c0 += CH) {
-        for (int i = threadIdx.x; i < CT * CT * CH; i += CT * CT) {
-            const int px = i / CH, c = i - px * CH;
-            const int py = by + px / CT, pxx = bx + px % CT;
-            s1[px][c] = (py < H && pxx < W && c0 + c < C) ? f1[((long)py * W + pxx) * C + c0 + c] : 0.f;
+    for (int d = 0; d < 9; ++d) acc[d] = 0.f;
+    for (int c0 = 0; c0 < C; c0 += CHK) {
+        // f1 tile: 128 px x 16 ch = 512 float4
+        for (int i = threadIdx.x; i < CTW * CTH * CHK / 4; i += CTW * CTH) {
+            const int px = i / (CHK / 4), q = (i - px * (CHK / 4)) * 4;
+            const int py = by + px / CTW, pxx = bx + px % CTW;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (py < H && pxx < W) v = *reinterpret_cast<const float4 *>(f1 + ((long)py * W + pxx) * C + c0 + q);
+            *reinterpret_cast<float4 *>(&s1[px][q]) = v;
         }
-        for (int i = threadIdx.x; i < CW * CW * CH; i += CT * CT) {
-            const int px = i / CH, c = i - px * CH;
-            const int py = by - HALO + px / CW, pxx = bx - HALO + px % CW;
-            s2[px][c] = (py >= 0 && py < H && pxx >= 0 && pxx < W && c0 + c < C)
-                            ? w2[((long)py * W + pxx) * C + c0 + c]
-                            : 0.f;
+        // w2 rows y + dy, columns x - 4 .. x + 19
+        for (int i = threadIdx.x; i < CTH * CWW * CHK / 4; i += CTW * CTH) {
+            const int px = i / (CHK / 4), q = (i - px * (CHK / 4)) * 4;
+            const int py = by + px / CWW + dy, pxx = bx - HALO + px % CWW;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (py >= 0 && py < H && pxx >= 0 && pxx < W)
+                v = *reinterpret_cast<const float4 *>(w2 + ((long)py * W + pxx) * C + c0 + q);
+            *reinterpret_cast<float4 *>(&s2[px][q]) = v;
         }
         __syncthreads();
-#pragma unroll 4
-        for (int c = 0; c < CH; ++c) {
-            const float a = s1[ty * CT + tx][c];
 #pragma unroll
-            for (int dy = 0; dy < 9; ++dy)
+        for (int c = 0; c < CHK; c += 4) {
+            const float4 a = *reinterpret_cast<const float4 *>(&s1[ty * CTW + tx][c]);
 #pragma unroll
-                for (int dx = 0; dx < 9; ++dx)
-                    acc[dy * 9 + dx] = fmaf(a, s2[(ty + dy) * CW + tx + dx][c], acc[dy * 9 + dx]);
+            for (int d = 0; d < 9; ++d) {
+                const float4 b = *reinterpret_cast<const float4 *>(&s2[ty * CWW + tx + d][c]);
+                acc[d] = fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, fmaf(a.w, b.w, acc[d]))));
+            }
         }
         __syncthreads();
     }
     if (!inb) return;
     const long pix = (long)y * W + xx;
     const float inv = 1.f / (float)C;
-    float *dst = x + pix * xld;
+    float *dst = x + pix * xld + (dy + HALO) * 9;
 #pragma unroll
-    for (int d = 0; d < 81; ++d) dst[d] = leaky(acc[d] * inv);
-    if (copy_f1)
+    for (int d = 0; d < 9; ++d) dst[d] = leaky(acc[d] * inv);
+    if (copy_f1 && dy == 0)
         for (int c = 0; c < C; c += 4)
-            *reinterpret_cast<float4 *>(dst + 96 + c) = *reinterpret_cast<const float4 *>(f1 + pix * C + c);
+            *reinterpret_cast<float4 *>(x + pix * xld + 96 + c) =
+                *reinterpret_cast<const float4 *>(f1 + pix * C + c);
 }
 
 int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x, int xld,
                 bool copy_f1, cudaStream_t st)
 {
-    const dim3 grid((W + CT - 1) / CT, (H + CT - 1) / CT);
-    k_corr<<<grid, CT * CT, 0, st>>>(f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
+    if (C % CHK != 0) {
+        set_error("correlation needs C % 16 == 0");
+        return SS_VALUE_ERROR;
+    }
+    const dim3 grid((W + CTW - 1) / CTW, (H + CTH - 1) / CTH, 9);
+    k_corr<<<grid, CTW * CTH, 0, st>>>(f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
     SS_LAUNCH_CHECK("k_corr");
     return SS_OK;
 }

@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "flownet.h"
 #include "ss_common.cuh"
 #include "tc_common.cuh"
@@ -72,7 +74,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvParams p)
     const int M = p.Ho * p.Wo;
     const int m0 = blockIdx.x * TC_BM;
     const int Ktot = p.k * p.k * p.Cin;
-    const int nk = (Ktot + C::BK - 1) / C::BK;
+    // split-K: this CTA owns K stages [kb, kb + nk) (blockIdx.y = split)
+    const int nk_all = (Ktot + C::BK - 1) / C::BK;
+    const int kb = blockIdx.y * p.k_per_split;
+    const int nk = min(p.k_per_split, nk_all - kb);
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) mbar_init(&done[s], 1);
@@ -154,16 +159,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvParams p)
 
     const uint32_t id = idesc(KIND == 0 ? 1u : 2u, 128u, (uint32_t)N);
 
-    prefetch(0);
-    issue_b(0, 0);
-    for (int kt = 0; kt < nk; ++kt) {
+    prefetch(kb);
+    issue_b(kb, 0);
+    for (int kt = 0; kt < nk; ++kt) {  // kt: local stage index, kb + kt: global
         const int s = kt % C::STAGES;
         store_a(s);
         if (kt + 1 < nk) {
             const int s1 = (kt + 1) % C::STAGES;
             if (kt + 1 >= C::STAGES) mbar_wait(&done[s1], ((kt + 1 - C::STAGES) / C::STAGES) & 1);
-            prefetch(kt + 1);
-            issue_b(kt + 1, s1);
+            prefetch(kb + kt + 1);
+            issue_b(kb + kt + 1, s1);
             cp_wait<1>();
         } else {
             cp_wait<0>();
@@ -202,7 +207,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvParams p)
     for (int c0 = 0; c0 < N; c0 += 16) {
         float v[16];
         tmem_ld16(trow + c0, v);
-        if (row < M && c0 < p.Cout) {
+        if (p.ws) {  // split-K partial sums, reduced by k_splitk_reduce
+            if (row < M) {
+                float *dst = p.ws + ((size_t)blockIdx.y * M + row) * N + c0;
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+        } else if (row < M && c0 < p.Cout) {
             float *dst = p.out + (long)row * p.out_ld + c0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -214,7 +226,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvParams p)
                 for (int i = 0; i < 16; i += 4)
                     *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
             } else {
-                for (int i = 0; i < p.Cout - c0; ++i) dst[i] = v[i];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (i < p.Cout - c0) dst[i] = v[i];
             }
         }
     }
@@ -223,19 +237,87 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvParams p)
     if (warp == 0) tmem_dealloc<TC_TMEM_COLS>(tmem);
 }
 
-template <int KIND>
-static int launch_tc(const ConvParams &p, cudaStream_t st)
+// out[m, n] = act(sum_s ws[s, m, n] + bias[n])
+__global__ void k_splitk_reduce(const float *__restrict__ ws, int splits, int M, int N, int Cout,
+                                const float *__restrict__ bias, int act, float *__restrict__ out,
+                                int out_ld)
 {
-    const size_t smem = TcCfg<KIND>::smem(p.Cout_pad);
-    static size_t configured = 0;
-    if (smem > configured) {
-        SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-        configured = smem;
+    const int n4 = (Cout + 3) / 4;
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)M * n4) return;
+    const int m = (int)(i / n4), n = (int)(i - (long)m * n4) * 4;
+    float4 acc = *reinterpret_cast<const float4 *>(ws + (size_t)m * N + n);
+    for (int s = 1; s < splits; ++s) {
+        const float4 v = *reinterpret_cast<const float4 *>(ws + ((size_t)s * M + m) * N + n);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
     }
+    float r[4] = {acc.x, acc.y, acc.z, acc.w};
+    float *dst = out + (long)m * out_ld + n;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (n + j >= Cout) break;
+        const float x = r[j] + bias[n + j];
+        dst[j] = act ? lk(x) : x;
+    }
+}
+
+static int n_sm_ = 0;
+
+// one-time kernel attributes (outside any stream capture): the largest layer
+// has N = 192 output channels
+int prepare_conv_tc()
+{
+    static bool done = false;
+    if (done) return SS_OK;
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)TcCfg<0>::smem(256)));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)TcCfg<1>::smem(192)));
+    int dev = 0;
+    SS_CUDA_TRY(cudaGetDevice(&dev));
+    SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, dev));
+    done = true;
+    return SS_OK;
+}
+
+template <int KIND>
+static int launch_tc(ConvParams p, cudaStream_t st)
+{
+    using C = TcCfg<KIND>;
+    const size_t smem = C::smem(p.Cout_pad);
+    if (int rc = prepare_conv_tc()) return rc;
+    if ((KIND == 0 && p.Cout_pad > 256) || (KIND == 1 && p.Cout_pad > 192)) {
+        set_error("conv_tc: too many output channels");
+        return SS_VALUE_ERROR;
+    }
+    const int n_sm = n_sm_;
     const int M = p.Ho * p.Wo;
-    k_conv_tc<KIND><<<(M + TC_BM - 1) / TC_BM, TC_THREADS, smem, st>>>(p);
+    const int ctas = (M + TC_BM - 1) / TC_BM;
+    const int nk = (p.k * p.k * p.Cin + C::BK - 1) / C::BK;
+    // split K when the pixel tiles alone leave SMs idle and K is long: each
+    // split keeps >= 4 stages so the pipeline still overlaps loads and MMAs
+    int splits = 1;
+    if (p.ws && ctas < n_sm && nk >= 8) {
+        splits = std::min((n_sm + ctas - 1) / ctas, nk / 4);
+        const size_t need = (size_t)splits * M * p.Cout_pad;
+        if (need > p.ws_floats) splits = (int)(p.ws_floats / ((size_t)M * p.Cout_pad));
+        splits = std::max(splits, 1);
+    }
+    p.k_per_split = (nk + splits - 1) / splits;
+    splits = (nk + p.k_per_split - 1) / p.k_per_split;
+    float *ws = p.ws;
+    if (splits == 1) p.ws = nullptr;
+    k_conv_tc<KIND><<<dim3(ctas, splits), TC_THREADS, smem, st>>>(p);
     SS_LAUNCH_CHECK("k_conv_tc");
+    if (splits > 1) {
+        const long n = (long)M * ((p.Cout + 3) / 4);
+        k_splitk_reduce<<<blocks_for(n, 256), 256, 0, st>>>(ws, splits, M, p.Cout_pad, p.Cout,
+                                                              p.bias, p.act, p.out, p.out_ld);
+        SS_LAUNCH_CHECK("k_splitk_reduce");
+    }
     return SS_OK;
 }
 
