@@ -26,6 +26,7 @@ struct ConvParams {
     float *ws = nullptr;        // split-K workspace (tensor-core path), may be null
     size_t ws_floats = 0;
     int k_per_split = 0;        // set by the launcher
+    int n_full = 0, n_off = 0;  // N-split (set by the launcher): weight rows [n_off, n_off + Cout_pad)
 };
 
 enum ConvMode { CONV_FFMA = 0, CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
