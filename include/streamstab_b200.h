@@ -105,6 +105,20 @@ SS_API int ss_solve_screened_poisson(const float *processed, const float *target
                               int h, int w, int c, const ss_params *p, const float *init,
                               float *out, int *div_iter, void *stream);
 
+/* ---- evaluation metrics -------------------------- */
+/* warping_error_pair (metrics.py:107-128) on device frames / flows:
+ * sums_host[0] = sum(mask * mean_c |a - warp(b)|), sums_host[1] = sum(mask),
+ * mask = occlusion_mask(fwd, bwd) * backward_warp mask; float64 sums.
+ * Synchronises the stream. */
+SS_API int ss_warping_error_sums(const float *frame_a, const float *frame_b, int h, int w, int c,
+                                 const float *fwd_uv, const uint8_t *fwd_valid,
+                                 const float *bwd_uv, const uint8_t *bwd_valid,
+                                 double *sums_host, void *stream);
+/* ssim (metrics.py:75-104): luma, 11x11 Gaussian sigma 1.5, reflect borders,
+ * valid-window mean, float64.  Synchronises the stream. */
+SS_API int ss_ssim(const float *a, const float *b, int h, int w, int c, double *out_host,
+                   void *stream);
+
 /* ---- sessions: SessionState + stabilize_step (consistency.py:306-413) ---- */
 typedef struct ss_session ss_session;
 

@@ -331,6 +331,65 @@ int ss_solve_screened_poisson(const float *processed, const float *target, const
     return rc;
 }
 
+// ---- metrics -------------------------------------------------------------------
+namespace {
+struct DevScratch {  // grow-only per-thread device scratch
+    void *p = nullptr;
+    size_t bytes = 0;
+    ~DevScratch() { cudaFree(p); }
+    int ensure(size_t b)
+    {
+        if (b <= bytes) return SS_OK;
+        cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        SS_CUDA_TRY(cudaMalloc(&p, b));
+        bytes = b;
+        return SS_OK;
+    }
+};
+thread_local DevScratch metric_scratch;
+}  // namespace
+
+int ss_warping_error_sums(const float *frame_a, const float *frame_b, int h, int w, int c,
+                          const float *fwd_uv, const uint8_t *fwd_valid, const float *bwd_uv,
+                          const uint8_t *bwd_valid, double *sums_host, void *stream)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    if (int rc = check_c(c)) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = metric_scratch.ensure(2 * sizeof(double))) return rc;
+    double *d = static_cast<double *>(metric_scratch.p);
+    if (int rc = launch_warping_error(frame_a, frame_b, h, w, c, fwd_uv, fwd_valid, bwd_uv,
+                                      bwd_valid, d, st))
+        return rc;
+    SS_CUDA_TRY(cudaMemcpyAsync(sums_host, d, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SS_CUDA_TRY(cudaStreamSynchronize(st));
+    return SS_OK;
+}
+
+int ss_ssim(const float *a, const float *b, int h, int w, int c, double *out_host, void *stream)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    if (int rc = check_c(c)) return rc;
+    if (h < 11 || w < 11) {
+        set_error("image " + std::to_string(w) + "x" + std::to_string(h) +
+                  " smaller than the 11x11 window");
+        return SS_VALUE_ERROR;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)h * w;
+    if (int rc = metric_scratch.ensure((7 * n + 1) * sizeof(double))) return rc;
+    double *scratch = static_cast<double *>(metric_scratch.p);
+    double *sum = scratch + 7 * n;
+    if (int rc = launch_ssim(a, b, h, w, c, scratch, sum, st)) return rc;
+    double s = 0.0;
+    SS_CUDA_TRY(cudaMemcpyAsync(&s, sum, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SS_CUDA_TRY(cudaStreamSynchronize(st));
+    *out_host = s / ((double)(h - 10) * (double)(w - 10));
+    return SS_OK;
+}
+
 // ---- sessions ----------------------------------------------------------------
 int ss_session_create(int h, int w, int c_in, int c_proc, void *stream, ss_session **out)
 {

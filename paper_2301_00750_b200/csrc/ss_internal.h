@@ -36,6 +36,13 @@ int launch_laplacian(const float *img, int h, int w, int c, float *out, bool pla
                      cudaStream_t st);
 int launch_hwc_to_planar(const float *src, int h, int w, int c, float *dst, cudaStream_t st);
 int launch_presolve(const PresolveArgs &a, int ci, int cp, bool with_next, cudaStream_t st);
+// metrics.cu: sums[0] = sum(mask * per_pixel), sums[1] = sum(mask) (device, float64)
+int launch_warping_error(const float *fa, const float *fb, int h, int w, int c, const float *fuv,
+                         const uint8_t *fvalid, const float *buv, const uint8_t *bvalid,
+                         double *sums, cudaStream_t st);
+// scratch: 7 * h * w doubles; *sum (device) = sum of the cropped SSIM map
+int launch_ssim(const float *a, const float *b, int h, int w, int c, double *scratch,
+                double *sum, cudaStream_t st);
 
 // numpy pairwise-sum tree for n elements (see solver.cu)
 struct PairwisePlan {

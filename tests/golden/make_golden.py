@@ -218,6 +218,43 @@ def make_streams(consistency, flow, synthetic):
     _save("streams.npz", **out)
 
 
+def make_metrics(flow, imgio, synthetic):
+    from streamstab import metrics
+
+    out = {}
+    rng = np.random.default_rng(505)
+    # E_warp pairs: translating texture with ground-truth flow, a sub-pixel
+    # flow, and flows recorded from the reference's DIS estimator
+    seq = synthetic.translating_sequence(frames=3, height=40, width=56, step=(2, 1), seed=5)
+    cases = [("gt", seq.processed[0], seq.processed[1], flow.ConstantFlow(2, 1)),
+             ("subpix", seq.processed[0], seq.processed[1], flow.ConstantFlow(1.37, -0.61)),
+             ("dis", seq.inputs[1], seq.inputs[2], flow.BuiltinFlow(flow.FlowOptions()))]
+    for tag, a, b, prov in cases:
+        fw = prov.flow_between(1, a, 2, b)
+        bw = prov.flow_between(2, b, 1, a)
+        out[f"ew_{tag}_a"] = np.asarray(a, np.float32)
+        out[f"ew_{tag}_b"] = np.asarray(b, np.float32)
+        out[f"ew_{tag}_fuv"], out[f"ew_{tag}_fvalid"] = fw.uv, fw.valid
+        out[f"ew_{tag}_buv"], out[f"ew_{tag}_bvalid"] = bw.uv, bw.valid
+        rec = {(1, 2): fw, (2, 1): bw}
+
+        class _P:
+            def flow_between(self, pa, fa, pb, fb):
+                return rec[(pa, pb)]
+
+        v = metrics.warping_error_pair(a, b, 1, 2, _P())
+        out[f"ew_{tag}_value"] = np.array(np.nan if v is None else v)
+    # SSIM: random frames, a grey pair, and noisy-vs-clean stylized frames
+    a = rng.random((23, 31, 3)).astype(np.float32)
+    b = np.clip(a + rng.normal(0, 0.05, a.shape), 0, 1).astype(np.float32)
+    g1 = rng.random((16, 12, 1)).astype(np.float32)
+    g2 = rng.random((16, 12, 1)).astype(np.float32)
+    for tag, x, y in (("rgb", a, b), ("gray", g1, g2), ("seq", seq.processed[0], seq.inputs[0])):
+        out[f"ssim_{tag}_a"], out[f"ssim_{tag}_b"] = x, y
+        out[f"ssim_{tag}_value"] = np.array(metrics.ssim(x, y))
+    _save("metrics.npz", **out)
+
+
 def main():
     consistency, flow, imgio, synthetic = _import_ref()
     make_warp(flow, imgio)
@@ -225,6 +262,7 @@ def main():
     make_weights(consistency)
     make_solver(consistency)
     make_streams(consistency, flow, synthetic)
+    make_metrics(flow, imgio, synthetic)
 
 
 if __name__ == "__main__":
