@@ -307,20 +307,44 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    bf16_peak = float(peaks.get("bf16_tflops_sustained", 1412.7))
     k1_gbs = 130.0 * h * w / (med_blend * 1e-3) / 1e9
-    roofline = {
+    solver_line = {
         "kernel": f"k_sgd_tma<{SOLVER_K}> (solver pass = {SOLVER_K} SGD-momentum iterations)",
         "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 2),
         "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": None,
         "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1965 MHz non-FMA op rate "
                        "(MEASURED_PEAKS.json has no FP32 entry)",
-        "launch_ms": round(per_pass_ms, 5),
-        "secondary": {
-            "kernel": "k_presolve (K1 fused warp+weights+blend)", "bound": "hbm",
-            "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(k1_gbs / hbm_peak, 4), "traffic": None, "launch_ms": round(med_blend, 5),
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
-    }
+        "launch_ms": round(per_pass_ms, 5), "stage_ms": round(med_solve, 4)}
+    k1_line = {
+        "kernel": "k_presolve (K1 fused warp+weights+blend)", "bound": "hbm",
+        "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+        "frac": round(k1_gbs / hbm_peak, 4), "traffic": None, "launch_ms": round(med_blend, 5),
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+    if args.flow == "constant":
+        roofline = dict(solver_line, secondary=[k1_line])
+    else:
+        # the flow network is the largest stage; its heaviest kernel is the
+        # 1/8-resolution first estimator conv, timed live on the session's
+        # buffers (CUDA events, 20 launches)
+        cms, cfl = ctypes.c_float(0.0), ctypes.c_double(0.0)
+        _check(L.ss_session_time_conv(state.handle, 3, 20, ctypes.byref(cms), ctypes.byref(cfl)), L)
+        conv_tf = cfl.value / (cms.value * 1e-3) / 1e12
+        # 3xTF32: tf32 runs at half the bf16 rate and each fp32 product is 3 MMAs
+        conv_peak = bf16_peak if args.flow == "bf16" else bf16_peak / 6.0
+        roofline = {
+            "kernel": "k_conv_tc<%d> est3_1 (1/8-res 3x3 conv, 147 live -> 128 ch, tcgen05/TMEM)"
+                      % (0 if args.flow == "bf16" else 1),
+            "bound": "tensor", "achieved": round(conv_tf, 2), "peak": round(conv_peak, 1),
+            "unit": "TFLOP/s", "frac": round(conv_tf / conv_peak, 4), "traffic": None,
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained" if args.flow == "bf16"
+                            else "derived: MEASURED_PEAKS bf16 sustained / 2 (tf32 rate) / 3 "
+                                 "(3xTF32 MMAs per fp32 product)"),
+            "launch_ms": round(cms.value, 5),
+            "flow_stage": {"ms": round(med_flow, 4), "gflop": 131.0,
+                           "achieved_tflops": round(131.0 / med_flow, 2)},
+            "secondary": [solver_line, k1_line],
+        }
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sec, cores, sample = _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
@@ -335,8 +359,8 @@ def main():
         "config": {"workload": f"{w}x{h} single stream per GPU, lite flow CNN ({args.flow}) + "
                                "default preset with per-frame interactive k1/k2/lambda schedule, "
                                "150 solver iterations",
-                   "flow": {"fp32": "lite flow CNN, fp32 (CUDA-core FFMA convs), random-init "
-                                    "seeded weights",
+                   "flow": {"fp32": "lite flow CNN, fp32-class (3xTF32 tcgen05 convs, fp32 "
+                                    "activations), random-init seeded weights",
                             "bf16": "lite flow CNN, bf16 tcgen05 convs, random-init seeded "
                                     "weights",
                             "constant": "ConstantFlow(2,1) on device"}[args.flow],

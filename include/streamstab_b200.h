@@ -179,6 +179,10 @@ SS_API int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *f
 SS_API int ss_session_attach_flownet(ss_session *s, ss_flownet *net);
 /* Compute flow slot `which` (0: t -> t-1, 1: t -> t+1) for the pending step. */
 SS_API int ss_session_compute_flow(ss_session *s, int which);
+/* Roofline probe: average device time of `reps` launches of the session's
+ * first estimator convolution at pyramid `level` (3..6) and its algorithmic
+ * FLOPs (live channels only). */
+SS_API int ss_session_time_conv(ss_session *s, int level, int reps, float *ms, double *flops);
 SS_API void *ss_session_stream(const ss_session *s);
 
 #ifdef __cplusplus

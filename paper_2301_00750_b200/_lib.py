@@ -35,7 +35,7 @@ EXPORTS = (
     "ss_step", "ss_output", "ss_output_device", "ss_last_timing", "ss_flows",
     "ss_session_stream", "ss_flownet_num_params", "ss_flownet_create", "ss_flownet_destroy",
     "ss_flownet_flow", "ss_session_attach_flownet", "ss_session_compute_flow",
-    "ss_warping_error_sums", "ss_ssim",
+    "ss_warping_error_sums", "ss_ssim", "ss_session_time_conv",
 )
 SS_FLOW_FP32 = 0
 SS_FLOW_BF16 = 1
@@ -103,6 +103,7 @@ def _declare(L):
         "ss_warping_error_sums": (i32, [vp, vp, i32, i32, i32, vp, vp, vp, vp,
                                         P(ctypes.c_double), vp]),
         "ss_ssim": (i32, [vp, vp, i32, i32, i32, P(ctypes.c_double), vp]),
+        "ss_session_time_conv": (i32, [vp, i32, i32, P(f32), P(ctypes.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -737,6 +737,15 @@ int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
     return fn::prepare_conv_tc();
 }
 
+int ss_session_time_conv(ss_session *s, int level, int reps, float *ms, double *flops)
+{
+    if (!s->run) {
+        set_error("no flow network attached to the session");
+        return SS_VALUE_ERROR;
+    }
+    return s->run->time_est1(level, reps < 1 ? 1 : reps, s->stream, ms, flops);
+}
+
 int ss_session_compute_flow(ss_session *s, int which)
 {
     if (which != 0 && which != 1) {

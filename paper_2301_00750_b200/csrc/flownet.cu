@@ -360,6 +360,36 @@ int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
     return flow_impl(a, b, uv, valid, st);
 }
 
+int Run::time_est1(int level, int reps, cudaStream_t st, float *ms, double *flops)
+{
+    if (level < 3 || level > 6) {
+        set_error("level must be 3..6");
+        return SS_VALUE_ERROR;
+    }
+    conv_mode_ = conv_mode;
+    ws_ = ws;
+    ws_floats_ = ws_floats;
+    const LayerDev &L = wts->L(est_idx(level, 1));
+    const int X = est_in(level), hh = H[level], ww = W[level];
+    cudaEvent_t ev0, ev1;
+    SS_CUDA_TRY(cudaEventCreate(&ev0));
+    SS_CUDA_TRY(cudaEventCreate(&ev1));
+    int rc = conv(L, x[level], X, hh, ww, e1[level], 128, st);  // warm-up
+    SS_CUDA_TRY(cudaEventRecord(ev0, st));
+    for (int i = 0; i < reps && !rc; ++i) rc = conv(L, x[level], X, hh, ww, e1[level], 128, st);
+    SS_CUDA_TRY(cudaEventRecord(ev1, st));
+    SS_CUDA_TRY(cudaEventSynchronize(ev1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    *ms = t / reps;
+    // algorithmic MACs over the live (unpadded) input channels: 81 corr + 2 flow + C_l
+    const int live = level == 6 ? 81 : 81 + 2 + PYR_CH[level - 1];
+    *flops = 2.0 * hh * ww * 9.0 * live * L.cout;
+    return rc;
+}
+
 int Run::pyramid_impl(int slot, const float *img, int c, cudaStream_t st)
 {
     Slot &sl = slots[slot];

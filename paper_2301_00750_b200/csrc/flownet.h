@@ -92,6 +92,9 @@ struct Run {
     int pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st);
     // flow from the frame in slot a toward the frame in slot b (both computed)
     int flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st);
+    // average device time (CUDA events) of `reps` launches of the first
+    // estimator conv at `level` on this run's buffers (roofline measurement)
+    int time_est1(int level, int reps, cudaStream_t st, float *ms, double *flops);
 
   private:
     int pyramid_impl(int slot, const float *img, int c, cudaStream_t st);
