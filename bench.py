@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--flow", default="fp32", choices=["fp32", "bf16", "constant"])
+    ap.add_argument("--flow", default="fp32", choices=["fp32", "bf16", "dis", "constant"])
     ap.add_argument("--height", type=int, default=H)
     ap.add_argument("--width", type=int, default=W)
     ap.add_argument("--no-e2e", action="store_true")
@@ -163,7 +163,9 @@ def _cpu_step_seconds(h, w, flow_kind, budget_s):
     t_cons = sum(cons) / len(cons)
     t_flow = 0.0
     sample = f"{len(cons)} full {w}x{h} consistency steps (oracle/streamstab_oracle.c, {cores} threads)"
-    if flow_kind != "constant":
+    if flow_kind == "dis":
+        sample += " (DIS flow not included: no CPU restatement of it on the box)"
+    if flow_kind in ("fp32", "bf16"):
         ch, cw = max(64, h // 4), max(64, w // 4)
         scale = (math.ceil(h / 64) * math.ceil(w / 64)) / (math.ceil(ch / 64) * math.ceil(cw / 64))
         wts = lf.make_weights(0)
@@ -231,8 +233,14 @@ def main():
     h, w = args.height, args.width
     L = _lib.lib()
     seq = DeviceSequence(h, w, step=(2, 1), seed=rank)
-    flow = ss.ConstantFlow(2, 1) if args.flow == "constant" else ss.LiteFlowNet(
-        seed=0, precision=args.flow)
+    if args.flow == "constant":
+        flow = ss.ConstantFlow(2, 1)
+    elif args.flow == "dis":
+        from paper_2301_00750_b200.flow import BuiltinFlow
+
+        flow = BuiltinFlow()  # the reference's default provider (flow.py:361-369)
+    else:
+        flow = ss.LiteFlowNet(seed=0, precision=args.flow)
     state = ss.SessionState(params=params_for(0))
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -321,7 +329,7 @@ def main():
         "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
         "frac": round(k1_gbs / hbm_peak, 4), "traffic": None, "launch_ms": round(med_blend, 5),
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
-    if args.flow == "constant":
+    if args.flow in ("constant", "dis"):
         roofline = dict(solver_line, secondary=[k1_line])
     else:
         # the flow network is the largest stage; its heaviest kernel is the
@@ -350,19 +358,25 @@ def main():
         sec, cores, sample = _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
         cpu = {"value": round(1.0 / sec, 5), "unit": "frames/s", "cores": cores, "kind": "port",
                "sample": sample}
-    launches = 1 + n_pass + (2 if args.flow == "constant" else flow_kernel_launches())
+    # DIS: per flow 2 luma + 2 x 4 box levels + per level (4 blur + resize +
+    # refine + 2 median + densify + 2 uniform) + finish
+    dis_launches = 2 * (2 + 8 + 5 * 11 + 1)
+    launches = 1 + n_pass + {"constant": 2, "dis": dis_launches}.get(args.flow,
+                                                                     flow_kernel_launches())
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"{w}x{h} single stream per GPU, lite flow CNN ({args.flow}) + "
+        "config": {"workload": f"{w}x{h} single stream per GPU, flow={args.flow} + "
                                "default preset with per-frame interactive k1/k2/lambda schedule, "
                                "150 solver iterations",
                    "flow": {"fp32": "lite flow CNN, fp32-class (3xTF32 tcgen05 convs, fp32 "
                                     "activations), random-init seeded weights",
                             "bf16": "lite flow CNN, bf16 tcgen05 convs, random-init seeded "
                                     "weights",
+                            "dis": "reference built-in DIS flow (BuiltinFlow, FlowOptions()) on "
+                                   "GPU, bit-identical to flow.py on the golden cases",
                             "constant": "ConstantFlow(2,1) on device"}[args.flow],
                    "streams_per_gpu": 1, "l2": "flushed between timed steps (256 MiB write)",
                    "stage_ms_median": {"flow": round(med_flow, 4), "warp_blend": round(med_blend, 4),
@@ -391,7 +405,7 @@ def run_e2e(args, L, state, pool, flow, torch, dist):
     out = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
     sess = state.handle
     pos = [int(L.ss_solved_through(sess)) + 1]  # last pushed position
-    use_cnn = args.flow != "constant"
+    use_cnn = args.flow in ("fp32", "bf16")
     if use_cnn:
         _check(L.ss_session_attach_flownet(sess, flow.handle()), L)
 
@@ -403,6 +417,9 @@ def run_e2e(args, L, state, pool, flow, torch, dist):
         if use_cnn:
             _check(L.ss_session_compute_flow(sess, 0), L)
             _check(L.ss_session_compute_flow(sess, 1), L)
+        elif args.flow == "dis":
+            for which in (0, 1):
+                _check(L.ss_session_compute_dis_flow(sess, which, 5, 9, 4, 1), L)
         else:
             _check(L.ss_set_constant_flow(sess, 0, 2.0, 1.0, -1), L)
             _check(L.ss_set_constant_flow(sess, 1, 2.0, 1.0, 1), L)

@@ -48,6 +48,9 @@ enum ss_status {
     SS_NO_MEMORY = 5,
 };
 
+/* One stream's device-resident state (see the session section below). */
+typedef struct ss_session ss_session;
+
 enum ss_where { SS_HOST = 0, SS_DEVICE = 1 };
 enum ss_dtype { SS_F32 = 0, SS_U8 = 1 };
 
@@ -105,6 +108,17 @@ SS_API int ss_solve_screened_poisson(const float *processed, const float *target
                               int h, int w, int c, const ss_params *p, const float *init,
                               float *out, int *div_iter, void *stream);
 
+/* ---- built-in DIS flow (estimate_flow, flow.py:168-325) --- */
+/* FlowOptions (flow.py:27-42): levels >= 1, odd patch >= 3, iterations per
+ * level, downscale in {1, 2, 4}.  Flow from frame_a toward frame_b ((h, w, c)
+ * float32 device pointers) into uv (h, w, 2) / valid (h, w) (may be NULL). */
+SS_API int ss_dis_flow(const float *frame_a, const float *frame_b, int h, int w, int c,
+                       int levels, int patch, int iters, int downscale, float *uv,
+                       uint8_t *valid, void *stream);
+/* BuiltinFlow inside a session: flow slot `which` (0: t -> t-1, 1: t -> t+1). */
+SS_API int ss_session_compute_dis_flow(ss_session *s, int which, int levels, int patch,
+                                       int iters, int downscale);
+
 /* ---- evaluation metrics -------------------------- */
 /* warping_error_pair (metrics.py:107-128) on device frames / flows:
  * sums_host[0] = sum(mask * mean_c |a - warp(b)|), sums_host[1] = sum(mask),
@@ -120,7 +134,6 @@ SS_API int ss_ssim(const float *a, const float *b, int h, int w, int c, double *
                    void *stream);
 
 /* ---- sessions: SessionState + stabilize_step (consistency.py:306-413) ---- */
-typedef struct ss_session ss_session;
 
 /* One stream's device-resident state: the (t-1, t, t+1) ring of
  * (input, processed) pairs, O_{t-1}, flows and solver buffers.  stream may be

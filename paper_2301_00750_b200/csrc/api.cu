@@ -8,6 +8,7 @@
 #include <memory>
 #include <string>
 
+#include "dis.h"
 #include "flownet.h"
 #include "ss_common.cuh"
 #include "ss_internal.h"
@@ -97,6 +98,7 @@ struct ss_session {
     std::unique_ptr<fn::Run> run;
     cudaEvent_t fev[2] = {nullptr, nullptr};
     bool flow_timed = false;
+    std::unique_ptr<dis::Estimator> dis;  // built-in flow (BuiltinFlow)
 };
 
 struct ss_flownet {
@@ -148,6 +150,7 @@ static void session_free(ss_session *s)
     for (auto &e : s->fev)
         if (e) cudaEventDestroy(e);
     s->run.reset();
+    s->dis.reset();
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
 
@@ -329,6 +332,40 @@ int ss_solve_screened_poisson(const float *processed, const float *target, const
     const int rc = solve_planar(wk, tA.p, tI.p ? tI.p : tA.p, tL.p, wc, *p, out, div_iter, st);
     cudaStreamSynchronize(st);  // temporaries are freed on return
     return rc;
+}
+
+// ---- built-in DIS flow ------------------------------------------------------------
+static dis::Options dis_options(int levels, int patch, int iters, int downscale)
+{
+    dis::Options o;
+    o.levels = levels;
+    o.patch = patch;
+    o.iters = iters;
+    o.downscale = downscale;
+    return o;
+}
+
+static bool same_opts(const dis::Options &a, const dis::Options &b)
+{
+    return a.levels == b.levels && a.patch == b.patch && a.iters == b.iters &&
+           a.downscale == b.downscale;
+}
+
+int ss_dis_flow(const float *frame_a, const float *frame_b, int h, int w, int c, int levels,
+                int patch, int iters, int downscale, float *uv, uint8_t *valid, void *stream)
+{
+    if (int rc = check_hw(h, w)) return rc;
+    if (int rc = check_c(c)) return rc;
+    static thread_local std::unique_ptr<dis::Estimator> est;
+    const dis::Options o = dis_options(levels, patch, iters, downscale);
+    if (!est || est->h != h || est->w != w || !same_opts(est->opts, o)) {
+        est.reset(new dis::Estimator());
+        if (int rc = est->init(h, w, o)) {
+            est.reset();
+            return rc;
+        }
+    }
+    return est->run(frame_a, frame_b, c, uv, valid, (cudaStream_t)stream);
 }
 
 // ---- metrics -------------------------------------------------------------------
@@ -735,6 +772,36 @@ int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
     s->run->conv_mode = conv_mode_for(net->precision);
     s->run->use_graphs = getenv("SS_FLOW_GRAPHS") == nullptr || strcmp(getenv("SS_FLOW_GRAPHS"), "0");
     return fn::prepare_conv_tc();
+}
+
+int ss_session_compute_dis_flow(ss_session *s, int which, int levels, int patch, int iters,
+                                int downscale)
+{
+    if (which != 0 && which != 1) {
+        set_error("which must be 0 (to previous) or 1 (to next)");
+        return SS_VALUE_ERROR;
+    }
+    const int64_t t = s->solved_through + 1, other = which == 0 ? t - 1 : t + 1;
+    const auto *a = find_pos(s, t), *b = find_pos(s, other);
+    if (!a || !b) {
+        set_error("frames " + std::to_string(t) + " and " + std::to_string(other) +
+                  " are not buffered");
+        return SS_VALUE_ERROR;
+    }
+    const dis::Options o = dis_options(levels, patch, iters, downscale);
+    if (!s->dis || !same_opts(s->dis->opts, o)) {
+        s->dis.reset(new dis::Estimator());
+        if (int rc = s->dis->init(s->h, s->w, o)) {
+            s->dis.reset();
+            return rc;
+        }
+    }
+    if (which == 0 || !s->flow_timed) SS_CUDA_TRY(cudaEventRecord(s->fev[0], s->stream));
+    if (int rc = s->dis->run(a->I, b->I, s->ci, s->uv[which], s->valid[which], s->stream)) return rc;
+    SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->stream));
+    s->flow_timed = true;
+    s->flow_for[which] = t;
+    return SS_OK;
 }
 
 int ss_session_time_conv(ss_session *s, int level, int reps, float *ms, double *flops)

@@ -1,0 +1,495 @@
+// Built-in DIS-style optical flow on B200: the reference's
+// default FlowProvider, estimate_flow (flow.py:168-325), restated for sm_100a.
+//
+// Per pyramid level (coarse to fine): scipy gaussian_filter(sigma = 1) of both
+// luma images (9 taps, "reflect", float64 accumulation in scipy's symmetric
+// order, float32 between passes), bilinear up-sampling of the previous flow,
+// one warp per 9x9 patch on the stride-4 grid (template + central gradients,
+// 2x2 Gauss-Newton Hessian, coarsest-level 7x7 integer search, 4 GN
+// iterations, SSD revert test -- every 81-term sum in numpy's pairwise order),
+// 3x3 median ("nearest") on the patch grid, np.interp densification with
+// bilinear grid sampling, and a 3x3 uniform filter (float64 sums).
+// Compiled with -fmad=false: the float32 op sequence follows numpy.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "dis.h"
+#include "ss_common.cuh"
+
+namespace ss {
+namespace dis {
+
+// ---------------------------------------------------------------------------
+// luma: (frame.astype(float32) @ [0.299, 0.587, 0.114]) (flow.py:45-51).  numpy
+// hands this to BLAS sgemv; the reference's OpenBLAS kernel evaluates
+// fma(b, wb, fma(g, wg, r * wr)) (checked bit for bit on the golden frames)
+__global__ void k_luma(const float *__restrict__ img, long n, int c, float *__restrict__ out)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (c == 1) {
+        out[i] = img[i];
+    } else {
+        out[i] = __fmaf_rn(img[i * 3 + 2], 0.114f,
+                           __fmaf_rn(img[i * 3 + 1], 0.587f, fmul(img[i * 3], 0.299f)));
+    }
+}
+
+// box_downscale (flow.py:69-80): numpy mean over (f, f): rows summed left to
+// right, then the row sums, then / f^2 in float32
+__global__ void k_box_down(const float *__restrict__ in, int h, int w, int f, int ho, int wo,
+                           float *__restrict__ out)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)ho * wo) return;
+    const int y = (int)(i / wo), x = (int)(i - (long)y * wo);
+    float tot = 0.f;
+    for (int dy = 0; dy < f; ++dy) {
+        const float *row = in + (long)(y * f + dy) * w + x * f;
+        float r = row[0];
+        for (int dx = 1; dx < f; ++dx) r = fadd(r, row[dx]);
+        tot = dy == 0 ? r : fadd(tot, r);
+    }
+    out[i] = __fdiv_rn(tot, (float)(f * f));
+}
+
+__constant__ double c_gw[9];  // gaussian_filter(sigma=1) weights, centre at [4]
+
+__device__ __forceinline__ int reflect_idx(int i, int n)
+{
+    while (i < 0 || i >= n) i = i < 0 ? -i - 1 : 2 * n - i - 1;
+    return i;
+}
+
+// one separable pass of scipy's correlate1d (symmetric kernel): centre first,
+// then (x[-j] + x[+j]) * w[j] for j = 4 .. 1, in float64; float32 output
+template <bool ALONG_Y>
+__global__ void k_gauss_pass(const float *__restrict__ in, int h, int w, float *__restrict__ out)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)h * w) return;
+    const int y = (int)(i / w), x = (int)(i - (long)y * w);
+    auto at = [&](int d) {
+        return ALONG_Y ? (double)in[(long)reflect_idx(y + d, h) * w + x]
+                       : (double)in[(long)y * w + reflect_idx(x + d, w)];
+    };
+    double t = __dmul_rn(at(0), c_gw[4]);
+#pragma unroll
+    for (int j = 4; j >= 1; --j) t = __dadd_rn(t, __dmul_rn(__dadd_rn(at(-j), at(j)), c_gw[4 - j]));
+    out[i] = (float)t;
+}
+
+// resize_bilinear (flow.py:54-66) of an (hi, wi, 2) field to (ho, wo), times s
+__global__ void k_resize_flow(const float *__restrict__ in, int hi, int wi, int ho, int wo,
+                              float ry, float rx, float s, float *__restrict__ out)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)ho * wo) return;
+    const int y = (int)(i / wo), x = (int)(i - (long)y * wo);
+    const float ys = fsub(fmul(fadd((float)y, 0.5f), ry), 0.5f);
+    const float xs = fsub(fmul(fadd((float)x, 0.5f), rx), 0.5f);
+    const Taps t = make_taps(ys, xs, hi, wi);
+    float v[2];
+    gather<2>(in, t, v);
+    out[i * 2] = fmul(v[0], s);
+    out[i * 2 + 1] = fmul(v[1], s);
+}
+
+// ---------------------------------------------------------------------------
+// patch refinement (flow.py:217-287): one warp per patch
+__device__ __forceinline__ int center_pos(int j, int n, int r, int stride, int extent)
+{
+    return j == n - 1 ? extent - 1 - r : r + j * stride;
+}
+
+// numpy pairwise sum of the n (8 <= n <= 128) values in buf: 8 strided
+// accumulators over the first n - n % 8, combined pairwise, then the tail in
+// order; all lanes receive the result
+__device__ __forceinline__ float pairwise_n(const float *buf, int lane, int n)
+{
+    __syncwarp();
+    const int body = n - n % 8;
+    float r = 0.f;
+    if (lane < 8) {
+        r = buf[lane];
+        for (int i = 8; i < body; i += 8) r = fadd(r, buf[i + lane]);
+    }
+    const float r1 = __shfl_sync(0xffffffffu, r, 1), r2 = __shfl_sync(0xffffffffu, r, 2),
+                r3 = __shfl_sync(0xffffffffu, r, 3), r4 = __shfl_sync(0xffffffffu, r, 4),
+                r5 = __shfl_sync(0xffffffffu, r, 5), r6 = __shfl_sync(0xffffffffu, r, 6),
+                r7 = __shfl_sync(0xffffffffu, r, 7);
+    float res = fadd(fadd(fadd(r, r1), fadd(r2, r3)), fadd(fadd(r4, r5), fadd(r6, r7)));
+    for (int i = body; i < n; ++i) res = fadd(res, buf[i]);
+    res = __shfl_sync(0xffffffffu, res, 0);
+    __syncwarp();
+    return res;
+}
+
+struct RefineArgs {
+    const float *a, *b;   // blurred luma of the two frames (h, w)
+    const float *uv;      // current dense flow (h, w, 2)
+    int h, w, ny, nx, r, stride, iters, exhaustive;
+    float *gu, *gv;       // patch-grid output (ny, nx)
+};
+
+__global__ void __launch_bounds__(256) k_refine(RefineArgs p)
+{
+    constexpr int MS = 4;  // patch pixels per lane: patch_size <= 11 (121 pixels)
+    __shared__ float sbuf[8][128];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long patch = (long)blockIdx.x * 8 + wid;
+    if (patch >= (long)p.ny * p.nx) return;  // warp-uniform
+    float *buf = sbuf[wid];
+    const int iy = (int)(patch / p.nx), ix = (int)(patch - (long)iy * p.nx);
+    const int cy = center_pos(iy, p.ny, p.r, p.stride, p.h);
+    const int cx = center_pos(ix, p.nx, p.r, p.stride, p.w);
+    const int h = p.h, w = p.w;
+
+    // this lane's patch pixels k = lane + 32 m (k < n), row-major in the patch
+    const int P = 2 * p.r + 1, n = P * P;
+    float T[MS], GX[MS], GY[MS], FY[MS], FX[MS];
+    bool on[MS];
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+        const int k = lane + 32 * m;
+        on[m] = k < n;
+        const int py = cy + (on[m] ? k / P : 0) - p.r, px = cx + (on[m] ? k % P : 0) - p.r;
+        const float *row = p.a + (long)py * w;
+        T[m] = row[px];
+        // _central_gradients (flow.py:306-315)
+        GX[m] = px == 0 ? fsub(row[1], row[0])
+                        : (px == w - 1 ? fsub(row[w - 1], row[w - 2]) : fmul(0.5f, fsub(row[px + 1], row[px - 1])));
+        GY[m] = py == 0 ? fsub(p.a[(long)w + px], p.a[px])
+                        : (py == h - 1 ? fsub(p.a[(long)(h - 1) * w + px], p.a[(long)(h - 2) * w + px])
+                                       : fmul(0.5f, fsub(p.a[(long)(py + 1) * w + px], p.a[(long)(py - 1) * w + px])));
+        FY[m] = (float)py;
+        FX[m] = (float)px;
+    }
+    auto sum81 = [&](float (&val)[MS]) {
+#pragma unroll
+        for (int m = 0; m < MS; ++m)
+            if (on[m]) buf[lane + 32 * m] = val[m];
+        return pairwise_n(buf, lane, n);
+    };
+    float tmp[MS];
+#pragma unroll
+    for (int m = 0; m < MS; ++m) tmp[m] = fmul(GX[m], GX[m]);
+    const float h00 = fadd(sum81(tmp), 1e-4f);
+#pragma unroll
+    for (int m = 0; m < MS; ++m) tmp[m] = fmul(GX[m], GY[m]);
+    const float h01 = sum81(tmp);
+#pragma unroll
+    for (int m = 0; m < MS; ++m) tmp[m] = fmul(GY[m], GY[m]);
+    const float h11 = fadd(sum81(tmp), 1e-4f);
+    const float det = fsub(fmul(h00, h11), fmul(h01, h01));
+    const float inv00 = __fdiv_rn(h11, det), inv01 = __fdiv_rn(-h01, det), inv11 = __fdiv_rn(h00, det);
+
+    float u = p.uv[((long)cy * w + cx) * 2], v = p.uv[((long)cy * w + cx) * 2 + 1];
+
+    // residuals of the bilinear samples of b at (p + (uu, vv)) (flow.py:254-256)
+    auto residuals = [&](float uu, float vv, float (&res)[MS]) {
+#pragma unroll
+        for (int m = 0; m < MS; ++m) {
+            const Taps t = make_taps(fadd(FY[m], vv), fadd(FX[m], uu), h, w);
+            float s;
+            gather<1>(p.b, t, &s);
+            res[m] = fsub(s, T[m]);
+        }
+    };
+    auto ssd = [&](float uu, float vv) {
+        float res[MS];
+        residuals(uu, vv, res);
+#pragma unroll
+        for (int m = 0; m < MS; ++m) res[m] = fmul(res[m], res[m]);
+        return sum81(res);
+    };
+
+    if (p.exhaustive) {  // flow.py:258-274
+        float best = ssd(u, v), bu = u, bv = v;
+        for (int dv = -3; dv <= 3; ++dv)
+            for (int du = -3; du <= 3; ++du) {
+                if (du == 0 && dv == 0) continue;
+                const float cu = fadd(u, (float)du), cv = fadd(v, (float)dv);
+                const float s = ssd(cu, cv);
+                if (s < best) {
+                    best = s;
+                    bu = cu;
+                    bv = cv;
+                }
+            }
+        u = bu;
+        v = bv;
+    }
+    const float u0 = u, v0 = v, init_ssd = ssd(u, v);  // flow.py:276-277
+    for (int it = 0; it < p.iters; ++it) {            // flow.py:278-284
+        float res[MS], t0[MS], t1[MS];
+        residuals(u, v, res);
+#pragma unroll
+        for (int m = 0; m < MS; ++m) {
+            t0[m] = fmul(GX[m], res[m]);
+            t1[m] = fmul(GY[m], res[m]);
+        }
+        const float b0 = sum81(t0), b1 = sum81(t1);
+        u = fsub(u, fadd(fmul(inv00, b0), fmul(inv01, b1)));
+        v = fsub(v, fadd(fmul(inv01, b0), fmul(inv11, b1)));
+    }
+    if (ssd(u, v) > init_ssd) {  // flow.py:285-287
+        u = u0;
+        v = v0;
+    }
+    if (lane == 0) {
+        p.gu[patch] = u;
+        p.gv[patch] = v;
+    }
+}
+
+// scipy median_filter(size=3, mode="nearest") on the (ny, nx) grid
+__global__ void k_median3(const float *__restrict__ in, int ny, int nx, float *__restrict__ out)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)ny * nx) return;
+    const int y = (int)(i / nx), x = (int)(i - (long)y * nx);
+    float v[9];
+    int k = 0;
+    for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx)
+            v[k++] = in[(long)min(max(y + dy, 0), ny - 1) * nx + min(max(x + dx, 0), nx - 1)];
+    for (int a = 1; a < 9; ++a) {  // insertion sort
+        const float t = v[a];
+        int b = a - 1;
+        while (b >= 0 && v[b] > t) {
+            v[b + 1] = v[b];
+            --b;
+        }
+        v[b + 1] = t;
+    }
+    out[i] = v[4];
+}
+
+// np.interp(pos, centres, arange(n)) in float64, then float32 (flow.py:322-324)
+__device__ __forceinline__ float grid_coord(int pos, int n, int r, int stride, int extent)
+{
+    const int c0 = r, cl = extent - 1 - r;
+    if (pos <= c0) return 0.0f;
+    if (pos >= cl) return (float)(n - 1);
+    int j = (pos - r) / stride;
+    if (j > n - 2) j = n - 2;
+    const int xj = center_pos(j, n, r, stride, extent), xj1 = center_pos(j + 1, n, r, stride, extent);
+    const double slope = 1.0 / (double)(xj1 - xj);
+    return (float)(slope * (double)(pos - xj) + (double)j);
+}
+
+// densify u and v from the grid (bilinear, flow.py:318-325) into (h, w) planes
+__global__ void k_densify(const float *__restrict__ gu, const float *__restrict__ gv, int ny,
+                          int nx, int r, int stride, int h, int w, float *__restrict__ du,
+                          float *__restrict__ dv)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)h * w) return;
+    const int y = (int)(i / w), x = (int)(i - (long)y * w);
+    const Taps t = make_taps(grid_coord(y, ny, r, stride, h), grid_coord(x, nx, r, stride, w), ny, nx);
+    gather<1>(gu, t, du + i);
+    gather<1>(gv, t, dv + i);
+}
+
+// scipy uniform_filter(size=3, mode="nearest"), one axis: ((l + c) + r) / 3 in
+// float64, float32 out; the last pass interleaves (u, v) into the flow field
+template <bool ALONG_Y, bool INTERLEAVE>
+__global__ void k_uniform3(const float *__restrict__ u, const float *__restrict__ v, int h, int w,
+                           float *__restrict__ ou, float *__restrict__ ov)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)h * w) return;
+    const int y = (int)(i / w), x = (int)(i - (long)y * w);
+    long a, c;
+    if (ALONG_Y) {
+        a = (long)max(y - 1, 0) * w + x;
+        c = (long)min(y + 1, h - 1) * w + x;
+    } else {
+        a = (long)y * w + max(x - 1, 0);
+        c = (long)y * w + min(x + 1, w - 1);
+    }
+    const float ru = (float)__ddiv_rn(__dadd_rn(__dadd_rn((double)u[a], (double)u[i]), (double)u[c]), 3.0);
+    const float rv = (float)__ddiv_rn(__dadd_rn(__dadd_rn((double)v[a], (double)v[i]), (double)v[c]), 3.0);
+    if (INTERLEAVE) {
+        ou[i * 2] = ru;
+        ou[i * 2 + 1] = rv;
+    } else {
+        ou[i] = ru;
+        ov[i] = rv;
+    }
+}
+
+__global__ void k_finish(const float *__restrict__ uv, long n, float *__restrict__ out,
+                         uint8_t *__restrict__ valid)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float a = uv[2 * i], b = uv[2 * i + 1];
+    out[2 * i] = a;
+    out[2 * i + 1] = b;
+    // FlowField validity: |component| <= 1e9 (imgio.py:172)
+    if (valid) valid[i] = fmaxf(fabsf(a), fabsf(b)) <= 1e9f ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+static int centers(int extent, int r, int stride)
+{
+    const int last = extent - 1 - r;
+    int n = (last - r) / stride + 1;
+    if (r + (n - 1) * stride != last) ++n;
+    return n;
+}
+
+Estimator::~Estimator()
+{
+    for (void *p : allocs) cudaFree(p);
+}
+
+int Estimator::init(int h_, int w_, const Options &o)
+{
+    h = h_;
+    w = w_;
+    opts = o;
+    if (o.levels < 1 || o.patch < 3 || o.patch % 2 == 0 || (o.downscale != 1 && o.downscale != 2 && o.downscale != 4)) {
+        set_error("invalid flow options");
+        return SS_VALUE_ERROR;
+    }
+    if (o.patch > 11) {
+        set_error("patch_size > 11 is not supported by the GPU estimator");
+        return SS_VALUE_ERROR;
+    }
+    const int h0 = o.downscale > 1 ? (h / o.downscale) : h;
+    const int w0 = o.downscale > 1 ? (w / o.downscale) : w;
+    if (std::min(h0, w0) < o.patch) {
+        set_error("resolution " + std::to_string(w0) + "x" + std::to_string(h0) +
+                  " smaller than patch size " + std::to_string(o.patch));
+        return SS_VALUE_ERROR;
+    }
+    // pyramid shapes (flow.py:197-201)
+    lh.assign(1, h0);
+    lw.assign(1, w0);
+    while ((int)lh.size() < o.levels && std::min(lh.back(), lw.back()) >= 2 * o.patch) {
+        lh.push_back(lh.back() / 2);
+        lw.push_back(lw.back() / 2);
+    }
+    auto alloc = [&](float **p, size_t n) -> int {
+        SS_CUDA_TRY(cudaMalloc(p, std::max<size_t>(n, 1) * sizeof(float)));
+        allocs.push_back(*p);
+        return SS_OK;
+    };
+    const int L = (int)lh.size();
+    g1.assign(L, nullptr);
+    g2.assign(L, nullptr);
+    int rc;
+    size_t maxpx = 0;
+    for (int l = 0; l < L; ++l) {
+        const size_t px = (size_t)lh[l] * lw[l];
+        maxpx = std::max(maxpx, px);
+        if ((rc = alloc(&g1[l], px)) || (rc = alloc(&g2[l], px))) return rc;
+    }
+    const int r = o.patch / 2, stride = std::max(1, o.patch / 2);
+    size_t maxgrid = 0;
+    for (int l = 0; l < L; ++l)
+        maxgrid = std::max(maxgrid, (size_t)centers(lh[l], r, stride) * centers(lw[l], r, stride));
+    if ((rc = alloc(&ga, maxpx)) || (rc = alloc(&gb, maxpx)) || (rc = alloc(&tmp, maxpx)) ||
+        (rc = alloc(&uvA, 2 * maxpx)) || (rc = alloc(&uvB, 2 * maxpx)) ||
+        (rc = alloc(&du, maxpx)) || (rc = alloc(&dv, maxpx)) || (rc = alloc(&du2, maxpx)) ||
+        (rc = alloc(&dv2, maxpx)) || (rc = alloc(&gu, maxgrid)) || (rc = alloc(&gv, maxgrid)) ||
+        (rc = alloc(&gu2, maxgrid)) || (rc = alloc(&gv2, maxgrid)) || (rc = alloc(&lum1, (size_t)h * w)) ||
+        (rc = alloc(&lum2, (size_t)h * w)))
+        return rc;
+    if (o.downscale > 1 && (rc = alloc(&full, 2 * (size_t)h * w))) return rc;
+    return SS_OK;
+}
+
+int Estimator::run(const float *fa, const float *fb, int c, float *uv_out, uint8_t *valid,
+                   cudaStream_t st)
+{
+    static bool wset = false;
+    if (!wset) {  // scipy _gaussian_kernel1d(sigma=1, order=0, radius=4), float64
+        double x[9];
+        for (int i = 0; i < 9; ++i) x[i] = std::exp(-0.5 * (double)((i - 4) * (i - 4)));
+        // phi_x.sum(): numpy pairwise order for 9 elements
+        const double s = (((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]))) + x[8];
+        for (double &v : x) v /= s;
+        SS_CUDA_TRY(cudaMemcpyToSymbol(c_gw, x, sizeof x));
+        wset = true;
+    }
+    const int T = 256;
+    const long n = (long)h * w;
+    k_luma<<<blocks_for(n, T), T, 0, st>>>(fa, n, c, lum1);
+    k_luma<<<blocks_for(n, T), T, 0, st>>>(fb, n, c, lum2);
+    const int L = (int)lh.size();
+    if (opts.downscale > 1) {
+        const long m = (long)lh[0] * lw[0];
+        k_box_down<<<blocks_for(m, T), T, 0, st>>>(lum1, h, w, opts.downscale, lh[0], lw[0], g1[0]);
+        k_box_down<<<blocks_for(m, T), T, 0, st>>>(lum2, h, w, opts.downscale, lh[0], lw[0], g2[0]);
+    } else {
+        SS_CUDA_TRY(cudaMemcpyAsync(g1[0], lum1, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        SS_CUDA_TRY(cudaMemcpyAsync(g2[0], lum2, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    }
+    for (int l = 1; l < L; ++l) {
+        const long m = (long)lh[l] * lw[l];
+        k_box_down<<<blocks_for(m, T), T, 0, st>>>(g1[l - 1], lh[l - 1], lw[l - 1], 2, lh[l], lw[l], g1[l]);
+        k_box_down<<<blocks_for(m, T), T, 0, st>>>(g2[l - 1], lh[l - 1], lw[l - 1], 2, lh[l], lw[l], g2[l]);
+    }
+    const int r = opts.patch / 2, stride = std::max(1, opts.patch / 2);
+    float *uv = uvA, *uv_next = uvB;
+    SS_CUDA_TRY(cudaMemsetAsync(uv, 0, 2 * (size_t)lh[L - 1] * lw[L - 1] * sizeof(float), st));
+    int ph = lh[L - 1], pw = lw[L - 1];
+    for (int l = L - 1; l >= 0; --l) {
+        const int hl = lh[l], wl = lw[l];
+        const long m = (long)hl * wl;
+        // gaussian_filter(., 1.0): axis 0 then axis 1 (flow.py:207-208)
+        k_gauss_pass<true><<<blocks_for(m, T), T, 0, st>>>(g1[l], hl, wl, tmp);
+        k_gauss_pass<false><<<blocks_for(m, T), T, 0, st>>>(tmp, hl, wl, ga);
+        k_gauss_pass<true><<<blocks_for(m, T), T, 0, st>>>(g2[l], hl, wl, tmp);
+        k_gauss_pass<false><<<blocks_for(m, T), T, 0, st>>>(tmp, hl, wl, gb);
+        if (ph != hl || pw != wl) {  // flow.py:209-211
+            const float scale = (float)((double)hl / (double)ph);
+            k_resize_flow<<<blocks_for(m, T), T, 0, st>>>(uv, ph, pw, hl, wl,
+                                                           (float)((double)ph / hl),
+                                                           (float)((double)pw / wl), scale, uv_next);
+            std::swap(uv, uv_next);
+        }
+        const int ny = centers(hl, r, stride), nx = centers(wl, r, stride);
+        RefineArgs a;
+        a.a = ga;
+        a.b = gb;
+        a.uv = uv;
+        a.h = hl;
+        a.w = wl;
+        a.ny = ny;
+        a.nx = nx;
+        a.r = r;
+        a.stride = stride;
+        a.iters = opts.iters;
+        a.exhaustive = l == L - 1;
+        a.gu = gu;
+        a.gv = gv;
+        const long np = (long)ny * nx;
+        k_refine<<<(unsigned)((np + 7) / 8), 256, 0, st>>>(a);
+        k_median3<<<blocks_for(np, T), T, 0, st>>>(gu, ny, nx, gu2);
+        k_median3<<<blocks_for(np, T), T, 0, st>>>(gv, ny, nx, gv2);
+        k_densify<<<blocks_for(m, T), T, 0, st>>>(gu2, gv2, ny, nx, r, stride, hl, wl, du, dv);
+        k_uniform3<true, false><<<blocks_for(m, T), T, 0, st>>>(du, dv, hl, wl, du2, dv2);
+        k_uniform3<false, true><<<blocks_for(m, T), T, 0, st>>>(du2, dv2, hl, wl, uv_next, nullptr);
+        std::swap(uv, uv_next);
+        ph = hl;
+        pw = wl;
+    }
+    if (opts.downscale > 1) {  // flow.py:187: resize to (h, w) * downscale
+        k_resize_flow<<<blocks_for(n, T), T, 0, st>>>(uv, ph, pw, h, w, (float)((double)ph / h),
+                                                       (float)((double)pw / w),
+                                                       (float)opts.downscale, full);
+        uv = full;
+    }
+    k_finish<<<blocks_for(n, T), T, 0, st>>>(uv, n, uv_out, valid);
+    SS_LAUNCH_CHECK("dis");
+    return SS_OK;
+}
+
+}  // namespace dis
+}  // namespace ss

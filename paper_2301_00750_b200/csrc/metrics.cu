@@ -114,9 +114,9 @@ __device__ __forceinline__ int reflect(int i, int n)
     return i;
 }
 
-// luma in float32 exactly as frame.astype(float32) @ LUMA_WEIGHTS is not
-// reproducible bit for bit (BLAS order); it is computed as ((r*wr + g*wg) + b*wb)
-// in float32, then widened to float64 like ssim() does
+// luma = frame.astype(float32) @ LUMA_WEIGHTS (flow.py:45-51), which numpy
+// hands to BLAS sgemv: fma(b, wb, fma(g, wg, r * wr)) in float32 (see dis.cu),
+// then widened to float64 like ssim() does
 template <int C>
 __global__ void k_luma64(const float *__restrict__ img, long n, double *__restrict__ out)
 {
@@ -125,8 +125,8 @@ __global__ void k_luma64(const float *__restrict__ img, long n, double *__restri
     if (C == 1) {
         out[i] = (double)img[i];
     } else {
-        const float l = __fadd_rn(__fadd_rn(__fmul_rn(img[i * 3], 0.299f), __fmul_rn(img[i * 3 + 1], 0.587f)),
-                                  __fmul_rn(img[i * 3 + 2], 0.114f));
+        const float l = __fmaf_rn(img[i * 3 + 2], 0.114f,
+                                  __fmaf_rn(img[i * 3 + 1], 0.587f, __fmul_rn(img[i * 3], 0.299f)));
         out[i] = (double)l;
     }
 }

@@ -9,6 +9,7 @@ flow straight into a session's device slot implement ``device_flow``.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
 from typing import Protocol
 
 import numpy as np
@@ -108,6 +109,65 @@ class ConstantFlow:
 
     def device_flow(self, session, which: int, pos_a: int, pos_b: int) -> None:
         _dev.check(_lib.lib().ss_set_constant_flow(session, which, self.u, self.v, pos_b - pos_a))
+
+
+@dataclass(frozen=True)
+class FlowOptions:
+    """flow.py:27-42 -- tuning knobs of the built-in estimator."""
+
+    levels: int = 5
+    patch_size: int = 9
+    iterations_per_level: int = 4
+    downscale: int = 1
+
+    def __post_init__(self):
+        if self.levels < 1:
+            raise ValueError("levels must be >= 1")
+        if self.patch_size < 3 or self.patch_size % 2 == 0:
+            raise ValueError("patch_size must be odd and >= 3")
+        if self.downscale not in (1, 2, 4):
+            raise ValueError("downscale must be 1, 2 or 4")
+
+
+def estimate_flow(from_frame, to_frame, opts: FlowOptions = FlowOptions()) -> FlowField:
+    """flow.py:168-189: DIS-style coarse-to-fine inverse-search flow from
+    ``from_frame`` toward ``to_frame``, on the GPU (csrc/dis.cu)."""
+    if tuple(from_frame.shape[:2]) != tuple(to_frame.shape[:2]):
+        raise ResolutionMismatch(
+            f"frames differ: {tuple(from_frame.shape[:2])} vs {tuple(to_frame.shape[:2])}")
+    host = not _dev.is_torch(from_frame)
+    a, b = _dev.to_dev(from_frame), _dev.to_dev(to_frame)
+    if a.ndim == 2:
+        a, b = a[:, :, None].contiguous(), b[:, :, None].contiguous()
+    h, w, c = a.shape
+    t = _dev.torch()
+    uv = t.empty((h, w, 2), device=a.device, dtype=t.float32)
+    valid = t.empty((h, w), device=a.device, dtype=t.uint8)
+    _dev.check(_lib.lib().ss_dis_flow(a.data_ptr(), b.data_ptr(), h, w, c, opts.levels,
+                                      opts.patch_size, opts.iterations_per_level, opts.downscale,
+                                      uv.data_ptr(), valid.data_ptr(), _dev.stream_ptr()))
+    if host:
+        t.cuda.current_stream().synchronize()
+        return FlowField(uv.cpu().numpy(), valid.cpu().numpy().astype(bool))
+    return FlowField(uv, valid.bool())
+
+
+class BuiltinFlow:
+    """flow.py:361-369: the reference's default provider, on B200.  Inside a
+    session the flow is written straight into the session's HBM flow slot."""
+
+    def __init__(self, opts: FlowOptions = FlowOptions()):
+        self.opts = opts
+        self.backend_id = (f"builtin(levels={opts.levels},patch={opts.patch_size},"
+                           f"downscale={opts.downscale})")
+
+    def flow_between(self, pos_a, frame_a, pos_b, frame_b) -> FlowField:
+        return estimate_flow(frame_a, frame_b, self.opts)
+
+    def device_flow(self, session, which: int, pos_a: int, pos_b: int) -> None:
+        o = self.opts
+        _dev.check(_lib.lib().ss_session_compute_dis_flow(session, which, o.levels, o.patch_size,
+                                                          o.iterations_per_level, o.downscale))
 
 
 class ReplayFlow:

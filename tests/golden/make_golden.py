@@ -255,8 +255,36 @@ def make_metrics(flow, imgio, synthetic):
     _save("metrics.npz", **out)
 
 
+def make_dis(flow, synthetic):
+    """Reference DIS flows (estimate_flow, flow.py:168-325) for GPU parity."""
+    out = {}
+    rng = np.random.default_rng(606)
+    tex = synthetic.noise_texture(128, 128, rng)
+    tex2 = synthetic.noise_texture(128, 128, rng, smoothness=2.5)
+    seq = synthetic.translating_sequence(frames=3, height=96, width=128, step=(2, 1), seed=12)
+    gray = flow.luma(seq.inputs[0])[:, :, None]
+    cases = [
+        ("shift", tex, np.roll(tex, shift=(3, 5), axis=(0, 1)), flow.FlowOptions()),
+        ("same", tex[:64, :64], tex[:64, :64], flow.FlowOptions()),
+        ("down2", tex2, np.roll(tex2, shift=(2, 4), axis=(0, 1)), flow.FlowOptions(downscale=2)),
+        ("seqprev", seq.inputs[1], seq.inputs[0], flow.FlowOptions()),
+        ("seqnext", seq.inputs[1], seq.inputs[2], flow.FlowOptions()),
+        ("gray", gray, np.roll(gray, shift=(1, -2), axis=(0, 1)), flow.FlowOptions(levels=3)),
+        ("odd", seq.inputs[0][:77, :101], seq.inputs[1][:77, :101], flow.FlowOptions(patch_size=7)),
+    ]
+    for tag, a, b, opts in cases:
+        f = flow.estimate_flow(a, b, opts)
+        out[f"{tag}_a"] = np.asarray(a, np.float32)
+        out[f"{tag}_b"] = np.asarray(b, np.float32)
+        out[f"{tag}_uv"] = f.uv
+        out[f"{tag}_opts"] = np.array([opts.levels, opts.patch_size, opts.iterations_per_level,
+                                       opts.downscale])
+    _save("dis.npz", **out)
+
+
 def main():
     consistency, flow, imgio, synthetic = _import_ref()
+    make_dis(flow, synthetic)
     make_warp(flow, imgio)
     make_occlusion(flow, imgio)
     make_weights(consistency)
