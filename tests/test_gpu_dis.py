@@ -65,6 +65,21 @@ def test_dis_reference_flow_tests(ss):
         FlowOptions(downscale=3)
 
 
+def test_reference_default_path_end_to_end(ss, golden):
+    """The reference's default configuration end to end -- stabilize_stream with
+    BuiltinFlow() -- on the golden "dis" stream: GPU flows are computed on the
+    device (not replayed) and the outputs match the reference's within the exp
+    ulp tolerance of the consistency step."""
+    from conftest import stream_case
+    from paper_2301_00750_b200.flow import BuiltinFlow
+
+    g = golden("streams.npz")
+    inputs, processed, outputs, _, _ = stream_case(g, "dis")
+    got = dict(ss.stabilize_stream(zip(inputs, processed), ss.preset("default"), BuiltinFlow()))
+    assert sorted(got) == sorted(outputs)
+    assert max(float(np.abs(got[t] - outputs[t]).max()) for t in got) <= 1e-5
+
+
 def test_builtin_flow_session_matches_stateless(ss):
     """BuiltinFlow inside a session (device slot) == the stateless estimator,
     and the stream stays within 1e-3 of the oracle fed the same flows."""
