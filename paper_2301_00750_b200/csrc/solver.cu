@@ -104,6 +104,7 @@ struct BlockedArgs {
     int h, w, c;
     int iters;                // iterations in this pass (<= K)
     float eta, kappa;
+    float negzero;            // -0.0f, passed at run time (see fmul2)
     unsigned *maxbits;        // this pass's slot
 };
 
@@ -130,16 +131,39 @@ __device__ __forceinline__ float sgd_update(float o, float op, float N, float S,
     return fadd(fsub(o, g), m);
 }
 
+// The same update for the thread's two columns at once with packed FP32
+// (FFMA2 / FADD2 / FMUL2): per lane identical IEEE ops, half the instructions.
+__device__ __forceinline__ float2 sgd_update2(float2 o, float2 op, float2 N, float2 S, float2 W,
+                                              float2 E, float2 lp, float2 a, float2 wcv,
+                                              float2 eta, float2 kappa, float2 z)
+{
+    float2 g = ffma2(o, make_float2(-4.0f, -4.0f), N);
+    g = fadd2(g, S);
+    g = fadd2(g, W);
+    g = fadd2(g, E);
+    g = fsub2(g, lp);
+    float2 d = fsub2(o, a);
+    d = fmul2(d, wcv, z);
+    g = fsub2(d, g);
+    g = fmul2(g, eta, z);
+    float2 m = fsub2(o, op);
+    m = fmul2(m, kappa, z);
+    return fadd2(fsub2(o, g), m);
+}
+
+__device__ __forceinline__ float &el(float2 &v, int k) { return k ? v.y : v.x; }
+__device__ __forceinline__ float el(const float2 &v, int k) { return k ? v.y : v.x; }
+
 // One iteration for one thread's 2 x R block.  X holds the current iterate,
 // Y the previous one; Y is overwritten with the new iterate (the caller swaps
 // roles).  Reads neighbours from smem buffer `cur`, writes new values to `nxt`.
 template <bool FAST, int P>
-__device__ __forceinline__ void blk_iter(float (&X)[blk::R][2], float (&Y)[blk::R][2],
-                                         const float (&Av)[blk::R][2],
-                                         const float (&Lv)[blk::R][2],
-                                         const float (&Wv)[blk::R][2], const float *cur,
+__device__ __forceinline__ void blk_iter(float2 (&X)[blk::R], float2 (&Y)[blk::R],
+                                         const float2 (&Av)[blk::R], const float2 (&Lv)[blk::R],
+                                         const float2 (&Wv)[blk::R], const float *cur,
                                          float *nxt, int r0, int c0, int lo_r, int hi_r,
-                                         int lo_c, int hi_c, float eta, float kappa, float &mx)
+                                         int lo_c, int hi_c, float eta, float kappa,
+                                         float negzero, float &mx)
 {
     using namespace blk;
     if (FAST) {
@@ -151,19 +175,17 @@ __device__ __forceinline__ void blk_iter(float (&X)[blk::R][2], float (&Y)[blk::
         }
         const float2 nv = *reinterpret_cast<const float2 *>(cur + r0 * P + c0 + 2);
         const float2 sv = *reinterpret_cast<const float2 *>(cur + (r0 + R + 1) * P + c0 + 2);
+        const float2 eta2 = make_float2(eta, eta), kap2 = make_float2(kappa, kappa);
+        const float2 z2 = make_float2(negzero, negzero);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const float n0 = r == 0 ? nv.x : X[r - 1][0];
-            const float n1 = r == 0 ? nv.y : X[r - 1][1];
-            const float s0 = r == R - 1 ? sv.x : X[r + 1][0];
-            const float s1 = r == R - 1 ? sv.y : X[r + 1][1];
-            const float u0 = sgd_update(X[r][0], Y[r][0], n0, s0, wv[r], X[r][1], Lv[r][0],
-                                        Av[r][0], Wv[r][0], eta, kappa);
-            const float u1 = sgd_update(X[r][1], Y[r][1], n1, s1, X[r][0], ev[r], Lv[r][1],
-                                        Av[r][1], Wv[r][1], eta, kappa);
-            Y[r][0] = u0;
-            Y[r][1] = u1;
-            mx = fmaxf(mx, fmaxf(fabsf(u0), fabsf(u1)));
+            const float2 n = r == 0 ? nv : X[r - 1];
+            const float2 s = r == R - 1 ? sv : X[r + 1];
+            const float2 wn = make_float2(wv[r], X[r].x), en = make_float2(X[r].y, ev[r]);
+            const float2 u =
+                sgd_update2(X[r], Y[r], n, s, wn, en, Lv[r], Av[r], Wv[r], eta2, kap2, z2);
+            Y[r] = u;
+            mx = fmaxf(mx, fmaxf(fabsf(u.x), fabsf(u.y)));
         }
     } else {
 #pragma unroll
@@ -178,34 +200,33 @@ __device__ __forceinline__ void blk_iter(float (&X)[blk::R][2], float (&Y)[blk::
                 const float S = cur[(sr + 1) * P + cc + 2];
                 const float Wn = cur[(rr + 1) * P + wcl + 2];
                 const float En = cur[(rr + 1) * P + ecl + 2];
-                const float u = sgd_update(X[r][k], Y[r][k], N, S, Wn, En, Lv[r][k], Av[r][k],
-                                           Wv[r][k], eta, kappa);
-                Y[r][k] = u;
+                const float u = sgd_update(el(X[r], k), el(Y[r], k), N, S, Wn, En, el(Lv[r], k),
+                                           el(Av[r], k), el(Wv[r], k), eta, kappa);
+                el(Y[r], k) = u;
                 mx = fmaxf(mx, fabsf(u));
             }
         }
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-        *reinterpret_cast<float2 *>(nxt + (r0 + r + 1) * P + c0 + 2) = make_float2(Y[r][0], Y[r][1]);
+    for (int r = 0; r < R; ++r) *reinterpret_cast<float2 *>(nxt + (r0 + r + 1) * P + c0 + 2) = Y[r];
 }
 
 template <bool FAST, int P>
-__device__ __forceinline__ void blk_run(float (&X)[blk::R][2], float (&Y)[blk::R][2],
-                                        const float (&Av)[blk::R][2],
-                                        const float (&Lv)[blk::R][2],
-                                        const float (&Wv)[blk::R][2], float *sm0, float *sm1,
+__device__ __forceinline__ void blk_run(float2 (&X)[blk::R], float2 (&Y)[blk::R],
+                                        const float2 (&Av)[blk::R], const float2 (&Lv)[blk::R],
+                                        const float2 (&Wv)[blk::R], float *sm0, float *sm1,
                                         int r0, int c0, int lo_r, int hi_r, int lo_c, int hi_c,
-                                        int iters, float eta, float kappa, float &mx)
+                                        int iters, float eta, float kappa, float negzero,
+                                        float &mx)
 {
     // iterations alternate roles: even -> (X cur, Y prev) read sm0 write sm1
     for (int it = 0; it < iters; it += 2) {
         blk_iter<FAST, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, eta, kappa,
-                          mx);
+                          negzero, mx);
         __syncthreads();
         if (it + 1 < iters) {
             blk_iter<FAST, P>(Y, X, Av, Lv, Wv, sm1, sm0, r0, c0, lo_r, hi_r, lo_c, hi_c, eta,
-                              kappa, mx);
+                              kappa, negzero, mx);
             __syncthreads();
         }
     }
@@ -214,10 +235,9 @@ __device__ __forceinline__ void blk_run(float (&X)[blk::R][2], float (&Y)[blk::R
 // run one region's iterations (fast or edge path, warp-uniform) and write the
 // interior back; returns the max-bits contribution of this thread
 template <int P>
-__device__ __forceinline__ unsigned blk_tile(float (&X)[blk::R][2], float (&Y)[blk::R][2],
-                                             const float (&Av)[blk::R][2],
-                                             const float (&Lv)[blk::R][2],
-                                             const float (&Wv)[blk::R][2], float *sm0, float *sm1,
+__device__ __forceinline__ unsigned blk_tile(float2 (&X)[blk::R], float2 (&Y)[blk::R],
+                                             const float2 (&Av)[blk::R], const float2 (&Lv)[blk::R],
+                                             const float2 (&Wv)[blk::R], float *sm0, float *sm1,
                                              const BlockedArgs &a, int K, int rx0, int ry0, int ch)
 {
     using namespace blk;
@@ -237,10 +257,10 @@ __device__ __forceinline__ unsigned blk_tile(float (&X)[blk::R][2], float (&Y)[b
     float mx = 0.0f;
     if (fast)
         blk_run<true, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters,
-                         a.eta, a.kappa, mx);
+                         a.eta, a.kappa, a.negzero, mx);
     else
         blk_run<false, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters,
-                          a.eta, a.kappa, mx);
+                          a.eta, a.kappa, a.negzero, mx);
 
     // after an odd number of iterations the current iterate lives in Y
     const bool odd = a.iters & 1;
@@ -252,8 +272,8 @@ __device__ __forceinline__ unsigned blk_tile(float (&X)[blk::R][2], float (&Y)[b
         const bool interior_r = r0 + r >= K && r0 + r < RH - K;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const float o = odd ? Y[r][k] : X[r][k];
-            const float op = odd ? X[r][k] : Y[r][k];
+            const float o = odd ? el(Y[r], k) : el(X[r], k);
+            const float op = odd ? el(X[r], k) : el(Y[r], k);
             nan_seen |= (o != o);
             const int gx = gx0 + k;
             if (interior_r && interior_c && gy < h && gx < w) {
@@ -296,7 +316,7 @@ __global__ void __launch_bounds__(blk::THREADS, 1) k_sgd_blocked(BlockedArgs a)
     // zero both buffers (padding must be finite; interior is overwritten)
     for (int i = threadIdx.y * PAIRS + threadIdx.x; i < 2 * SH * SW; i += THREADS) sm0[i] = 0.0f;
 
-    float X[R][2], Y[R][2], Av[R][2], Lv[R][2], Wv[R][2];
+    float2 X[R], Y[R], Av[R], Lv[R], Wv[R];
     const int gx0 = rx0 + c0, gy0 = ry0 + r0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -305,17 +325,16 @@ __global__ void __launch_bounds__(blk::THREADS, 1) k_sgd_blocked(BlockedArgs a)
         for (int k = 0; k < 2; ++k) {
             const int gx = min(max(gx0 + k, 0), w - 1);
             const long q = (long)gy * w + gx;
-            X[r][k] = __ldg(a.O + plane + q);
-            Y[r][k] = __ldg(a.Oprev + plane + q);
-            Av[r][k] = __ldg(a.A + plane + q);
-            Lv[r][k] = __ldg(a.lapP + plane + q);
-            Wv[r][k] = __ldg(a.wc + q);
+            el(X[r], k) = __ldg(a.O + plane + q);
+            el(Y[r], k) = __ldg(a.Oprev + plane + q);
+            el(Av[r], k) = __ldg(a.A + plane + q);
+            el(Lv[r], k) = __ldg(a.lapP + plane + q);
+            el(Wv[r], k) = __ldg(a.wc + q);
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-        *reinterpret_cast<float2 *>(sm0 + (r0 + r + 1) * SW + c0 + 2) = make_float2(X[r][0], X[r][1]);
+    for (int r = 0; r < R; ++r) *reinterpret_cast<float2 *>(sm0 + (r0 + r + 1) * SW + c0 + 2) = X[r];
     __syncthreads();
     const unsigned bits = blk_tile<SW>(X, Y, Av, Lv, Wv, sm0, sm1, a, K, rx0, ry0, ch);
     push_maxbits(bits, a.maxbits);
@@ -423,21 +442,16 @@ __global__ void __launch_bounds__(blk::THREADS, 1)
         const int rx0 = tx * OW - K, ry0 = ty * OH - K;
         mbar_wait(bar, phase);
         phase ^= 1;
-        float X[R][2], Y[R][2], Av[R][2], Lv[R][2], Wv[R][2];
+        float2 X[R], Y[R], Av[R], Lv[R], Wv[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int o = (r0 + r) * RW + c0;
-            const float2 x2 = *reinterpret_cast<const float2 *>(stage + 0 * STAGE + o);
-            const float2 y2 = *reinterpret_cast<const float2 *>(stage + 1 * STAGE + o);
-            const float2 a2 = *reinterpret_cast<const float2 *>(stage + 2 * STAGE + o);
-            const float2 l2 = *reinterpret_cast<const float2 *>(stage + 3 * STAGE + o);
-            const float2 w2 = *reinterpret_cast<const float2 *>(stage + 4 * STAGE + o);
-            X[r][0] = x2.x; X[r][1] = x2.y;
-            Y[r][0] = y2.x; Y[r][1] = y2.y;
-            Av[r][0] = a2.x; Av[r][1] = a2.y;
-            Lv[r][0] = l2.x; Lv[r][1] = l2.y;
-            Wv[r][0] = w2.x; Wv[r][1] = w2.y;
-            *reinterpret_cast<float2 *>(sm0 + (r0 + r + 1) * SW2 + c0 + 2) = x2;
+            X[r] = *reinterpret_cast<const float2 *>(stage + 0 * STAGE + o);
+            Y[r] = *reinterpret_cast<const float2 *>(stage + 1 * STAGE + o);
+            Av[r] = *reinterpret_cast<const float2 *>(stage + 2 * STAGE + o);
+            Lv[r] = *reinterpret_cast<const float2 *>(stage + 3 * STAGE + o);
+            Wv[r] = *reinterpret_cast<const float2 *>(stage + 4 * STAGE + o);
+            *reinterpret_cast<float2 *>(sm0 + (r0 + r + 1) * SW2 + c0 + 2) = X[r];
         }
         __syncthreads();  // stage consumed, sm0 holds O
         if (tid == 0 && t + (int)gridDim.x < ntiles) {
@@ -836,6 +850,7 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
             a.iters = std::min(K, iters - ps * K);
             a.eta = p.eta;
             a.kappa = p.kappa;
+            a.negzero = -0.0f;
             a.maxbits = wk.maxbits + ps;
             if (variant == 2) {
                 const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];

@@ -36,6 +36,41 @@ __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b)
 __device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
 
+// Packed FP32 (sm_100 FADD2 / FMUL2 / FFMA2): two independent IEEE
+// round-to-nearest operations per instruction -- bit-identical per lane to the
+// scalar __f*_rn forms.
+__device__ __forceinline__ uint64_t f2u(float2 a) { return *reinterpret_cast<uint64_t *>(&a); }
+__device__ __forceinline__ float2 u2f(uint64_t a) { return *reinterpret_cast<float2 *>(&a); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b)
+{
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b)
+{
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+// a * b + z with z = (-0, -0) supplied at RUN time: exactly round(a * b)
+// (including the sign of zero).  ptxas contracts mul.rn.f32x2 -- and an fma
+// with a literal -0 addend -- into a following add/sub as one FFMA2, which
+// would skip the product's rounding; an addend it cannot see as zero keeps the
+// product a separate instruction, as numpy's is.
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b, float2 z)
+{
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(z)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c)
+{
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(d);
+}
+
 // Bilinear tap set of flow.py:83-99 for one sample position (ys, xs) before
 // clamping: clamp to [0, h-1] x [0, w-1], floor, +1 neighbours clamped, and the
 // fractional weights (exact in float32, flow.py:95-96).
