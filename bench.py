@@ -227,7 +227,7 @@ def main():
 
     import paper_2301_00750_b200 as ss
     from paper_2301_00750_b200 import _lib
-    from paper_2301_00750_b200.consistency import _run_step
+    from paper_2301_00750_b200.consistency import _run_step, _start_flow_to_prev
     from paper_2301_00750_b200.synthetic import DeviceSequence
 
     h, w = args.height, args.width
@@ -262,6 +262,7 @@ def main():
     push()
 
     def step():
+        _start_flow_to_prev(state, flow)  # stabilize_stream's order
         push()
         state.params = params_for(pos)
         _run_step(state, flow, with_next=True, return_host=False)
@@ -411,11 +412,15 @@ def run_e2e(args, L, state, pool, flow, torch, dist):
 
     def step(k):
         pos[0] += 1
+        if use_cnn:
+            # flow t -> t-1 needs only buffered frames: start it on the side
+            # stream first so the host->device copy of frame t+1 overlaps it
+            # (the order consistency.stabilize_stream uses)
+            _check(L.ss_session_compute_flow(sess, 0), L)
         _check(L.ss_push_pair(sess, pos[0], host_i[k % n_host].data_ptr(),
                               host_p[k % n_host].data_ptr(), _lib.SS_F32, _lib.SS_HOST), L)
         t = int(L.ss_solved_through(sess)) + 1
         if use_cnn:
-            _check(L.ss_session_compute_flow(sess, 0), L)
             _check(L.ss_session_compute_flow(sess, 1), L)
         elif args.flow == "dis":
             for which in (0, 1):
@@ -445,8 +450,8 @@ def run_e2e(args, L, state, pool, flow, torch, dist):
     world = dist.get_world_size() if dist else 1
     return {"value": round(world * args.steps / dt, 3), "unit": "frames/s",
             "h2d_bytes_per_step": 2 * h * w * 3 * 4, "d2h_bytes_per_step": h * w * 3 * 4,
-            "path": "C ABI: ss_push_pair(host pinned f32) + ss_session_compute_flow x2 + ss_step "
-                    "+ ss_output(host pinned)",
+            "path": "C ABI: ss_session_compute_flow(0) + ss_push_pair(host pinned f32) + "
+                    "ss_session_compute_flow(1) + ss_step + ss_output(host pinned)",
             "timer": "host wall clock around K steps, device synchronised at both ends"}
 
 

@@ -272,6 +272,7 @@ class SessionState:
         self._first_output = None
         self._out_cache = None
         self._squeeze = False
+        self._flow0_for = None  # step whose flow t -> t-1 was started early
 
     # -- device session ------------------------------------------------------
     def _ensure_session(self, input_frame, processed_frame):
@@ -411,11 +412,29 @@ def _provide_flow(state: SessionState, flow_backend, which: int, t: int, other: 
                                  _lib.SS_HOST))
 
 
+def _start_flow_to_prev(state: SessionState, flow_backend) -> None:
+    """Start the pending step's flow t -> t-1 before the next pair is pushed.
+
+    It needs only frames already buffered; with a device-native provider it
+    runs on the session's side stream, so the host->device copy of the next
+    pair overlaps it.  _run_step then skips it (pure scheduling: same flow).
+    """
+    if not hasattr(flow_backend, "device_flow") or state.handle is None:
+        return
+    t = state.solved_through + 1
+    if not any(p == t - 1 for p, _, _ in state.pairs) or not any(p == t for p, _, _ in state.pairs):
+        return
+    _provide_flow(state, flow_backend, 0, t, t - 1)
+    state._flow0_for = t
+
+
 def _run_step(state: SessionState, flow_backend, with_next: bool, return_host: bool = True):
     t = state._snippet(want_next=with_next)
     params = state.params
     t0 = time.perf_counter()
-    _provide_flow(state, flow_backend, 0, t, t - 1)
+    if state._flow0_for != t:
+        _provide_flow(state, flow_backend, 0, t, t - 1)
+    state._flow0_for = None
     if with_next:
         _provide_flow(state, flow_backend, 1, t, t + 1)
     flow_ms = (time.perf_counter() - t0) * 1e3
@@ -459,6 +478,8 @@ def stabilize_stream(pairs, params: ConsistencyParams, flow_backend: FlowProvide
     position = 0
     for input_frame, processed_frame in pairs:
         position += 1
+        if position >= 3:
+            _start_flow_to_prev(state, flow_backend)
         state.push_pair(position, input_frame, processed_frame)
         if position == 1:
             yield 1, state.prev_output

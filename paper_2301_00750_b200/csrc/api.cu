@@ -98,8 +98,22 @@ struct ss_session {
     std::unique_ptr<fn::Run> run;
     cudaEvent_t fev[2] = {nullptr, nullptr};
     bool flow_timed = false;
+    // the flow to the previous frame runs on a side stream, concurrently with
+    // the next frame's pyramid and the flow to it on the session stream
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    bool side_pending = false;
+    int side_slots[2] = {-1, -1};  // ring slots whose pyramids the side flow reads
     std::unique_ptr<dis::Estimator> dis;  // built-in flow (BuiltinFlow)
 };
+
+// session-stream work that touches what the side-stream flow reads or writes
+// waits for it (idempotent; the flag is cleared once a step consumed it)
+static int join_side(const ss_session *s)
+{
+    if (s->side_pending) SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->join, 0));
+    return SS_OK;
+}
 
 struct ss_flownet {
     int device;
@@ -149,6 +163,12 @@ static void session_free(ss_session *s)
         if (e) cudaEventDestroy(e);
     for (auto &e : s->fev)
         if (e) cudaEventDestroy(e);
+    if (s->side) {
+        cudaStreamSynchronize(s->side);
+        cudaStreamDestroy(s->side);
+    }
+    if (s->fork) cudaEventDestroy(s->fork);
+    if (s->join) cudaEventDestroy(s->join);
     s->run.reset();
     s->dis.reset();
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
@@ -475,6 +495,9 @@ int ss_session_destroy(ss_session *s)
 
 int ss_session_reset(ss_session *s)
 {
+    if (int rc = join_side(s)) return rc;
+    s->side_pending = false;
+    s->flow_timed = false;
     s->n_pairs = 0;
     s->has_output = false;
     s->solved_through = 0;
@@ -511,6 +534,10 @@ int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, 
         s->order[2] = idx;
     }
     auto &sl = s->slot[idx];
+    // the pending side flow reads the pyramids of two other ring slots; the
+    // copy into this slot overlaps it unless it evicts one of them
+    if (idx == s->side_slots[0] || idx == s->side_slots[1])
+        if (int rc = join_side(s)) return rc;
     if (s->run) s->run->slots[idx].key = -1;  // the frame's cached pyramid is stale
     if (int rc = copy_frame(s, sl.I, I, s->ci, dtype, where)) return rc;
     if (int rc = copy_frame(s, sl.P, P, s->cp, dtype, where)) return rc;
@@ -548,6 +575,7 @@ int ss_set_flow(ss_session *s, int which, const float *uv, const uint8_t *valid,
         set_error("which must be 0 (to previous) or 1 (to next)");
         return SS_VALUE_ERROR;
     }
+    if (int rc = join_side(s)) return rc;
     const size_t px = (size_t)s->h * s->w;
     const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     SS_CUDA_TRY(cudaMemcpyAsync(s->uv[which], uv, px * 2 * sizeof(float), kind, s->stream));
@@ -568,6 +596,7 @@ int ss_set_constant_flow(ss_session *s, int which, double u, double v, int steps
     // ConstantFlow: uv = (u * steps, v * steps) in float64 then float32
     const float fu = (float)(u * steps), fv = (float)(v * steps);
     const long px = (long)s->h * s->w;
+    if (int rc = join_side(s)) return rc;
     k_fill_flow<<<blocks_for(px, 256), 256, 0, s->stream>>>(s->uv[which], s->valid[which], px, fu, fv);
     SS_LAUNCH_CHECK("k_fill_flow");
     s->flow_for[which] = s->solved_through + 1;
@@ -614,6 +643,8 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
         set_error("iterations must be >= 1");
         return SS_VALUE_ERROR;
     }
+    if (int rc = join_side(s)) return rc;
+    s->side_pending = false;
     SS_CUDA_TRY(cudaEventRecord(s->ev[0], s->stream));
     PresolveArgs a;
     a.h = s->h;
@@ -695,6 +726,7 @@ int ss_flows(const ss_session *s, int which, float *uv_dst, uint8_t *valid_dst, 
         set_error("which must be 0 (to previous) or 1 (to next)");
         return SS_VALUE_ERROR;
     }
+    if (int rc = join_side(s)) return rc;
     const size_t px = (size_t)s->h * s->w;
     const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (uv_dst) SS_CUDA_TRY(cudaMemcpyAsync(uv_dst, s->uv[which], px * 2 * sizeof(float), kind, s->stream));
@@ -762,15 +794,26 @@ int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b,
 int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
 {
     if (s->net == net && s->run) return SS_OK;
+    if (int rc = join_side(s)) return rc;
+    SS_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->side_pending = false;
     s->net = net;
+    // SS_FLOW_CONCURRENT=0 runs both flows of a step on the session stream
+    const char *cc = getenv("SS_FLOW_CONCURRENT");
+    const bool concurrent = cc == nullptr || strcmp(cc, "0");
     s->run.reset(new fn::Run());
-    if (int rc = s->run->init(&net->wts, s->h, s->w)) {
+    if (int rc = s->run->init(&net->wts, s->h, s->w, concurrent ? 2 : 1)) {
         s->run.reset();
         s->net = nullptr;
         return rc;
     }
     s->run->conv_mode = conv_mode_for(net->precision);
     s->run->use_graphs = getenv("SS_FLOW_GRAPHS") == nullptr || strcmp(getenv("SS_FLOW_GRAPHS"), "0");
+    if (concurrent && !s->side) {
+        SS_CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+        SS_CUDA_TRY(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming));
+        SS_CUDA_TRY(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming));
+    }
     return fn::prepare_conv_tc();
 }
 
@@ -788,6 +831,7 @@ int ss_session_compute_dis_flow(ss_session *s, int which, int levels, int patch,
                   " are not buffered");
         return SS_VALUE_ERROR;
     }
+    if (int rc = join_side(s)) return rc;
     const dis::Options o = dis_options(levels, patch, iters, downscale);
     if (!s->dis || !same_opts(s->dis->opts, o)) {
         s->dis.reset(new dis::Estimator());
@@ -810,6 +854,8 @@ int ss_session_time_conv(ss_session *s, int level, int reps, float *ms, double *
         set_error("no flow network attached to the session");
         return SS_VALUE_ERROR;
     }
+    if (int rc = join_side(s)) return rc;
+    s->run->select_set(0);
     return s->run->time_est1(level, reps < 1 ? 1 : reps, s->stream, ms, flops);
 }
 
@@ -832,12 +878,40 @@ int ss_session_compute_flow(ss_session *s, int which)
     }
     const int ia = (int)(a - s->slot), ib = (int)(b - s->slot);
     if (which == 0 || !s->flow_timed) {
+        if (which == 0 && s->side_pending) {  // a second flow to the previous frame
+            if (int rc = join_side(s)) return rc;
+            s->side_pending = false;
+        }
         SS_CUDA_TRY(cudaEventRecord(s->fev[0], s->stream));
+    }
+    // pyramids always run on the session stream (they share scratch buffers);
+    // recomputing one the pending side flow reads waits for it first
+    for (int k = 0; k < 2; ++k) {
+        const int sl = k == 0 ? ia : ib;
+        const int64_t pos = k == 0 ? t : other;
+        if (s->side_pending && (sl == s->side_slots[0] || sl == s->side_slots[1]) &&
+            s->run->slots[sl].key != pos)
+            if (int rc = join_side(s)) return rc;
     }
     if (int rc = s->run->pyramid(ia, t, a->I, s->ci, s->stream)) return rc;
     if (int rc = s->run->pyramid(ib, other, b->I, s->ci, s->stream)) return rc;
-    if (int rc = s->run->flow(ia, ib, s->uv[which], s->valid[which], s->stream)) return rc;
-    SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->stream));
+    if (which == 0 && s->side) {
+        // fork: the flow to t-1 (estimator buffer set 1) overlaps whatever the
+        // session stream does next -- typically the pyramid of t+1 and the flow
+        // to it (set 0); ss_step / any conflicting call joins it
+        SS_CUDA_TRY(cudaEventRecord(s->fork, s->stream));
+        SS_CUDA_TRY(cudaStreamWaitEvent(s->side, s->fork, 0));
+        if (int rc = s->run->flow(ia, ib, s->uv[0], s->valid[0], s->side, 1)) return rc;
+        SS_CUDA_TRY(cudaEventRecord(s->join, s->side));
+        SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->side));
+        s->side_pending = true;
+        s->side_slots[0] = ia;
+        s->side_slots[1] = ib;
+    } else {
+        if (int rc = s->run->flow(ia, ib, s->uv[which], s->valid[which], s->stream, 0)) return rc;
+        if (int rc = join_side(s)) return rc;  // fev[1] marks the end of both flows
+        SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->stream));
+    }
     s->flow_timed = true;
     s->flow_for[which] = t;
     return SS_OK;

@@ -186,8 +186,25 @@ Run::~Run()
     for (void *p : allocs) cudaFree(p);
 }
 
-int Run::init(const Weights *wt, int h_, int w_)
+void Run::select_set(int set)
 {
+    const EstBufs &s = sets[set < nsets ? set : 0];
+    for (int l = 0; l < 7; ++l) {
+        x[l] = s.x[l];
+        e1[l] = s.e1[l];
+        e2[l] = s.e2[l];
+        E[l] = s.E[l];
+        w2[l] = s.w2[l];
+    }
+    ra = s.ra;
+    rb = s.rb;
+    rr = s.rr;
+    ws = s.ws;
+}
+
+int Run::init(const Weights *wt, int h_, int w_, int nsets_)
+{
+    nsets = nsets_ < 1 ? 1 : (nsets_ > 2 ? 2 : nsets_);
     wts = wt;
     h = h_;
     w = w_;
@@ -211,20 +228,25 @@ int Run::init(const Weights *wt, int h_, int w_)
     for (auto &sl : slots)
         for (int l = 3; l <= 6; ++l)
             if ((rc = alloc(&sl.lvl[l], (size_t)H[l] * W[l] * PYR_CH[l - 1]))) return rc;
-    for (int l = 3; l <= 6; ++l) {
-        const size_t px = (size_t)H[l] * W[l];
-        if ((rc = alloc(&x[l], px * est_in(l)))) return rc;
-        if ((rc = alloc(&e1[l], px * 128))) return rc;
-        if ((rc = alloc(&e2[l], px * 128))) return rc;
-        if ((rc = alloc(&E[l], px * E_LD))) return rc;
-        if ((rc = alloc(&w2[l], px * PYR_CH[l - 1]))) return rc;
+    ws_floats = 6u << 20;  // 24 MB of split-K partials per set
+    for (int s = 0; s < nsets; ++s) {
+        EstBufs &b = sets[s];
+        for (int l = 0; l < 7; ++l) b.x[l] = b.e1[l] = b.e2[l] = b.E[l] = b.w2[l] = nullptr;
+        for (int l = 3; l <= 6; ++l) {
+            const size_t px = (size_t)H[l] * W[l];
+            if ((rc = alloc(&b.x[l], px * est_in(l)))) return rc;
+            if ((rc = alloc(&b.e1[l], px * 128))) return rc;
+            if ((rc = alloc(&b.e2[l], px * 128))) return rc;
+            if ((rc = alloc(&b.E[l], px * E_LD))) return rc;
+            if ((rc = alloc(&b.w2[l], px * PYR_CH[l - 1]))) return rc;
+        }
+        const size_t px3 = (size_t)H[3] * W[3];
+        if ((rc = alloc(&b.ra, px3 * 128))) return rc;
+        if ((rc = alloc(&b.rb, px3 * 128))) return rc;
+        if ((rc = alloc(&b.rr, px3 * 4))) return rc;
+        if ((rc = alloc(&b.ws, ws_floats))) return rc;
     }
-    const size_t px3 = (size_t)H[3] * W[3];
-    if ((rc = alloc(&ra, px3 * 128))) return rc;
-    if ((rc = alloc(&rb, px3 * 128))) return rc;
-    if ((rc = alloc(&rr, px3 * 4))) return rc;
-    ws_floats = 6u << 20;  // 24 MB of split-K partials
-    if ((rc = alloc(&ws, ws_floats))) return rc;
+    select_set(0);
     return SS_OK;
 }
 
@@ -344,10 +366,12 @@ int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st
     return SS_OK;
 }
 
-int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
+int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st, int set)
 {
+    set = set < nsets ? set : 0;
+    select_set(set);
     if (use_graphs && !prof.on) {
-        const auto k = std::make_tuple(a, b, (void *)uv, (void *)valid);
+        const auto k = std::make_tuple(a, b, (void *)uv, (void *)valid, set);
         auto &g = flow_graphs[k];
         int rc;
         if (!g && (rc = capture(st, &g, [&] { return flow_impl(a, b, uv, valid, st); }))) {
@@ -394,7 +418,7 @@ int Run::pyramid_impl(int slot, const float *img, int c, cudaStream_t st)
 {
     Slot &sl = slots[slot];
     conv_mode_ = conv_mode;
-    ws_ = ws;
+    ws_ = sets[0].ws;  // pyramids run on the session stream, as does the set-0 flow
     ws_floats_ = ws_floats;
     int rc;
     prof.mark("start", st);

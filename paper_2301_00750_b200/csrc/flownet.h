@@ -75,23 +75,33 @@ struct Run {
         int64_t key = -1;
         float *lvl[7] = {nullptr};
     } slots[3];
+    // estimator / refinement buffers of the flow being computed (one set per
+    // concurrently running flow; select_set points these at a set)
     float *x[7] = {nullptr}, *e1[7] = {nullptr}, *e2[7] = {nullptr}, *E[7] = {nullptr},
           *w2[7] = {nullptr};
     float *ra = nullptr, *rb = nullptr, *rr = nullptr;
     float *ws = nullptr;  // split-K partial sums
     size_t ws_floats = 0;
+    struct EstBufs {
+        float *x[7], *e1[7], *e2[7], *E[7], *w2[7];
+        float *ra, *rb, *rr, *ws;
+    } sets[2];
+    int nsets = 1;
     std::vector<void *> allocs;
     // CUDA graphs (sessions: every buffer is fixed per ring slot, so the
     // ~60 launches of a pyramid / flow replay as one graph launch)
     bool use_graphs = false;
     std::map<std::tuple<int, const void *, int>, cudaGraphExec_t> pyr_graphs;
-    std::map<std::tuple<int, int, void *, void *>, cudaGraphExec_t> flow_graphs;
+    std::map<std::tuple<int, int, void *, void *, int>, cudaGraphExec_t> flow_graphs;
     ~Run();
-    int init(const Weights *w, int h, int w_);
+    int init(const Weights *w, int h, int w_, int nsets = 1);
     // pyramid of img (h, w, c) into slot (skipped if key matches)
     int pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st);
-    // flow from the frame in slot a toward the frame in slot b (both computed)
-    int flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st);
+    // flow from the frame in slot a toward the frame in slot b (both computed),
+    // using estimator buffer set `set` (two flows may run concurrently on two
+    // streams with different sets)
+    int flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st, int set = 0);
+    void select_set(int set);
     // average device time (CUDA events) of `reps` launches of the first
     // estimator conv at `level` on this run's buffers (roofline measurement)
     int time_est1(int level, int reps, cudaStream_t st, float *ms, double *flops);

@@ -113,3 +113,17 @@ def test_session_flows_match_stateless(ss, net):
         _lib.lib().ss_flows(state.handle, which, uv.ctypes.data, None, _lib.SS_HOST)
         ref = net.flow_between(2, seq.inputs[1], other, seq.inputs[other - 1])
         assert np.array_equal(uv, ref.uv)
+
+
+def test_concurrent_flows_bitwise_equal_serial(ss, net, monkeypatch):
+    """The flow to t-1 on the side stream (started before the next push) gives
+    the same stream, bit for bit, as both flows serialised on one stream."""
+    from paper_2301_00750_b200 import synthetic
+
+    seq = synthetic.translating_sequence(frames=7, height=72, width=120, seed=9)
+    conc = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"), net))
+    monkeypatch.setenv("SS_FLOW_CONCURRENT", "0")
+    serial = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"), net))
+    assert sorted(conc) == sorted(serial) == list(range(1, 8))
+    for t in conc:
+        assert np.array_equal(conc[t], serial[t]), t
