@@ -11,7 +11,8 @@ import os
 import subprocess
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libstreamstab_b200.so")
+# SS_LIB_PATH: an alternative build of the same library (diagnostics)
+LIB_PATH = os.environ.get("SS_LIB_PATH") or os.path.join(_PKG, "lib", "libstreamstab_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 
 SS_OK = 0

@@ -814,6 +814,7 @@ int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
         SS_CUDA_TRY(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming));
         SS_CUDA_TRY(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming));
     }
+    if (int rc = fn::prepare_conv_tma()) return rc;
     return fn::prepare_conv_tc();
 }
 

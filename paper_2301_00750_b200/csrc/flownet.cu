@@ -64,6 +64,7 @@ Weights::~Weights()
 {
     cudaFree(block);
     cudaFree(tc_block);
+    cudaFree(tma_block);
 }
 
 int Weights::expected_params()
@@ -174,6 +175,57 @@ int Weights::upload(const float *host, int64_t n)
         layers[i].tc_bf16 = static_cast<uint8_t *>(tc_block) + obf[i];
         layers[i].tc_tf32 = static_cast<uint8_t *>(tc_block) + otf[i];
     }
+
+    // TMA path (flownet_tma.cu): per layer [kblocks][parts][2 np][32] fp32 --
+    // kblock = cb * k*k + tap (channel block outer, filter tap inner), per
+    // output-channel part np tf32-hi rows then np lo rows, 32 input channels
+    // cb * 32 + c' per row (zero past cin)
+    std::vector<size_t> otm(layers.size(), 0);
+    size_t tm_total = 0;
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        otm[i] = tm_total;
+        tm_total += (size_t)l.k * l.k * ((l.cin + 31) / 32) * 2 * l.cout_pad * 32;
+    }
+    std::vector<float> tmh(tm_total, 0.0f);
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        const int taps = l.k * l.k, N = l.cout_pad;
+        const int parts = (N + 127) / 128, np = N / parts;
+        const float *wl = dev.data() + woff[i];  // [K][cout_pad]
+        float *dst = tmh.data() + otm[i];
+        for (int tap = 0; tap < taps; ++tap)
+            for (int c = 0; c < l.cin; ++c) {
+                const size_t kb = (size_t)(c / 32) * taps + tap;
+                for (int n = 0; n < l.cout; ++n) {
+                    const float f = wl[(size_t)(tap * l.cin + c) * N + n];
+                    uint32_t u;
+                    std::memcpy(&u, &f, 4);
+                    const uint32_t hu = u & 0xffffe000u;
+                    float hi;
+                    std::memcpy(&hi, &hu, 4);
+                    const int part = n / np, nn = n - part * np;
+                    const size_t row = (size_t)part * 2 * np + nn;
+                    dst[(kb * 2 * N + row) * 32 + c % 32] = hi;
+                    dst[(kb * 2 * N + row + np) * 32 + c % 32] = f - hi;
+                }
+            }
+    }
+    cudaFree(tma_block);
+    tma_block = nullptr;
+    SS_CUDA_TRY(cudaMalloc(&tma_block, tm_total * sizeof(float)));
+    SS_CUDA_TRY(cudaMemcpy(tma_block, tmh.data(), tm_total * sizeof(float), cudaMemcpyHostToDevice));
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        const int parts = (l.cout_pad + 127) / 128, np = l.cout_pad / parts;
+        l.wt_tma = tma_block + otm[i];
+        l.tma_T = tma_taps_per_stage(l.k, l.stride, np);
+        const int kblocks = l.k * l.k * ((l.cin + 31) / 32);
+        if (int rc = encode_weight_map(&l.tmB, l.wt_tma, kblocks, 2 * l.cout_pad, np, l.tma_T)) return rc;
+    }
     return SS_OK;
 }
 
@@ -253,6 +305,9 @@ int Run::init(const Weights *wt, int h_, int w_, int nsets_)
 static thread_local int conv_mode_ = CONV_TC_TF32X3;  // set by the Run issuing the convs
 static thread_local float *ws_ = nullptr;
 static thread_local size_t ws_floats_ = 0;
+// SS_CONV_TMA=0: the fp32 path uses the register-gather tcgen05 kernel
+// (flownet_tc.cu) instead of the TMA-fed one (A/B comparison)
+static const bool use_tma_ = getenv("SS_CONV_TMA") == nullptr || strcmp(getenv("SS_CONV_TMA"), "0");
 
 // SS_FLOW_PROFILE=1: per-launch device times of the network (CUDA events),
 // printed to stderr after every pyramid / flow call (diagnostics only)
@@ -323,7 +378,10 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
     p.Ho = (Hi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.Wo = (Wi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.act = L.act;
+    p.tmB = &L.tmB;
+    p.tma_T = L.tma_T;
     if (conv_mode_ == CONV_FFMA) return launch_conv_ffma(p, st);
+    if (conv_mode_ == CONV_TC_TF32X3 && use_tma_) return launch_conv_tma(p, st);
     return launch_conv_tc(p, conv_mode_ == CONV_TC_BF16 ? 0 : 1, st);
 }
 

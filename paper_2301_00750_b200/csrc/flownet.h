@@ -2,6 +2,7 @@
 // paper_2301_00750_b200/liteflownet.py for the architecture table).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,6 +28,8 @@ struct ConvParams {
     size_t ws_floats = 0;
     int k_per_split = 0;        // set by the launcher
     int n_full = 0, n_off = 0;  // N-split (set by the launcher): weight rows [n_off, n_off + Cout_pad)
+    const void *tmB = nullptr;  // TMA weight map (CUtensorMap, flownet_tma.cu), fp32 path
+    int tma_T = 1;              // taps per weight stage of that map
 };
 
 enum ConvMode { CONV_FFMA = 0, CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
@@ -35,6 +38,13 @@ int launch_conv_ffma(const ConvParams &p, cudaStream_t st);
 // kind 0: bf16 operands (kind::f16); kind 1: 3xTF32 (kind::tf32)
 int launch_conv_tc(const ConvParams &p, int kind, cudaStream_t st);
 int prepare_conv_tc();  // one-time kernel attributes (call outside stream capture)
+// TMA-fed warp-specialised 3xTF32 conv (flownet_tma.cu)
+int launch_conv_tma(const ConvParams &p, cudaStream_t st);
+int prepare_conv_tma();
+int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, int np, int T);
+int tma_taps_per_stage(int k, int stride, int np);
+int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,
+                         int act, float *out, int out_ld, cudaStream_t st);
 int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,
                      float *out, int ld_out, cudaStream_t st);
 int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st);
@@ -50,6 +60,11 @@ struct LayerDev {
     bool dw;
     float *w = nullptr, *b = nullptr;
     const void *tc_bf16 = nullptr, *tc_tf32 = nullptr;  // tensor-core stage layouts
+    // TMA path (flownet_tma.cu): [kblock = cb * k*k + tap][part][hi np rows;
+    // lo np rows][32 channels] fp32, its tensor map, taps per stage
+    const float *wt_tma = nullptr;
+    int tma_T = 1;
+    alignas(64) CUtensorMap tmB;
 };
 
 // Weights on one device, in liteflownet.layer_table() order.
@@ -57,6 +72,7 @@ struct Weights {
     std::vector<LayerDev> layers;
     float *block = nullptr;
     void *tc_block = nullptr;
+    float *tma_block = nullptr;
     ~Weights();
     static int expected_params();
     int upload(const float *host, int64_t n);

@@ -313,6 +313,15 @@ __global__ void k_splitk_reduce(const float *__restrict__ ws, int splits, int M,
     }
 }
 
+int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,
+                         int act, float *out, int out_ld, cudaStream_t st)
+{
+    const long n = (long)M * ((Cout + 3) / 4);
+    k_splitk_reduce<<<blocks_for(n, 256), 256, 0, st>>>(ws, splits, M, N, Cout, bias, act, out, out_ld);
+    SS_LAUNCH_CHECK("k_splitk_reduce");
+    return SS_OK;
+}
+
 static int n_sm_ = 0;
 
 // one-time kernel attributes (outside any stream capture): the largest layer

@@ -1,0 +1,544 @@
+// TMA-fed, warp-specialised implicit-GEMM convolution on tcgen05 (sm_100a):
+// fp32 activations, "3xTF32" products (fp32-class accuracy).
+//
+//   D[m, n] = sum_k A[m, k] * W[k, n]   m = output pixel (128 per tile),
+//   n = output channel, k = (32-channel block, filter tap, channel)
+//
+// 3xTF32: a = a_hi + a_lo, w = w_hi + w_lo (hi = tf32 truncation, lo exact);
+// D = a_hi w_hi + a_hi w_lo + a_lo w_hi.  The weights of one output-channel
+// part sit in shared memory as [w_hi rows; w_lo rows] (2 np rows), so ONE
+// MMA with N = 2 np computes a_hi w_hi and a_hi w_lo into two TMEM column
+// ranges and a second (N = np) adds a_lo w_hi to the first: two tcgen05.mma
+// per K = 8 step; the epilogue sums the two ranges.
+//
+// A operand (the activations), two modes:
+//   halo (stride-1 convs): a tile is 16 output rows x 8 columns; per 32-channel
+//     block ONE tiled TMA load brings the (16 + 2p) x (8 + 2p) input halo
+//     (OOB zero fill = the padding), converted to (hi, lo) once; each filter
+//     tap is a shifted, strided view of it -- start row (ky * halo_w + kx) *
+//     dil, 8-row groups halo_w rows apart -- described directly by the UMMA
+//     descriptor (the SWIZZLE_128B pattern follows the absolute shared
+//     address: tools/umma_shift_probe.cu);
+//   im2col (strided convs): per (tap, channel block) ONE TMA im2col load of the
+//     128-pixel column (the hardware walks the window, the stride and the
+//     border).
+// B operand: one 3-D TMA load per stage brings T taps x [hi; lo] weight rows
+// (T taps per stage for narrow layers, so a stage carries enough MMA work).
+//
+// Warp roles (persistent CTAs, one per SM, walking (tile, K-split) units):
+//   warp 0      TMA producer          warps 6-9  converters (A -> hi, lo)
+//   warp 1      MMA issuer            warps 2-5  epilogue (TMEM -> bias, act,
+//                                                 fp32 NHWC or split-K partials)
+// TMEM holds two accumulators, so the epilogue of a unit overlaps the MMAs of
+// the next.  Producer and MMA warps run converged; one elected lane issues.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "flownet.h"
+#include "ss_common.cuh"
+#include "tc_common.cuh"
+
+// 1: the raw fp32 tile feeds the a_hi MMAs directly (the tensor core reads
+// only the tf32 bits of an fp32 operand -- same products as the truncated hi)
+#ifndef SS_TF32_HW_TRUNCATES
+#define SS_TF32_HW_TRUNCATES 0
+#endif
+
+namespace ss {
+namespace fn {
+
+using namespace tc;
+
+namespace {
+
+constexpr int TM_THREADS = 320;
+constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA
+constexpr int HT_H = 16, HT_W = 8;  // halo-mode output tile (rows x columns)
+
+struct ConvArgs {
+    int halo;          // 1 halo mode, 0 im2col mode
+    int H, W, M;       // output size, M = H * W
+    int stride, k, dil, pad, taps, cin, ncb;
+    int T, sp_cb;      // taps per stage, stages per channel block
+    int tiles_x, n_tiles, nk_all, k_per_split, units;
+    int a_box, a_slot, na, halo_w;
+    int np, part_row, Cout, act, out_ld, stages, b_stage;
+    const float *bias;
+    float *out;
+    float *ws;  // split-K partials [split][M][np] (null: final output)
+};
+
+__device__ __forceinline__ float lk(float v) { return v >= 0.f ? v : 0.1f * v; }
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// one K = 8 step of 3xTF32 (see the file comment), elected lane of a converged warp
+__device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, uint64_t b,
+                                         uint32_t id2, uint32_t id1, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %6, 1;\n\t}" ::"r"(d),
+        "l"(ah), "l"(al), "l"(b), "r"(acc), "r"(id2), "r"(id1)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(TM_THREADS, 1)
+    k_conv_tc3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const ConvArgs a)
+{
+    extern __shared__ __align__(1024) uint8_t cv_smem[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(cv_smem) + 1023) & ~uintptr_t(1023));
+    const int S = a.stages, NA = a.na, np = a.np;
+    uint8_t *aslots = base;                          // [NA][raw | lo]
+    uint8_t *bst = base + 2 * NA * a.a_slot;         // [S][T][2 np rows x 128 B]
+    uint64_t *a_full = reinterpret_cast<uint64_t *>(bst + S * a.b_stage);
+    uint64_t *a_conv = a_full + NA, *a_empty = a_conv + NA;
+    uint64_t *b_full = a_empty + NA, *b_empty = b_full + S;
+    uint64_t *acc_full = b_empty + S, *acc_empty = acc_full + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t acc_cols = (uint32_t)(2 * np + 31) / 32 * 32;
+    uint32_t tcols = 32;
+    while (tcols < 2 * acc_cols) tcols <<= 1;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NA; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_conv[i], 4);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_rt(tmem_slot, tcols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        }
+        uint32_t ga = 0, gb = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+            const int tile = u % a.n_tiles, split = u / a.n_tiles;
+            int x0, y0;
+            if (a.halo) {
+                const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+                x0 = tx * HT_W - a.pad;
+                y0 = ty * HT_H - a.pad;
+            } else {
+                const int m0 = tile * 128, oy = m0 / a.W, ox = m0 - oy * a.W;
+                x0 = ox * a.stride - a.pad;
+                y0 = oy * a.stride - a.pad;
+            }
+            const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
+            int cb = kb / a.sp_cb, grp = kb - cb * a.sp_cb;
+            for (int st = kb; st < ke; ++st, ++gb) {
+                const int tap0 = grp * a.T;
+                if (!a.halo || st == kb || grp == 0) {
+                    const int sa = (int)(ga % (uint32_t)NA);
+                    mbar_wait(&a_empty[sa], ((ga / NA) & 1) ^ 1);
+                    if (elect_one()) {
+                        const uint32_t dst = smem_u32(aslots + sa * 2 * a.a_slot);
+                        mbar_expect_tx(&a_full[sa], (uint32_t)a.a_box);
+                        if (a.halo) {
+                            tma_tile_3d(dst, &tmA, cb * 32, x0, y0, &a_full[sa]);
+                        } else {
+                            const int ky = tap0 / a.k, kx = tap0 - ky * a.k;
+                            tma_im2col_4d(dst, &tmA, cb * 32, x0, y0, 0, (uint16_t)(kx * a.dil),
+                                          (uint16_t)(ky * a.dil), &a_full[sa]);
+                        }
+                    }
+                    __syncwarp();
+                    ++ga;
+                }
+                const int s = (int)(gb % (uint32_t)S);
+                mbar_wait(&b_empty[s], ((gb / S) & 1) ^ 1);
+                if (elect_one()) {
+                    mbar_expect_tx(&b_full[s], (uint32_t)a.b_stage);
+                    tma_tile_3d(smem_u32(bst + s * a.b_stage), &tmB, 0, a.part_row, cb * a.taps + tap0, &b_full[s]);
+                }
+                __syncwarp();
+                if (++grp == a.sp_cb) {
+                    grp = 0;
+                    ++cb;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t id2 = idesc(2u, 128u, (uint32_t)(2 * np)), id1 = idesc(2u, 128u, (uint32_t)np);
+        const uint32_t sbo = a.halo ? (uint32_t)a.halo_w * 128u : 1024u;
+        const uint32_t bstride = (uint32_t)(2 * np * 128);
+        uint32_t ga = 0, gb = 0, uc = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
+            const int split = u / a.n_tiles;
+            const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
+            const uint32_t acc = uc & 1;
+            mbar_wait(&acc_empty[acc], ((uc >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + acc * acc_cols;
+            int cb = kb / a.sp_cb, grp = kb - cb * a.sp_cb, sa = 0;
+            for (int st = kb; st < ke; ++st, ++gb) {
+                const bool a_event = !a.halo || st == kb || grp == 0;
+                if (a_event) {
+                    sa = (int)(ga % (uint32_t)NA);
+                    mbar_wait(&a_conv[sa], (ga / NA) & 1);
+                    ++ga;
+                }
+                const int s = (int)(gb % (uint32_t)S);
+                mbar_wait(&b_full[s], (gb / S) & 1);
+                tc_fence_after();
+                const int tap0 = grp * a.T, nt = min(a.T, a.taps - tap0);
+                const int nks = min(4, (a.cin - cb * 32 + 7) >> 3);
+                const uint32_t araw = smem_u32(aslots + sa * 2 * a.a_slot);
+                const uint32_t b0 = smem_u32(bst + s * a.b_stage);
+                int ky = tap0 / a.k, kx = tap0 - ky * a.k;
+                for (int j = 0; j < nt; ++j) {
+                    const uint32_t off = a.halo ? (uint32_t)((ky * a.halo_w + kx) * a.dil) * 128u : 0u;
+                    const uint64_t ah = sdesc_sw128_sbo(araw + off, sbo);
+                    const uint64_t al = sdesc_sw128_sbo(araw + a.a_slot + off, sbo);
+                    const uint64_t bd = sdesc_sw128(b0 + j * bstride);
+                    for (int i = 0; i < nks; ++i)  // +32 bytes of K = +2 in the address field
+                        mma_step(d, ah + 2 * i, al + 2 * i, bd + 2 * i, id2, id1,
+                                 (st > kb || j > 0 || i > 0) ? 1u : 0u);
+                    if (++kx == a.k) {
+                        kx = 0;
+                        ++ky;
+                    }
+                }
+                mma_commit_elect(&b_empty[s]);
+                const bool a_last = !a.halo || grp == a.sp_cb - 1 || st == ke - 1;
+                if (a_last) mma_commit_elect(&a_empty[sa]);
+                __syncwarp();
+                if (++grp == a.sp_cb) {
+                    grp = 0;
+                    ++cb;
+                }
+            }
+            mma_commit_elect(&acc_full[acc]);
+            __syncwarp();
+        }
+    } else if (warp < 6) {
+        // ---------------- epilogue ----------------
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        uint32_t uc = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
+            const uint32_t acc = uc & 1;
+            mbar_wait(&acc_full[acc], (uc >> 1) & 1);
+            tc_fence_after();
+            const int tile = u % a.n_tiles, split = u / a.n_tiles;
+            const int m = q * 32 + lane;
+            bool ok;
+            size_t pix;
+            if (a.halo) {
+                const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+                const int oy = ty * HT_H + (m >> 3), ox = tx * HT_W + (m & 7);
+                ok = oy < a.H && ox < a.W;
+                pix = (size_t)oy * a.W + ox;
+            } else {
+                pix = (size_t)tile * 128 + m;
+                ok = pix < (size_t)a.M;
+            }
+            const uint32_t t0 = tmem + acc * acc_cols + ((uint32_t)(q * 32) << 16);
+            for (int c0 = 0; c0 < np; c0 += 16) {
+                float v[16], w[16];
+                tmem_ld16(t0 + c0, v);
+                tmem_ld16(t0 + np + c0, w);
+                if (!ok) continue;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += w[i];
+                if (a.ws) {
+                    float *dst = a.ws + ((size_t)split * a.M + pix) * np + c0;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                } else if (c0 < a.Cout) {
+                    float *dst = a.out + pix * a.out_ld + c0;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float x = v[i] + (c0 + i < a.Cout ? __ldg(a.bias + c0 + i) : 0.f);
+                        v[i] = a.act ? lk(x) : x;
+                    }
+                    if (c0 + 16 <= a.Cout) {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (i < a.Cout - c0) dst[i] = v[i];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+        }
+    } else {
+        // ---------------- converters: A -> (hi in place, lo beside) ----------------
+        const int t = threadIdx.x - 192;
+        const int n16 = a.a_box / 16;
+        uint32_t ga = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+            const int split = u / a.n_tiles;
+            const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
+            int grp = kb % a.sp_cb;
+            for (int st = kb; st < ke; ++st) {
+                const bool a_event = !a.halo || st == kb || grp == 0;
+                if (++grp == a.sp_cb) grp = 0;
+                if (!a_event) continue;
+                const int sa = (int)(ga % (uint32_t)NA);
+                mbar_wait(&a_full[sa], (ga / NA) & 1);
+                ++ga;
+                float4 *ar = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot);
+                float4 *lo = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot + a.a_slot);
+                for (int j = t; j < n16; j += 128) {
+                    const float4 v = ar[j];
+                    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+#if !SS_TF32_HW_TRUNCATES
+                    ar[j] = h;
+#endif
+                    lo[j] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_conv[sa]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_rt(tmem, tcols);
+    }
+}
+
+template <class PFN>
+PFN driver_fn(const char *name)
+{
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+        return reinterpret_cast<PFN>(p);
+    return nullptr;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tiled_fn()
+{
+    static auto fn = driver_fn<PFN_cuTensorMapEncodeTiled_v12000>("cuTensorMapEncodeTiled");
+    return fn;
+}
+
+PFN_cuTensorMapEncodeIm2col_v12000 im2col_fn()
+{
+    static auto fn = driver_fn<PFN_cuTensorMapEncodeIm2col_v12000>("cuTensorMapEncodeIm2col");
+    return fn;
+}
+
+int n_sm_tma = 0;
+
+int encode_act_map(CUtensorMap *m, const ConvParams &p, bool halo, int halo_w, int halo_h)
+{
+    CUresult r;
+    if (halo) {
+        auto fn = tiled_fn();
+        if (!fn) {
+            set_error("cuTensorMapEncodeTiled unavailable");
+            return SS_CUDA_ERROR;
+        }
+        const cuuint64_t dims[3] = {(cuuint64_t)p.Cin, (cuuint64_t)p.W, (cuuint64_t)p.H};
+        const cuuint64_t strides[2] = {(cuuint64_t)p.in_ld * 4, (cuuint64_t)p.in_ld * 4 * p.W};
+        const cuuint32_t box[3] = {32, (cuuint32_t)halo_w, (cuuint32_t)halo_h};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(p.in), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        auto fn = im2col_fn();
+        if (!fn) {
+            set_error("cuTensorMapEncodeIm2col unavailable");
+            return SS_CUDA_ERROR;
+        }
+        const cuuint64_t dims[4] = {(cuuint64_t)p.Cin, (cuuint64_t)p.W, (cuuint64_t)p.H, 1};
+        const cuuint64_t strides[3] = {(cuuint64_t)p.in_ld * 4, (cuuint64_t)p.in_ld * 4 * p.W,
+                                       (cuuint64_t)p.in_ld * 4 * p.W * p.H};
+        const int up = p.pad - p.dil * (p.k - 1);
+        const int lower[2] = {-p.pad, -p.pad};  // (W, H)
+        const int upper[2] = {up, up};
+        const cuuint32_t estr[4] = {1, (cuuint32_t)p.stride, (cuuint32_t)p.stride, 1};
+        r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(p.in), dims, strides, lower, upper, 32,
+               128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) {
+        set_error(std::string("activation tensor map encode failed: ") + std::to_string((int)r));
+        return SS_CUDA_ERROR;
+    }
+    return SS_OK;
+}
+
+}  // namespace
+
+int tma_taps_per_stage(int k, int stride, int np)
+{
+    if (stride != 1) return 1;
+    return std::max(1, std::min(k * k, 36864 / (2 * np * 128)));
+}
+
+// weight tensor map over [kblocks][rows = parts * 2 np][32] fp32: per stage
+// one box of 32 K x 2 np rows ([hi; lo] of one part) x T kblocks (taps)
+int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, int np, int T)
+{
+    auto fn = tiled_fn();
+    if (!fn) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return SS_CUDA_ERROR;
+    }
+    const cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)kblocks};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)rows * 128};
+    const cuuint32_t box[3] = {32, (cuuint32_t)(2 * np), (cuuint32_t)T};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(wt), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (weights) failed: " + std::to_string((int)r));
+        return SS_CUDA_ERROR;
+    }
+    return SS_OK;
+}
+
+int prepare_conv_tma()
+{
+    static bool done = false;
+    if (done) return SS_OK;
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+    int dev = 0;
+    SS_CUDA_TRY(cudaGetDevice(&dev));
+    SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm_tma, cudaDevAttrMultiProcessorCount, dev));
+    done = true;
+    return SS_OK;
+}
+
+// one output-channel part (rows [part * 2 np, +2 np) of the weight tensor)
+static int launch_part(const ConvParams &p, const CUtensorMap &tmA, bool halo, int halo_w, int halo_h,
+                       int part, int np, cudaStream_t st)
+{
+    ConvArgs a;
+    a.halo = halo ? 1 : 0;
+    a.H = p.Ho;
+    a.W = p.Wo;
+    a.M = p.Ho * p.Wo;
+    a.stride = p.stride;
+    a.k = p.k;
+    a.dil = p.dil;
+    a.pad = p.pad;
+    a.taps = p.k * p.k;
+    a.cin = p.Cin;
+    a.ncb = (p.Cin + 31) / 32;
+    a.T = p.tma_T;
+    a.sp_cb = (a.taps + a.T - 1) / a.T;
+    if (halo) {
+        a.tiles_x = (p.Wo + HT_W - 1) / HT_W;
+        a.n_tiles = a.tiles_x * ((p.Ho + HT_H - 1) / HT_H);
+        a.halo_w = halo_w;
+        a.a_box = halo_w * halo_h * 128;
+        a.na = 2;
+    } else {
+        a.tiles_x = 0;
+        a.n_tiles = (a.M + 127) / 128;
+        a.halo_w = 8;
+        a.a_box = 128 * 128;
+        a.na = 4;
+    }
+    a.a_slot = (a.a_box + 1023) / 1024 * 1024;
+    a.nk_all = a.ncb * a.sp_cb;
+    a.np = np;
+    a.part_row = part * 2 * np;
+    a.Cout = std::min(np, p.Cout - part * np);
+    a.act = p.act;
+    a.out_ld = p.out_ld;
+    a.bias = p.bias + part * np;
+    a.out = p.out + part * np;
+    a.b_stage = a.T * 2 * np * 128;
+    const int fixed = 2 * a.na * a.a_slot + 1024 + 512;
+    a.stages = std::min(8, (SMEM_MAX - fixed) / a.b_stage);
+    if (a.stages < 2 && !halo) {
+        a.na = 2;
+        a.stages = std::min(8, (SMEM_MAX - (2 * a.na * a.a_slot + 1536)) / a.b_stage);
+    }
+    if (a.stages < 2) {
+        set_error("conv stage does not fit in shared memory");
+        return SS_VALUE_ERROR;
+    }
+    // split K when the tiles alone leave SMs idle (>= 2 stages per split)
+    int splits = 1;
+    if (p.ws && a.n_tiles < n_sm_tma && a.nk_all >= 4) {
+        splits = std::min((n_sm_tma + a.n_tiles - 1) / a.n_tiles, a.nk_all / 2);
+        const size_t need = (size_t)splits * a.M * np;
+        if (need > p.ws_floats) splits = (int)(p.ws_floats / ((size_t)a.M * np));
+        splits = std::max(splits, 1);
+    }
+    a.k_per_split = (a.nk_all + splits - 1) / splits;
+    splits = (a.nk_all + a.k_per_split - 1) / a.k_per_split;
+    a.ws = splits > 1 ? p.ws : nullptr;
+    a.units = a.n_tiles * splits;
+    const int grid = std::min(a.units, n_sm_tma);
+    const size_t smem = (size_t)2 * a.na * a.a_slot + (size_t)a.stages * a.b_stage + 1024 + 512;
+    k_conv_tc3<<<grid, TM_THREADS, smem, st>>>(tmA, *static_cast<const CUtensorMap *>(p.tmB), a);
+    SS_LAUNCH_CHECK("k_conv_tc3");
+    if (splits > 1)
+        return launch_splitk_reduce(p.ws, splits, a.M, np, a.Cout, a.bias, p.act, a.out, p.out_ld, st);
+    return SS_OK;
+}
+
+int launch_conv_tma(const ConvParams &p, cudaStream_t st)
+{
+    if (int rc = prepare_conv_tma()) return rc;
+    if (!p.tmB) {
+        set_error("conv layer has no TMA weight map");
+        return SS_VALUE_ERROR;
+    }
+    static const bool halo_on = getenv("SS_CONV_HALO") == nullptr || strcmp(getenv("SS_CONV_HALO"), "0");
+    const bool halo = halo_on && p.stride == 1 && p.Ho == p.H && p.Wo == p.W;
+    if (!halo && p.tma_T != 1) {
+        set_error("im2col conv path needs one tap per stage");
+        return SS_VALUE_ERROR;
+    }
+    const int halo_w = HT_W + 2 * p.pad, halo_h = HT_H + 2 * p.pad;
+    alignas(64) CUtensorMap tmA;
+    if (int rc = encode_act_map(&tmA, p, halo, halo_w, halo_h)) return rc;
+    const int parts = (p.Cout_pad + 127) / 128;
+    const int np = p.Cout_pad / parts;
+    for (int part = 0; part < parts; ++part)
+        if (int rc = launch_part(p, tmA, halo, halo_w, halo_h, part, np, st)) return rc;
+    return SS_OK;
+}
+
+}  // namespace fn
+}  // namespace ss

@@ -97,6 +97,83 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
     return d;                 // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// arrive + expect `bytes` of TMA transactions on the current phase
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// TMA im2col load (4-D NHWC tensor map): the pixel column starting at input
+// coordinate (w, h, n) shifted by the filter-tap offset (ow, oh), channels
+// [c, c + channelsPerPixel)
+__device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const void *map, int c, int w, int h,
+                                              int n, uint16_t ow, uint16_t oh, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+        "h"(ow), "h"(oh)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_tile_2d(uint32_t dst, const void *map, int x, int y,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// shared-memory matrix descriptor, K-major, SWIZZLE_128B (the layout TMA
+// writes for 128-byte rows): 8-row atoms of 1024 B (SBO), LBO unused; a K
+// offset inside the 128-byte row is added to the start address
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr)
+{
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;  // version
+    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// as sdesc_sw128 with an explicit stride between 8-row groups: a view whose
+// rows are consecutive 128-byte rows of a larger swizzled tile, 8-row groups
+// `sbo` bytes apart, starting at any 128-byte row (the swizzle is a function
+// of the absolute shared address, so shifted / strided views of a tile TMA
+// wrote read back correctly with base offset 0 -- tools/umma_shift_probe.cu)
+__device__ __forceinline__ uint64_t sdesc_sw128_sbo(uint32_t saddr, uint32_t sbo)
+{
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+__device__ __forceinline__ void tma_tile_3d(uint32_t dst, const void *map, int x, int y, int z,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // instruction descriptor: D f32, A/B format (1 = BF16, 2 = TF32), both K-major
 __host__ __device__ constexpr uint32_t idesc(uint32_t ab_format, uint32_t M, uint32_t N)
 {
@@ -123,6 +200,42 @@ __device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t a, uint64_t b,
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
         "l"(a), "l"(b), "r"(id), "r"(acc)
         : "memory");
+}
+
+// Warp-converged issue: the whole warp runs the loop (so addresses and
+// descriptors stay in uniform registers) and elect.sync picks one lane to
+// issue -- avoids a per-instruction ELECT / R2UR.BROADCAST waterfall.
+__device__ __forceinline__ void mma_tf32_elect(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t id,
+                                               uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+        "l"(a), "l"(b), "r"(id), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t *bar)
+{
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ bool elect_one()
+{
+    uint32_t e = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(e));
+    return e != 0;
 }
 
 // arrive on *bar when every tcgen05 op issued so far by this thread completes
