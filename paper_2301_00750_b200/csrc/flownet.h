@@ -15,6 +15,36 @@
 namespace ss {
 namespace fn {
 
+// Programmatic dependent launch (PDL) for the network's kernel chain: every
+// kernel is launched with programmatic stream serialization, triggers its
+// dependents on entry and waits (griddepcontrol.wait) before its first
+// global-memory access, so a kernel's launch and prologue (barrier init, TMEM
+// allocation, tensor-map prefetch) overlap the tail of the previous one.
+// SS_FLOW_PDL=0 launches them plainly.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+bool pdl_enabled();
+int pdl_status(cudaError_t e, const char *what);
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(const char *name, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+               cudaStream_t st, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return pdl_status(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...), name);
+}
+
 struct ConvParams {
     const float *in;
     int in_ld, H, W, Cin;       // input NHWC slice (Cin % 4 == 0, 16-byte aligned)
@@ -41,6 +71,7 @@ int prepare_conv_tc();  // one-time kernel attributes (call outside stream captu
 // TMA-fed warp-specialised 3xTF32 conv (flownet_tma.cu)
 int launch_conv_tma(const ConvParams &p, cudaStream_t st);
 int prepare_conv_tma();
+int prepare_flow_kernels();
 int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, int np, int T);
 int tma_taps_per_stage(int k, int stride, int np);
 int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,

@@ -6,6 +6,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "flownet.h"
 #include "ss_common.cuh"
 
@@ -13,6 +16,14 @@ namespace ss {
 namespace fn {
 
 __device__ __forceinline__ float leaky(float v) { return v >= 0.f ? v : 0.1f * v; }
+
+bool pdl_enabled()
+{
+    static const bool on = getenv("SS_FLOW_PDL") == nullptr || strcmp(getenv("SS_FLOW_PDL"), "0");
+    return on;
+}
+
+int pdl_status(cudaError_t e, const char *what) { return e == cudaSuccess ? SS_OK : cuda_status(e, what); }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred)
 {
@@ -37,6 +48,7 @@ constexpr int BM = 128, BK = 16, AS = BK + 4;
 template <int BN>
 __global__ void __launch_bounds__(16 * (BN / 4)) k_conv_ffma(ConvParams p)
 {
+    pdl_wait();
     constexpr int NT = BN / 4;       // channel groups
     constexpr int THREADS = 16 * NT; // 16 pixel groups
     __shared__ __align__(16) float As[2][BM][AS];
@@ -173,6 +185,7 @@ __global__ void k_depthwise(const float *__restrict__ in, int ld, int H, int W, 
                             const float *__restrict__ w, int dil, float *__restrict__ out,
                             int ld_out)
 {
+    pdl_wait();
     const int C4 = C / 4;
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long)H * W * C4) return;
@@ -203,9 +216,8 @@ int launch_depthwise(const float *in, int ld, int H, int W, int C, const float *
                      float *out, int ld_out, cudaStream_t st)
 {
     const long n = (long)H * W * (C / 4);
-    k_depthwise<<<blocks_for(n, 256), 256, 0, st>>>(in, ld, H, W, C, w, dil, out, ld_out);
-    SS_LAUNCH_CHECK("k_depthwise");
-    return SS_OK;
+    return launch_pdl("k_depthwise", k_depthwise, dim3(blocks_for(n, 256)), dim3(256), 0, st, in, ld, H, W, C,
+                      w, dil, out, ld_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -214,6 +226,7 @@ int launch_depthwise(const float *in, int ld, int H, int W, int C, const float *
 __global__ void k_prep(const float *__restrict__ img, int h, int w, int c, int H, int W,
                        float *__restrict__ out)
 {
+    pdl_wait();
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long)H * W) return;
     const int y = (int)(i / W), x = (int)(i - (long)y * W);
@@ -232,9 +245,8 @@ __global__ void k_prep(const float *__restrict__ img, int h, int w, int c, int H
 
 int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st)
 {
-    k_prep<<<blocks_for((long)H * W, 256), 256, 0, st>>>(img, h, w, c, H, W, out);
-    SS_LAUNCH_CHECK("k_prep");
-    return SS_OK;
+    return launch_pdl("k_prep", k_prep, dim3(blocks_for((long)H * W, 256)), dim3(256), 0, st, img, h, w, c, H, W,
+                      out);
 }
 
 // ---------------------------------------------------------------------------
@@ -253,6 +265,7 @@ __global__ void k_up2_warp(const float *__restrict__ coarse, int cld, int Hc, in
                            const float *__restrict__ f2, int C, int H, int W,
                            float *__restrict__ x, int xld, float *__restrict__ w2)
 {
+    pdl_wait();
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long)H * W) return;
     const int y = (int)(i / W), xx = (int)(i - (long)y * W);
@@ -297,89 +310,147 @@ __global__ void k_up2_warp(const float *__restrict__ coarse, int cld, int Hc, in
 int launch_up2_warp(const float *coarse, int cld, int Hc, int Wc, const float *f2, int C, int H,
                     int W, float *x, int xld, float *w2, cudaStream_t st)
 {
-    k_up2_warp<<<blocks_for((long)H * W, 128), 128, 0, st>>>(coarse, cld, Hc, Wc, f2, C, H, W, x,
-                                                              xld, w2);
-    SS_LAUNCH_CHECK("k_up2_warp");
-    return SS_OK;
+    return launch_pdl("k_up2_warp", k_up2_warp, dim3(blocks_for((long)H * W, 128)), dim3(128), 0, st, coarse,
+                      cld, Hc, Wc, f2, C, H, W, x, xld, w2);
 }
 
 // ---------------------------------------------------------------------------
 // cost volume: x[:, d] = leaky(sum_c f1_c * w2_c(p + d) / C), d in [-4,4]^2;
-// also copies f1 into x[:, 96:96+C] (l < 6).  One CTA per (16 x 8 pixel tile,
-// dy): each thread owns one pixel and the 9 dx displacements of that dy row,
-// channels staged 16 at a time ([pixel][channel] smem, w2 rows y + dy with a
-// +-4 column halo).  Grid z = 9 keeps even the 17 x 30 coarsest level spread
-// over dozens of SMs.
-constexpr int CTW = 16, CTH = 8, CHK = 16, HALO = 4, CWW = CTW + 2 * HALO;
+// also copies f1 into x[:, 96:96+C] (l < 6).
+//
+// One CTA per (8 x 16 pixel tile, group of 3 dy rows): 64 threads, each owns
+// 2 horizontally adjacent pixels x 3 dy x 9 dx = 54 accumulators in
+// registers.  Channels stream through shared memory 16 at a time
+// (cp.async, double-buffered, zero fill outside the image): the f1 tile and
+// the w2 rows y + dy with a +-4 column halo.  Per float4 of channels a thread
+// reads its 2 f1 vectors and 3 x 10 w2 vectors and does 216 FMAs.  Rows of
+// the staged tiles are padded so the 8 threads of an LDS.128 phase (8
+// consecutive tile rows) hit distinct bank groups.
+constexpr int CR_TW = 16, CR_TH = 8, CR_CK = 16, CR_HALO = 4;
+constexpr int CR_PX = CR_CK + 4;                          // floats per staged pixel
+constexpr int CR_WW = CR_TW + 2 * CR_HALO;                // 24 w2 columns
+constexpr int CR_WR = CR_TH + 2;                          // w2 rows per dy group
+constexpr int CR_W2P = CR_WW * CR_PX + 4;                 // w2 row pitch (odd # of 16 B)
+constexpr int CR_F1P = CR_TW * CR_PX + 4;                 // f1 row pitch
+constexpr int CR_W2F = CR_WR * CR_W2P, CR_F1F = CR_TH * CR_F1P;
 
-__global__ void __launch_bounds__(CTW *CTH) k_corr(const float *__restrict__ f1,
-                                                   const float *__restrict__ w2, int C, int H,
-                                                   int W, float *__restrict__ x, int xld,
-                                                   int copy_f1)
+__global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const float *__restrict__ w2,
+                                             int C, int H, int W, float *__restrict__ x, int xld,
+                                             int copy_f1)
 {
-    __shared__ __align__(16) float s1[CTW * CTH][CHK + 4];
-    __shared__ __align__(16) float s2[CTH * CWW][CHK + 4];
-    const int tx = threadIdx.x % CTW, ty = threadIdx.x / CTW;
-    const int bx = blockIdx.x * CTW, by = blockIdx.y * CTH;
-    const int dy = (int)blockIdx.z - HALO;
-    const int y = by + ty, xx = bx + tx;
-    const bool inb = y < H && xx < W;
-    float acc[9];
-#pragma unroll
-    for (int d = 0; d < 9; ++d) acc[d] = 0.f;
-    for (int c0 = 0; c0 < C; c0 += CHK) {
-        // f1 tile: 128 px x 16 ch = 512 float4
-        for (int i = threadIdx.x; i < CTW * CTH * CHK / 4; i += CTW * CTH) {
-            const int px = i / (CHK / 4), q = (i - px * (CHK / 4)) * 4;
-            const int py = by + px / CTW, pxx = bx + px % CTW;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (py < H && pxx < W) v = *reinterpret_cast<const float4 *>(f1 + ((long)py * W + pxx) * C + c0 + q);
-            *reinterpret_cast<float4 *>(&s1[px][q]) = v;
+    pdl_wait();
+    extern __shared__ __align__(16) float cr_smem[];
+    float(*sw)[CR_W2F] = reinterpret_cast<float(*)[CR_W2F]>(cr_smem);
+    float(*sf)[CR_F1F] = reinterpret_cast<float(*)[CR_F1F]>(cr_smem + 2 * CR_W2F);
+    const int t = threadIdx.x;
+    const int ty = t & 7, cx = (t >> 3) * 2;  // tile row, first of 2 columns
+    const int bx = blockIdx.x * CR_TW, by = blockIdx.y * CR_TH;
+    const int dy0 = (int)blockIdx.z * 3 - CR_HALO;  // dy rows dy0 .. dy0 + 2
+
+    auto load = [&](int buf, int c0) {
+        // w2: CR_WR rows x 24 columns x 4 float4
+        for (int i = t; i < CR_WR * CR_WW * 4; i += 64) {
+            const int q = i & 3, px = (i >> 2) % CR_WW, r = (i >> 2) / CR_WW;
+            const int gy = by + r + dy0, gx = bx - CR_HALO + px;
+            const bool ok = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            cp_async16(&sw[buf][r * CR_W2P + px * CR_PX + q * 4],
+                       w2 + ((long)(ok ? gy : 0) * W + (ok ? gx : 0)) * C + c0 + q * 4, ok);
         }
-        // w2 rows y + dy, columns x - 4 .. x + 19
-        for (int i = threadIdx.x; i < CTH * CWW * CHK / 4; i += CTW * CTH) {
-            const int px = i / (CHK / 4), q = (i - px * (CHK / 4)) * 4;
-            const int py = by + px / CWW + dy, pxx = bx - HALO + px % CWW;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (py >= 0 && py < H && pxx >= 0 && pxx < W)
-                v = *reinterpret_cast<const float4 *>(w2 + ((long)py * W + pxx) * C + c0 + q);
-            *reinterpret_cast<float4 *>(&s2[px][q]) = v;
+        for (int i = t; i < CR_TH * CR_TW * 4; i += 64) {
+            const int q = i & 3, px = (i >> 2) % CR_TW, r = (i >> 2) / CR_TW;
+            const int gy = by + r, gx = bx + px;
+            const bool ok = gy < H && gx < W;
+            cp_async16(&sf[buf][r * CR_F1P + px * CR_PX + q * 4],
+                       f1 + ((long)(ok ? gy : 0) * W + (ok ? gx : 0)) * C + c0 + q * 4, ok);
+        }
+        cp_async_commit();
+    };
+
+    float acc[2][3][9];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int d = 0; d < 9; ++d) acc[p][j][d] = 0.f;
+
+    const int nch = C / CR_CK;
+    load(0, 0);
+    for (int k = 0; k < nch; ++k) {
+        const int buf = k & 1;
+        if (k + 1 < nch) {
+            load(buf ^ 1, (k + 1) * CR_CK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
+        if (copy_f1 && blockIdx.z == 1) {  // f1 -> x[:, 96 + c], one dy group does it
+            for (int i = t; i < CR_TH * CR_TW * 4; i += 64) {
+                const int q = i & 3, px = (i >> 2) % CR_TW, r = (i >> 2) / CR_TW;
+                const int gy = by + r, gx = bx + px;
+                if (gy < H && gx < W)
+                    *reinterpret_cast<float4 *>(x + ((long)gy * W + gx) * xld + 96 + k * CR_CK + q * 4) =
+                        *reinterpret_cast<const float4 *>(&sf[buf][r * CR_F1P + px * CR_PX + q * 4]);
+            }
+        }
+        const float *w = &sw[buf][ty * CR_W2P + cx * CR_PX];
+        const float *a = &sf[buf][ty * CR_F1P + cx * CR_PX];
 #pragma unroll
-        for (int c = 0; c < CHK; c += 4) {
-            const float4 a = *reinterpret_cast<const float4 *>(&s1[ty * CTW + tx][c]);
+        for (int c = 0; c < CR_CK; c += 4) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(a + c);
+            const float4 a1 = *reinterpret_cast<const float4 *>(a + CR_PX + c);
 #pragma unroll
-            for (int d = 0; d < 9; ++d) {
-                const float4 b = *reinterpret_cast<const float4 *>(&s2[ty * CWW + tx + d][c]);
-                acc[d] = fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, fmaf(a.w, b.w, acc[d]))));
+            for (int j = 0; j < 3; ++j) {
+                float4 b[10];
+#pragma unroll
+                for (int d = 0; d < 10; ++d) b[d] = *reinterpret_cast<const float4 *>(w + j * CR_W2P + d * CR_PX + c);
+#pragma unroll
+                for (int d = 0; d < 9; ++d) {
+                    acc[0][j][d] = fmaf(a0.x, b[d].x, fmaf(a0.y, b[d].y, fmaf(a0.z, b[d].z, fmaf(a0.w, b[d].w, acc[0][j][d]))));
+                    acc[1][j][d] = fmaf(a1.x, b[d + 1].x, fmaf(a1.y, b[d + 1].y,
+                                        fmaf(a1.z, b[d + 1].z, fmaf(a1.w, b[d + 1].w, acc[1][j][d]))));
+                }
             }
         }
         __syncthreads();
     }
-    if (!inb) return;
-    const long pix = (long)y * W + xx;
     const float inv = 1.f / (float)C;
-    float *dst = x + pix * xld + (dy + HALO) * 9;
+    const int y = by + ty;
 #pragma unroll
-    for (int d = 0; d < 9; ++d) dst[d] = leaky(acc[d] * inv);
-    if (copy_f1 && dy == 0)
-        for (int c = 0; c < C; c += 4)
-            *reinterpret_cast<float4 *>(x + pix * xld + 96 + c) =
-                *reinterpret_cast<const float4 *>(f1 + pix * C + c);
+    for (int p = 0; p < 2; ++p) {
+        const int xx = bx + cx + p;
+        if (y >= H || xx >= W) continue;
+        float *dst = x + ((long)y * W + xx) * xld + (dy0 + CR_HALO) * 9;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int d = 0; d < 9; ++d) dst[j * 9 + d] = leaky(acc[p][j][d] * inv);
+    }
+}
+
+// one-time kernel attributes (call outside stream capture)
+int prepare_flow_kernels()
+{
+    static bool done = false;
+    if (done) return SS_OK;
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(2 * (CR_W2F + CR_F1F) * sizeof(float))));
+    done = true;
+    return SS_OK;
 }
 
 int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x, int xld,
                 bool copy_f1, cudaStream_t st)
 {
-    if (C % CHK != 0) {
+    if (C % CR_CK != 0) {
         set_error("correlation needs C % 16 == 0");
         return SS_VALUE_ERROR;
     }
-    const dim3 grid((W + CTW - 1) / CTW, (H + CTH - 1) / CTH, 9);
-    k_corr<<<grid, CTW * CTH, 0, st>>>(f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
-    SS_LAUNCH_CHECK("k_corr");
-    return SS_OK;
+    const dim3 grid((W + CR_TW - 1) / CR_TW, (H + CR_TH - 1) / CR_TH, 3);
+    const size_t smem = 2 * (CR_W2F + CR_F1F) * sizeof(float);
+    if (int rc = prepare_flow_kernels()) return rc;
+    return launch_pdl("k_corr", k_corr, grid, dim3(64), smem, st, f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -389,6 +460,7 @@ __global__ void k_flow_final(const float *__restrict__ f3, int ld3, const float 
                              int ldr, int Hc, int Wc, int h, int w, float *__restrict__ uv,
                              uint8_t *__restrict__ valid)
 {
+    pdl_wait();
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long)h * w) return;
     const int y = (int)(i / w), x = (int)(i - (long)y * w);
@@ -414,10 +486,8 @@ __global__ void k_flow_final(const float *__restrict__ f3, int ld3, const float 
 int launch_flow_final(const float *f3, int ld3, const float *r, int ldr, int Hc, int Wc, int h,
                       int w, float *uv, uint8_t *valid, cudaStream_t st)
 {
-    k_flow_final<<<blocks_for((long)h * w, 256), 256, 0, st>>>(f3, ld3, r, ldr, Hc, Wc, h, w, uv,
-                                                               valid);
-    SS_LAUNCH_CHECK("k_flow_final");
-    return SS_OK;
+    return launch_pdl("k_flow_final", k_flow_final, dim3(blocks_for((long)h * w, 256)), dim3(256), 0, st, f3, ld3,
+                      r, ldr, Hc, Wc, h, w, uv, valid);
 }
 
 }  // namespace fn

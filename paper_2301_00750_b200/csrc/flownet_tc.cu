@@ -63,6 +63,7 @@ __device__ __forceinline__ float lk(float v) { return v >= 0.f ? v : 0.1f * v; }
 template <int KIND>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvParams p)
 {
+    pdl_wait();
     using C = TcCfg<KIND>;
     constexpr int S = C::STAGES;
     extern __shared__ __align__(1024) uint8_t tc_smem[];
@@ -291,6 +292,7 @@ __global__ void k_splitk_reduce(const float *__restrict__ ws, int splits, int M,
                                 const float *__restrict__ bias, int act, float *__restrict__ out,
                                 int out_ld)
 {
+    pdl_wait();
     const int n4 = (Cout + 3) / 4;
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long)M * n4) return;
@@ -317,9 +319,8 @@ int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, co
                          int act, float *out, int out_ld, cudaStream_t st)
 {
     const long n = (long)M * ((Cout + 3) / 4);
-    k_splitk_reduce<<<blocks_for(n, 256), 256, 0, st>>>(ws, splits, M, N, Cout, bias, act, out, out_ld);
-    SS_LAUNCH_CHECK("k_splitk_reduce");
-    return SS_OK;
+    return launch_pdl("k_splitk_reduce", k_splitk_reduce, dim3(blocks_for(n, 256)), dim3(256), 0, st, ws, splits,
+                      M, N, Cout, bias, act, out, out_ld);
 }
 
 static int n_sm_ = 0;
@@ -396,14 +397,10 @@ static int launch_tc_part(ConvParams p, cudaStream_t st)
     // one M tile per CTA (measured faster than persistent CTAs here: the
     // hardware overlaps the per-tile prologues of co-resident CTAs); the
     // kernel's tile loop also supports a persistent grid
-    k_conv_tc<KIND><<<dim3(ctas, splits), TC_THREADS, smem, st>>>(p);
-    SS_LAUNCH_CHECK("k_conv_tc");
-    if (splits > 1) {
-        const long n = (long)M * ((p.Cout + 3) / 4);
-        k_splitk_reduce<<<blocks_for(n, 256), 256, 0, st>>>(ws, splits, M, p.Cout_pad, p.Cout,
-                                                              p.bias, p.act, p.out, p.out_ld);
-        SS_LAUNCH_CHECK("k_splitk_reduce");
-    }
+    if (int rc = launch_pdl("k_conv_tc", k_conv_tc<KIND>, dim3(ctas, splits), dim3(TC_THREADS), smem, st, p))
+        return rc;
+    if (splits > 1)
+        return launch_splitk_reduce(ws, splits, M, p.Cout_pad, p.Cout, p.bias, p.act, p.out, p.out_ld, st);
     return SS_OK;
 }
 

@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
         }
+        pdl_wait();  // the activations are the previous kernel's output
         uint32_t ga = 0, gb = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
             const int tile = u % a.n_tiles, split = u / a.n_tiles;
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     } else if (warp < 6) {
         // ---------------- epilogue ----------------
         const int q = warp & 3;  // TMEM lane quarter this warp may access
+        pdl_wait();
         uint32_t uc = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
             const uint32_t acc = uc & 1;
@@ -332,6 +334,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) pdl_trigger();  // dependents launch as this grid drains
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_rt(tmem, tcols);
@@ -437,6 +440,7 @@ int prepare_conv_tma()
 {
     static bool done = false;
     if (done) return SS_OK;
+    if (int rc = prepare_flow_kernels()) return rc;
     SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
     int dev = 0;
     SS_CUDA_TRY(cudaGetDevice(&dev));
@@ -510,8 +514,9 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, bool halo, i
     a.units = a.n_tiles * splits;
     const int grid = std::min(a.units, n_sm_tma);
     const size_t smem = (size_t)2 * a.na * a.a_slot + (size_t)a.stages * a.b_stage + 1024 + 512;
-    k_conv_tc3<<<grid, TM_THREADS, smem, st>>>(tmA, *static_cast<const CUtensorMap *>(p.tmB), a);
-    SS_LAUNCH_CHECK("k_conv_tc3");
+    if (int rc = launch_pdl("k_conv_tc3", k_conv_tc3, dim3(grid), dim3(TM_THREADS), smem, st, tmA,
+                            *static_cast<const CUtensorMap *>(p.tmB), a))
+        return rc;
     if (splits > 1)
         return launch_splitk_reduce(p.ws, splits, a.M, np, a.Cout, a.bias, p.act, a.out, p.out_ld, st);
     return SS_OK;
