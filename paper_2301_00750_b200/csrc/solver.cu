@@ -106,6 +106,9 @@ struct BlockedArgs {
     float eta, kappa;
     float negzero;            // -0.0f, passed at run time (see fmul2)
     unsigned *maxbits;        // this pass's slot
+    int aligned;              // K = 8, h % 8 == 0, w % 2 == 0: every image edge falls on a
+                              // thread-block boundary, so the fast path also serves the
+                              // edge tiles (replicate boundary by clamped smem offsets)
 };
 
 // One SGD-momentum update (consistency.py:282-291).  The first Laplacian step
@@ -163,18 +166,25 @@ __device__ __forceinline__ void blk_iter(float2 (&X)[blk::R], float2 (&Y)[blk::R
                                          const float2 (&Wv)[blk::R], const float *cur,
                                          float *nxt, int r0, int c0, int lo_r, int hi_r,
                                          int lo_c, int hi_c, float eta, float kappa,
-                                         float negzero, float &mx)
+                                         float negzero, bool track, float &mx)
 {
     using namespace blk;
     if (FAST) {
+        // neighbour offsets; at an image edge (which, in the fast path, lies on
+        // this thread's block boundary) the replicate boundary reads the cell
+        // itself, still in smem from the previous iteration
+        const int wcol = c0 == lo_c ? c0 + 2 : c0 + 1;
+        const int ecol = c0 + 1 == hi_c ? c0 + 3 : c0 + 4;
+        const int nrow = r0 == lo_r ? r0 + 1 : r0;
+        const int srow = r0 + R - 1 == hi_r ? r0 + R : r0 + R + 1;
         float wv[R], ev[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            wv[r] = cur[(r0 + r + 1) * P + c0 + 1];
-            ev[r] = cur[(r0 + r + 1) * P + c0 + 4];
+            wv[r] = cur[(r0 + r + 1) * P + wcol];
+            ev[r] = cur[(r0 + r + 1) * P + ecol];
         }
-        const float2 nv = *reinterpret_cast<const float2 *>(cur + r0 * P + c0 + 2);
-        const float2 sv = *reinterpret_cast<const float2 *>(cur + (r0 + R + 1) * P + c0 + 2);
+        const float2 nv = *reinterpret_cast<const float2 *>(cur + nrow * P + c0 + 2);
+        const float2 sv = *reinterpret_cast<const float2 *>(cur + srow * P + c0 + 2);
         const float2 eta2 = make_float2(eta, eta), kap2 = make_float2(kappa, kappa);
         const float2 z2 = make_float2(negzero, negzero);
 #pragma unroll
@@ -185,7 +195,7 @@ __device__ __forceinline__ void blk_iter(float2 (&X)[blk::R], float2 (&Y)[blk::R
             const float2 u =
                 sgd_update2(X[r], Y[r], n, s, wn, en, Lv[r], Av[r], Wv[r], eta2, kap2, z2);
             Y[r] = u;
-            mx = fmaxf(mx, fmaxf(fabsf(u.x), fabsf(u.y)));
+            if (track) mx = fmaxf(mx, fmaxf(fabsf(u.x), fabsf(u.y)));
         }
     } else {
 #pragma unroll
@@ -217,16 +227,16 @@ __device__ __forceinline__ void blk_run(float2 (&X)[blk::R], float2 (&Y)[blk::R]
                                         const float2 (&Wv)[blk::R], float *sm0, float *sm1,
                                         int r0, int c0, int lo_r, int hi_r, int lo_c, int hi_c,
                                         int iters, float eta, float kappa, float negzero,
-                                        float &mx)
+                                        bool track, float &mx)
 {
     // iterations alternate roles: even -> (X cur, Y prev) read sm0 write sm1
     for (int it = 0; it < iters; it += 2) {
         blk_iter<FAST, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, eta, kappa,
-                          negzero, mx);
+                          negzero, track, mx);
         __syncthreads();
         if (it + 1 < iters) {
             blk_iter<FAST, P>(Y, X, Av, Lv, Wv, sm1, sm0, r0, c0, lo_r, hi_r, lo_c, hi_c, eta,
-                              kappa, negzero, mx);
+                              kappa, negzero, track, mx);
             __syncthreads();
         }
     }
@@ -252,15 +262,18 @@ __device__ __forceinline__ unsigned blk_tile(float2 (&X)[blk::R], float2 (&Y)[bl
     const int lo_c = max(-rx0, -1), hi_c = min(w - 1 - rx0, RW);
     // the fast path must be warp-uniform: __syncthreads (bar.sync.aligned)
     // inside blk_run must be reached at the same PC by every lane of a warp
-    const bool fast = __all_sync(0xffffffffu, gx0 >= 1 && gx0 + 2 <= w - 1 && gy0 >= 1 &&
-                                                  gy0 + R <= h - 1);
+    // (aligned: every block is wholly inside or wholly outside the image; the
+    // outside ones compute ignored values and stay out of the max / NaN scan)
+    const bool fast = a.aligned || __all_sync(0xffffffffu, gx0 >= 1 && gx0 + 2 <= w - 1 && gy0 >= 1 &&
+                                                               gy0 + R <= h - 1);
+    const bool track = !a.aligned || (gx0 >= 0 && gx0 + 2 <= w && gy0 >= 0 && gy0 + R <= h);
     float mx = 0.0f;
     if (fast)
         blk_run<true, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters,
-                         a.eta, a.kappa, a.negzero, mx);
+                         a.eta, a.kappa, a.negzero, track, mx);
     else
         blk_run<false, P>(X, Y, Av, Lv, Wv, sm0, sm1, r0, c0, lo_r, hi_r, lo_c, hi_c, a.iters,
-                          a.eta, a.kappa, a.negzero, mx);
+                          a.eta, a.kappa, a.negzero, track, mx);
 
     // after an odd number of iterations the current iterate lives in Y
     const bool odd = a.iters & 1;
@@ -274,7 +287,7 @@ __device__ __forceinline__ unsigned blk_tile(float2 (&X)[blk::R], float2 (&Y)[bl
         for (int k = 0; k < 2; ++k) {
             const float o = odd ? el(Y[r], k) : el(X[r], k);
             const float op = odd ? el(X[r], k) : el(Y[r], k);
-            nan_seen |= (o != o);
+            nan_seen |= track && (o != o);
             const int gx = gx0 + k;
             if (interior_r && interior_c && gy < h && gx < w) {
                 const long q = (long)gy * w + gx;
@@ -852,6 +865,8 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
             a.kappa = p.kappa;
             a.negzero = -0.0f;
             a.maxbits = wk.maxbits + ps;
+            a.aligned = (variant == 2 ? K : K_LDG) == 8 && wk.h % 8 == 0 && wk.w % 2 == 0 &&
+                        getenv("SS_SOLVER_ALIGNED") == nullptr;
             if (variant == 2) {
                 const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];
                 if (K == 4) rc = launch_tma<4>(mp, a, st);
