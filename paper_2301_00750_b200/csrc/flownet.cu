@@ -222,7 +222,7 @@ int Weights::upload(const float *host, int64_t n)
         if (l.dw) continue;
         const int parts = (l.cout_pad + 127) / 128, np = l.cout_pad / parts;
         l.wt_tma = tma_block + otm[i];
-        l.tma_T = tma_taps_per_stage(l.k, l.stride, np);
+        l.tma_T = tma_taps_per_stage(l.k, l.stride, l.dil, l.cin, np);
         const int kblocks = l.k * l.k * ((l.cin + 31) / 32);
         if (int rc = encode_weight_map(&l.tmB, l.wt_tma, kblocks, 2 * l.cout_pad, np, l.tma_T)) return rc;
     }

@@ -73,7 +73,7 @@ int launch_conv_tma(const ConvParams &p, cudaStream_t st);
 int prepare_conv_tma();
 int prepare_flow_kernels();
 int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, int np, int T);
-int tma_taps_per_stage(int k, int stride, int np);
+int tma_taps_per_stage(int k, int stride, int dil, int cin, int np);
 int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,
                          int act, float *out, int out_ld, cudaStream_t st);
 int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,

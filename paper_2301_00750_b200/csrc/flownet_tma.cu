@@ -63,13 +63,13 @@ constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA
 constexpr int HT_H = 16, HT_W = 8;  // halo-mode output tile (rows x columns)
 
 struct ConvArgs {
-    int halo;          // 1 halo mode, 0 im2col mode
+    int amode;         // A operand: 0 im2col, 1 halo (stride 1), 2 phase halo (3x3 stride 2)
     int H, W, M;       // output size, M = H * W
-    int stride, k, dil, pad, taps, cin, ncb;
-    int T, sp_cb;      // taps per stage, stages per channel block
+    int stride, k, dil, pad, taps, cin, ncb, cpp;  // cpp: channels per A row (8, 16, 32)
+    int T, sp_cb;      // taps per B stage, stages per channel block
     int tiles_x, n_tiles, nk_all, k_per_split, units;
-    int a_box, a_slot, na, halo_w;
-    int np, part_row, Cout, act, out_ld, stages, b_stage;
+    int a_box, a_slot, na, halo_w, ph_bytes;  // ph_bytes: one phase region (amode 2)
+    int np, part_row, Cout, act, out_ld, stages, b_stage, b_res;
     const float *bias;
     float *out;
     float *ws;  // split-K partials [split][M][np] (null: final output)
@@ -78,6 +78,19 @@ struct ConvArgs {
 __device__ __forceinline__ float lk(float v) { return v >= 0.f ? v : 0.1f * v; }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// K-major swizzled smem descriptor for rows of rowb bytes (SWIZZLE_{32,64,128}B:
+// layout 6 / 4 / 2), 8-row groups sbo bytes apart, any row-aligned start
+__device__ __forceinline__ uint64_t sdesc_sw(uint32_t saddr, uint32_t sbo, uint32_t layout)
+{
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
 
 // one K = 8 step of 3xTF32 (see the file comment), elected lane of a converged warp
 __device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, uint64_t b,
@@ -93,6 +106,14 @@ __device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, u
         : "memory");
 }
 
+// whether stage st (of a unit starting at kb) loads a new A operand
+template <int AMODE>
+__device__ __forceinline__ bool a_event(int st, int kb, int grp)
+{
+    return AMODE == 0 || st == kb || grp == 0;
+}
+
+template <int AMODE, bool BRES>
 __global__ void __launch_bounds__(TM_THREADS, 1)
     k_conv_tc3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const ConvArgs a)
@@ -108,7 +129,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     uint64_t *acc_full = b_empty + S, *acc_empty = acc_full + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index through a shuffle: the compiler then knows it (and every
+    // role branch) is warp-uniform and keeps descriptors in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const uint32_t acc_cols = (uint32_t)(2 * np + 31) / 32 * 32;
     uint32_t tcols = 32;
     while (tcols < 2 * acc_cols) tcols <<= 1;
@@ -133,7 +156,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const uint32_t rowb = (uint32_t)a.cpp * 4u;
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -141,48 +165,66 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
         }
+        if (BRES && elect_one()) {
+            // all weight stages of the layer stay resident: one load per CTA
+            mbar_expect_tx(&b_full[0], (uint32_t)(a.nk_all * a.b_stage));
+            for (int kk = 0; kk < a.nk_all; ++kk) {
+                const int cb = kk / a.sp_cb, grp = kk - cb * a.sp_cb;
+                tma_tile_3d(smem_u32(bst + kk * a.b_stage), &tmB, 0, a.part_row, cb * a.taps + grp * a.T,
+                            &b_full[0]);
+            }
+        }
+        __syncwarp();
         pdl_wait();  // the activations are the previous kernel's output
         uint32_t ga = 0, gb = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
             const int tile = u % a.n_tiles, split = u / a.n_tiles;
             int x0, y0;
-            if (a.halo) {
-                const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
-                x0 = tx * HT_W - a.pad;
-                y0 = ty * HT_H - a.pad;
-            } else {
+            if (AMODE == 0) {
                 const int m0 = tile * 128, oy = m0 / a.W, ox = m0 - oy * a.W;
                 x0 = ox * a.stride - a.pad;
                 y0 = oy * a.stride - a.pad;
+            } else {
+                const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+                x0 = tx * HT_W * a.stride - a.pad;
+                y0 = ty * HT_H * a.stride - a.pad;
             }
             const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
             int cb = kb / a.sp_cb, grp = kb - cb * a.sp_cb;
             for (int st = kb; st < ke; ++st, ++gb) {
                 const int tap0 = grp * a.T;
-                if (!a.halo || st == kb || grp == 0) {
+                if (a_event<AMODE>(st, kb, grp)) {
                     const int sa = (int)(ga % (uint32_t)NA);
                     mbar_wait(&a_empty[sa], ((ga / NA) & 1) ^ 1);
                     if (elect_one()) {
                         const uint32_t dst = smem_u32(aslots + sa * 2 * a.a_slot);
                         mbar_expect_tx(&a_full[sa], (uint32_t)a.a_box);
-                        if (a.halo) {
-                            tma_tile_3d(dst, &tmA, cb * 32, x0, y0, &a_full[sa]);
+                        if (AMODE == 1) {
+                            tma_tile_3d(dst, &tmA, cb * a.cpp, x0, y0, &a_full[sa]);
+                        } else if (AMODE == 2) {
+                            // the four (row, column) parity phases of the stride-2 window
+                            for (int ph = 0; ph < 4; ++ph)
+                                tma_tile_3d(dst + ph * a.ph_bytes, &tmA, cb * a.cpp, x0 + (ph & 1), y0 + (ph >> 1),
+                                            &a_full[sa]);
                         } else {
                             const int ky = tap0 / a.k, kx = tap0 - ky * a.k;
-                            tma_im2col_4d(dst, &tmA, cb * 32, x0, y0, 0, (uint16_t)(kx * a.dil),
+                            tma_im2col_4d(dst, &tmA, cb * a.cpp, x0, y0, 0, (uint16_t)(kx * a.dil),
                                           (uint16_t)(ky * a.dil), &a_full[sa]);
                         }
                     }
                     __syncwarp();
                     ++ga;
                 }
-                const int s = (int)(gb % (uint32_t)S);
-                mbar_wait(&b_empty[s], ((gb / S) & 1) ^ 1);
-                if (elect_one()) {
-                    mbar_expect_tx(&b_full[s], (uint32_t)a.b_stage);
-                    tma_tile_3d(smem_u32(bst + s * a.b_stage), &tmB, 0, a.part_row, cb * a.taps + tap0, &b_full[s]);
+                if (!BRES) {
+                    const int s = (int)(gb % (uint32_t)S);
+                    mbar_wait(&b_empty[s], ((gb / S) & 1) ^ 1);
+                    if (elect_one()) {
+                        mbar_expect_tx(&b_full[s], (uint32_t)a.b_stage);
+                        tma_tile_3d(smem_u32(bst + s * a.b_stage), &tmB, 0, a.part_row, cb * a.taps + tap0,
+                                    &b_full[s]);
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
                 if (++grp == a.sp_cb) {
                     grp = 0;
                     ++cb;
@@ -192,8 +234,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         const uint32_t id2 = idesc(2u, 128u, (uint32_t)(2 * np)), id1 = idesc(2u, 128u, (uint32_t)np);
-        const uint32_t sbo = a.halo ? (uint32_t)a.halo_w * 128u : 1024u;
+        const uint32_t alay = rowb == 128 ? 2u : (rowb == 64 ? 4u : 6u);
+        const uint32_t sbo = (AMODE == 0 ? 8u : (uint32_t)a.halo_w) * rowb;
         const uint32_t bstride = (uint32_t)(2 * np * 128);
+        if (BRES) mbar_wait(&b_full[0], 0);
         uint32_t ga = 0, gb = 0, uc = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
             const int split = u / a.n_tiles;
@@ -204,24 +248,30 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             const uint32_t d = tmem + acc * acc_cols;
             int cb = kb / a.sp_cb, grp = kb - cb * a.sp_cb, sa = 0;
             for (int st = kb; st < ke; ++st, ++gb) {
-                const bool a_event = !a.halo || st == kb || grp == 0;
-                if (a_event) {
+                if (a_event<AMODE>(st, kb, grp)) {
                     sa = (int)(ga % (uint32_t)NA);
                     mbar_wait(&a_conv[sa], (ga / NA) & 1);
                     ++ga;
                 }
-                const int s = (int)(gb % (uint32_t)S);
-                mbar_wait(&b_full[s], (gb / S) & 1);
+                const int s = BRES ? st : (int)(gb % (uint32_t)S);
+                if (!BRES) mbar_wait(&b_full[s], (gb / S) & 1);
                 tc_fence_after();
                 const int tap0 = grp * a.T, nt = min(a.T, a.taps - tap0);
-                const int nks = min(4, (a.cin - cb * 32 + 7) >> 3);
+                const int nks = min(a.cpp, a.cin - cb * a.cpp + 7) >> 3;
                 const uint32_t araw = smem_u32(aslots + sa * 2 * a.a_slot);
                 const uint32_t b0 = smem_u32(bst + s * a.b_stage);
                 int ky = tap0 / a.k, kx = tap0 - ky * a.k;
                 for (int j = 0; j < nt; ++j) {
-                    const uint32_t off = a.halo ? (uint32_t)((ky * a.halo_w + kx) * a.dil) * 128u : 0u;
-                    const uint64_t ah = sdesc_sw128_sbo(araw + off, sbo);
-                    const uint64_t al = sdesc_sw128_sbo(araw + a.a_slot + off, sbo);
+                    uint32_t off = 0;
+                    if (AMODE == 1)
+                        off = (uint32_t)((ky * a.halo_w + kx) * a.dil) * rowb;
+                    else if (AMODE == 2)
+                        off = (uint32_t)(((ky & 1) * 2 + (kx & 1)) * a.ph_bytes) +
+                              (uint32_t)((ky >> 1) * a.halo_w + (kx >> 1)) * rowb;
+                    const uint64_t ah = sdesc_sw(araw + off, sbo, alay);
+                    const uint64_t al = sdesc_sw(araw + a.a_slot + off, sbo, alay);
+                    // B rows hold 32 channels: a narrow A row (cpp < 32) only
+                    // ever meets channel block 0, whose first cpp channels align
                     const uint64_t bd = sdesc_sw128(b0 + j * bstride);
                     for (int i = 0; i < nks; ++i)  // +32 bytes of K = +2 in the address field
                         mma_step(d, ah + 2 * i, al + 2 * i, bd + 2 * i, id2, id1,
@@ -231,8 +281,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                         ++ky;
                     }
                 }
-                mma_commit_elect(&b_empty[s]);
-                const bool a_last = !a.halo || grp == a.sp_cb - 1 || st == ke - 1;
+                if (!BRES) mma_commit_elect(&b_empty[s]);
+                const bool a_last = AMODE == 0 || grp == a.sp_cb - 1 || st == ke - 1;
                 if (a_last) mma_commit_elect(&a_empty[sa]);
                 __syncwarp();
                 if (++grp == a.sp_cb) {
@@ -256,14 +306,14 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             const int m = q * 32 + lane;
             bool ok;
             size_t pix;
-            if (a.halo) {
+            if (AMODE == 0) {
+                pix = (size_t)tile * 128 + m;
+                ok = pix < (size_t)a.M;
+            } else {
                 const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
                 const int oy = ty * HT_H + (m >> 3), ox = tx * HT_W + (m & 7);
                 ok = oy < a.H && ox < a.W;
                 pix = (size_t)oy * a.W + ox;
-            } else {
-                pix = (size_t)tile * 128 + m;
-                ok = pix < (size_t)a.M;
             }
             const uint32_t t0 = tmem + acc * acc_cols + ((uint32_t)(q * 32) << 16);
             for (int c0 = 0; c0 < np; c0 += 16) {
@@ -303,16 +353,16 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     } else {
         // ---------------- converters: A -> (hi in place, lo beside) ----------------
         const int t = threadIdx.x - 192;
-        const int n16 = a.a_box / 16;
+        const int n16 = a.a_slot / 16;  // whole slot (phase padding included)
         uint32_t ga = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
             const int split = u / a.n_tiles;
             const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
             int grp = kb % a.sp_cb;
             for (int st = kb; st < ke; ++st) {
-                const bool a_event = !a.halo || st == kb || grp == 0;
+                const bool ev = a_event<AMODE>(st, kb, grp);
                 if (++grp == a.sp_cb) grp = 0;
-                if (!a_event) continue;
+                if (!ev) continue;
                 const int sa = (int)(ga % (uint32_t)NA);
                 mbar_wait(&a_full[sa], (ga / NA) & 1);
                 ++ga;
@@ -365,10 +415,19 @@ PFN_cuTensorMapEncodeIm2col_v12000 im2col_fn()
 
 int n_sm_tma = 0;
 
-int encode_act_map(CUtensorMap *m, const ConvParams &p, bool halo, int halo_w, int halo_h)
+CUtensorMapSwizzle swz_for(int rowb)
+{
+    return rowb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (rowb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// amode 1: box (cpp, halo_w, halo_h); amode 2: box (cpp, 18, 34) with
+// traversal stride 2 in W and H (a 9 x 17 phase of the stride-2 window);
+// amode 0: im2col column of 128 pixels
+int encode_act_map(CUtensorMap *m, const ConvParams &p, int amode, int cpp, int halo_w, int halo_h)
 {
     CUresult r;
-    if (halo) {
+    const int rowb = cpp * 4;
+    if (amode != 0) {
         auto fn = tiled_fn();
         if (!fn) {
             set_error("cuTensorMapEncodeTiled unavailable");
@@ -376,11 +435,12 @@ int encode_act_map(CUtensorMap *m, const ConvParams &p, bool halo, int halo_w, i
         }
         const cuuint64_t dims[3] = {(cuuint64_t)p.Cin, (cuuint64_t)p.W, (cuuint64_t)p.H};
         const cuuint64_t strides[2] = {(cuuint64_t)p.in_ld * 4, (cuuint64_t)p.in_ld * 4 * p.W};
-        const cuuint32_t box[3] = {32, (cuuint32_t)halo_w, (cuuint32_t)halo_h};
-        const cuuint32_t estr[3] = {1, 1, 1};
-        r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(p.in), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const cuuint32_t box2[3] = {(cuuint32_t)cpp, 18, 34}, box1[3] = {(cuuint32_t)cpp, (cuuint32_t)halo_w,
+                                                                          (cuuint32_t)halo_h};
+        const cuuint32_t estr2[3] = {1, 2, 2}, estr1[3] = {1, 1, 1};
+        r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(p.in), dims, strides,
+               amode == 2 ? box2 : box1, amode == 2 ? estr2 : estr1, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_for(rowb),
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
         auto fn = im2col_fn();
         if (!fn) {
@@ -394,8 +454,8 @@ int encode_act_map(CUtensorMap *m, const ConvParams &p, bool halo, int halo_w, i
         const int lower[2] = {-p.pad, -p.pad};  // (W, H)
         const int upper[2] = {up, up};
         const cuuint32_t estr[4] = {1, (cuuint32_t)p.stride, (cuuint32_t)p.stride, 1};
-        r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(p.in), dims, strides, lower, upper, 32,
-               128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(p.in), dims, strides, lower, upper,
+               (cuuint32_t)cpp, 128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_for(rowb),
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) {
@@ -407,9 +467,19 @@ int encode_act_map(CUtensorMap *m, const ConvParams &p, bool halo, int halo_w, i
 
 }  // namespace
 
-int tma_taps_per_stage(int k, int stride, int np)
+// A-operand mode of a layer (see launch_conv_tma): stride-1 -> halo; 3x3
+// stride 2 with <= 16 input channels -> phase halo (its four phase tiles of
+// 32-channel rows would not fit twice in shared memory); otherwise im2col
+static int amode_for(int k, int stride, int dil, int cin)
 {
-    if (stride != 1) return 1;
+    if (stride == 1) return 1;
+    if (stride == 2 && k == 3 && dil == 1 && cin <= 16) return 2;
+    return 0;
+}
+
+int tma_taps_per_stage(int k, int stride, int dil, int cin, int np)
+{
+    if (amode_for(k, stride, dil, cin) == 0) return 1;  // im2col: one tap per stage
     return std::max(1, std::min(k * k, 36864 / (2 * np * 128)));
 }
 
@@ -441,7 +511,12 @@ int prepare_conv_tma()
     static bool done = false;
     if (done) return SS_OK;
     if (int rc = prepare_flow_kernels()) return rc;
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
     int dev = 0;
     SS_CUDA_TRY(cudaGetDevice(&dev));
     SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm_tma, cudaDevAttrMultiProcessorCount, dev));
@@ -450,11 +525,11 @@ int prepare_conv_tma()
 }
 
 // one output-channel part (rows [part * 2 np, +2 np) of the weight tensor)
-static int launch_part(const ConvParams &p, const CUtensorMap &tmA, bool halo, int halo_w, int halo_h,
-                       int part, int np, cudaStream_t st)
+static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int amode, int cpp, int halo_w,
+                       int halo_h, int part, int np, cudaStream_t st)
 {
     ConvArgs a;
-    a.halo = halo ? 1 : 0;
+    a.amode = amode;
     a.H = p.Ho;
     a.W = p.Wo;
     a.M = p.Ho * p.Wo;
@@ -464,23 +539,34 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, bool halo, i
     a.pad = p.pad;
     a.taps = p.k * p.k;
     a.cin = p.Cin;
-    a.ncb = (p.Cin + 31) / 32;
+    a.cpp = cpp;
+    a.ncb = (p.Cin + cpp - 1) / cpp;
     a.T = p.tma_T;
     a.sp_cb = (a.taps + a.T - 1) / a.T;
-    if (halo) {
-        a.tiles_x = (p.Wo + HT_W - 1) / HT_W;
-        a.n_tiles = a.tiles_x * ((p.Ho + HT_H - 1) / HT_H);
-        a.halo_w = halo_w;
-        a.a_box = halo_w * halo_h * 128;
-        a.na = 2;
-    } else {
+    const int rowb = cpp * 4;
+    a.ph_bytes = 0;
+    if (amode == 0) {
         a.tiles_x = 0;
         a.n_tiles = (a.M + 127) / 128;
         a.halo_w = 8;
-        a.a_box = 128 * 128;
+        a.a_box = 128 * rowb;
+        a.a_slot = (a.a_box + 1023) / 1024 * 1024;
         a.na = 4;
+    } else {
+        a.tiles_x = (p.Wo + HT_W - 1) / HT_W;
+        a.n_tiles = a.tiles_x * ((p.Ho + HT_H - 1) / HT_H);
+        if (amode == 1) {
+            a.halo_w = halo_w;
+            a.a_box = halo_w * halo_h * rowb;
+            a.a_slot = (a.a_box + 1023) / 1024 * 1024;
+        } else {
+            a.halo_w = 9;  // phase tiles: 17 rows x 9 columns
+            a.ph_bytes = (9 * 17 * rowb + 1023) / 1024 * 1024;
+            a.a_box = 4 * 9 * 17 * rowb;
+            a.a_slot = 4 * a.ph_bytes;
+        }
+        a.na = 2;
     }
-    a.a_slot = (a.a_box + 1023) / 1024 * 1024;
     a.nk_all = a.ncb * a.sp_cb;
     a.np = np;
     a.part_row = part * 2 * np;
@@ -490,13 +576,20 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, bool halo, i
     a.bias = p.bias + part * np;
     a.out = p.out + part * np;
     a.b_stage = a.T * 2 * np * 128;
-    const int fixed = 2 * a.na * a.a_slot + 1024 + 512;
-    a.stages = std::min(8, (SMEM_MAX - fixed) / a.b_stage);
-    if (a.stages < 2 && !halo) {
-        a.na = 2;
-        a.stages = std::min(8, (SMEM_MAX - (2 * a.na * a.a_slot + 1536)) / a.b_stage);
+    const int bar_bytes = 1024 + 512;
+    // weights resident for the whole launch when every stage fits
+    static const bool res_on = getenv("SS_CONV_BRES") == nullptr || strcmp(getenv("SS_CONV_BRES"), "0");
+    a.b_res = res_on && 2 * a.na * a.a_slot + a.nk_all * a.b_stage + bar_bytes + a.nk_all * 16 <= SMEM_MAX;
+    if (a.b_res) {
+        a.stages = a.nk_all;
+    } else {
+        a.stages = std::min(8, (SMEM_MAX - 2 * a.na * a.a_slot - bar_bytes) / a.b_stage);
+        if (a.stages < 2 && amode == 0) {
+            a.na = 2;
+            a.stages = std::min(8, (SMEM_MAX - 2 * a.na * a.a_slot - bar_bytes) / a.b_stage);
+        }
     }
-    if (a.stages < 2) {
+    if (a.stages < (a.b_res ? 1 : 2)) {
         set_error("conv stage does not fit in shared memory");
         return SS_VALUE_ERROR;
     }
@@ -513,10 +606,19 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, bool halo, i
     a.ws = splits > 1 ? p.ws : nullptr;
     a.units = a.n_tiles * splits;
     const int grid = std::min(a.units, n_sm_tma);
-    const size_t smem = (size_t)2 * a.na * a.a_slot + (size_t)a.stages * a.b_stage + 1024 + 512;
-    if (int rc = launch_pdl("k_conv_tc3", k_conv_tc3, dim3(grid), dim3(TM_THREADS), smem, st, tmA,
-                            *static_cast<const CUtensorMap *>(p.tmB), a))
-        return rc;
+    const size_t smem = (size_t)2 * a.na * a.a_slot + (size_t)a.stages * a.b_stage + bar_bytes + a.stages * 16;
+    const CUtensorMap &tmB = *static_cast<const CUtensorMap *>(p.tmB);
+    int rc;
+    if (amode == 1)
+        rc = a.b_res ? launch_pdl("k_conv_tc3", k_conv_tc3<1, true>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a)
+                     : launch_pdl("k_conv_tc3", k_conv_tc3<1, false>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a);
+    else if (amode == 2)
+        rc = a.b_res ? launch_pdl("k_conv_tc3", k_conv_tc3<2, true>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a)
+                     : launch_pdl("k_conv_tc3", k_conv_tc3<2, false>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a);
+    else
+        rc = a.b_res ? launch_pdl("k_conv_tc3", k_conv_tc3<0, true>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a)
+                     : launch_pdl("k_conv_tc3", k_conv_tc3<0, false>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a);
+    if (rc) return rc;
     if (splits > 1)
         return launch_splitk_reduce(p.ws, splits, a.M, np, a.Cout, a.bias, p.act, a.out, p.out_ld, st);
     return SS_OK;
@@ -530,18 +632,22 @@ int launch_conv_tma(const ConvParams &p, cudaStream_t st)
         return SS_VALUE_ERROR;
     }
     static const bool halo_on = getenv("SS_CONV_HALO") == nullptr || strcmp(getenv("SS_CONV_HALO"), "0");
-    const bool halo = halo_on && p.stride == 1 && p.Ho == p.H && p.Wo == p.W;
-    if (!halo && p.tma_T != 1) {
+    int amode = halo_on ? amode_for(p.k, p.stride, p.dil, p.Cin) : 0;
+    if (amode == 1 && !(p.Ho == p.H && p.Wo == p.W)) amode = 0;
+    if (amode == 2 && p.pad != 1) amode = 0;
+    if (amode == 0 && p.tma_T != 1) {
         set_error("im2col conv path needs one tap per stage");
         return SS_VALUE_ERROR;
     }
+    static const bool wide = getenv("SS_CONV_CPP32") != nullptr;
+    const int cpp = (wide && amode != 2) ? 32 : (p.Cin <= 8 ? 8 : (p.Cin <= 16 ? 16 : 32));
     const int halo_w = HT_W + 2 * p.pad, halo_h = HT_H + 2 * p.pad;
     alignas(64) CUtensorMap tmA;
-    if (int rc = encode_act_map(&tmA, p, halo, halo_w, halo_h)) return rc;
+    if (int rc = encode_act_map(&tmA, p, amode, cpp, halo_w, halo_h)) return rc;
     const int parts = (p.Cout_pad + 127) / 128;
     const int np = p.Cout_pad / parts;
     for (int part = 0; part < parts; ++part)
-        if (int rc = launch_part(p, tmA, halo, halo_w, halo_h, part, np, st)) return rc;
+        if (int rc = launch_part(p, tmA, amode, cpp, halo_w, halo_h, part, np, st)) return rc;
     return SS_OK;
 }
 
