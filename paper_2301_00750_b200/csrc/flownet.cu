@@ -65,6 +65,7 @@ Weights::~Weights()
     cudaFree(block);
     cudaFree(tc_block);
     cudaFree(tma_block);
+    cudaFree(bf_block);
 }
 
 int Weights::expected_params()
@@ -222,9 +223,51 @@ int Weights::upload(const float *host, int64_t n)
         if (l.dw) continue;
         const int parts = (l.cout_pad + 127) / 128, np = l.cout_pad / parts;
         l.wt_tma = tma_block + otm[i];
-        l.tma_T = tma_taps_per_stage(l.k, l.stride, l.dil, l.cin, np);
+        l.tma_T = tma_taps_per_stage(l.k, l.stride, l.dil, l.cin, np, 1);
         const int kblocks = l.k * l.k * ((l.cin + 31) / 32);
         if (int rc = encode_weight_map(&l.tmB, l.wt_tma, kblocks, 2 * l.cout_pad, np, l.tma_T)) return rc;
+    }
+
+    // bf16 TMA path: [kblocks][cout_pad rows][32] bf16 (round to nearest even),
+    // same kblock order; rows of part p are [p * np, (p + 1) * np)
+    std::vector<size_t> obt(layers.size(), 0);
+    size_t bt_total = 0;
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        obt[i] = bt_total;
+        bt_total += (size_t)l.k * l.k * ((l.cin + 31) / 32) * l.cout_pad * 32;
+    }
+    std::vector<uint16_t> bth(bt_total, 0);
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        const int taps = l.k * l.k, N = l.cout_pad;
+        const float *wl = dev.data() + woff[i];
+        uint16_t *dst = bth.data() + obt[i];
+        for (int tap = 0; tap < taps; ++tap)
+            for (int c = 0; c < l.cin; ++c) {
+                const size_t kb = (size_t)(c / 32) * taps + tap;
+                for (int n = 0; n < l.cout; ++n) {
+                    const float f = wl[(size_t)(tap * l.cin + c) * N + n];
+                    uint32_t u;
+                    std::memcpy(&u, &f, 4);
+                    dst[(kb * N + n) * 32 + c % 32] = (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+                }
+            }
+    }
+    cudaFree(bf_block);
+    bf_block = nullptr;
+    SS_CUDA_TRY(cudaMalloc(&bf_block, bt_total * sizeof(uint16_t)));
+    SS_CUDA_TRY(cudaMemcpy(bf_block, bth.data(), bt_total * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        const int parts = (l.cout_pad + 127) / 128, np = l.cout_pad / parts;
+        l.wt_bf = static_cast<uint16_t *>(bf_block) + obt[i];
+        l.tma_T_bf = tma_taps_per_stage(l.k, l.stride, l.dil, l.cin, np, 0);
+        const int kblocks = l.k * l.k * ((l.cin + 31) / 32);
+        if (int rc = encode_weight_map_bf16(&l.tmB_bf, l.wt_bf, kblocks, l.cout_pad, np, l.tma_T_bf)) return rc;
     }
     return SS_OK;
 }
@@ -378,10 +421,11 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
     p.Ho = (Hi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.Wo = (Wi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.act = L.act;
-    p.tmB = &L.tmB;
-    p.tma_T = L.tma_T;
+    const bool bf = conv_mode_ == CONV_TC_BF16;
+    p.tmB = bf ? &L.tmB_bf : &L.tmB;
+    p.tma_T = bf ? L.tma_T_bf : L.tma_T;
     if (conv_mode_ == CONV_FFMA) return launch_conv_ffma(p, st);
-    if (conv_mode_ == CONV_TC_TF32X3 && use_tma_) return launch_conv_tma(p, st);
+    if (use_tma_) return launch_conv_tma(p, bf ? 0 : 1, st);
     return launch_conv_tc(p, conv_mode_ == CONV_TC_BF16 ? 0 : 1, st);
 }
 

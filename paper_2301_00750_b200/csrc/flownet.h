@@ -69,11 +69,12 @@ int launch_conv_ffma(const ConvParams &p, cudaStream_t st);
 int launch_conv_tc(const ConvParams &p, int kind, cudaStream_t st);
 int prepare_conv_tc();  // one-time kernel attributes (call outside stream capture)
 // TMA-fed warp-specialised 3xTF32 conv (flownet_tma.cu)
-int launch_conv_tma(const ConvParams &p, cudaStream_t st);
+int launch_conv_tma(const ConvParams &p, int prec, cudaStream_t st);  // prec: 1 3xTF32, 0 bf16
 int prepare_conv_tma();
 int prepare_flow_kernels();
 int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, int np, int T);
-int tma_taps_per_stage(int k, int stride, int dil, int cin, int np);
+int tma_taps_per_stage(int k, int stride, int dil, int cin, int np, int prec);
+int encode_weight_map_bf16(CUtensorMap *m, const void *wt, int kblocks, int rows, int np, int T);
 int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,
                          int act, float *out, int out_ld, cudaStream_t st);
 int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,
@@ -96,6 +97,10 @@ struct LayerDev {
     const float *wt_tma = nullptr;
     int tma_T = 1;
     alignas(64) CUtensorMap tmB;
+    // bf16 path: [kblock][part][np rows][32 channels] bf16, map, taps per stage
+    const void *wt_bf = nullptr;
+    int tma_T_bf = 1;
+    alignas(64) CUtensorMap tmB_bf;
 };
 
 // Weights on one device, in liteflownet.layer_table() order.
@@ -104,6 +109,7 @@ struct Weights {
     float *block = nullptr;
     void *tc_block = nullptr;
     float *tma_block = nullptr;
+    void *bf_block = nullptr;
     ~Weights();
     static int expected_params();
     int upload(const float *host, int64_t n);

@@ -32,6 +32,7 @@
 // TMEM holds two accumulators, so the epilogue of a unit overlaps the MMAs of
 // the next.  Producer and MMA warps run converged; one elected lane issues.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
@@ -106,6 +107,25 @@ __device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, u
         : "memory");
 }
 
+// one K = 16 step of bf16 x bf16 -> fp32 (kind::f16), elected lane
+__device__ __forceinline__ void mma_step_bf16(uint32_t d, uint64_t a_, uint64_t b, uint32_t id, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t}" ::"r"(d),
+        "l"(a_), "l"(b), "r"(acc), "r"(id)
+        : "memory");
+}
+
+// physical 16-byte chunk of logical chunk c in row r of a swizzled tile with
+// rows of rb bytes (SWIZZLE_{128,64,32}B; the tile base is 1024-aligned)
+__device__ __forceinline__ int swz_chunk(int c, int r, int rb)
+{
+    return rb == 128 ? (c ^ (r & 7)) : (rb == 64 ? (c ^ ((r >> 1) & 3)) : (c ^ ((r >> 2) & 1)));
+}
+
 // whether stage st (of a unit starting at kb) loads a new A operand
 template <int AMODE>
 __device__ __forceinline__ bool a_event(int st, int kb, int grp)
@@ -113,7 +133,9 @@ __device__ __forceinline__ bool a_event(int st, int kb, int grp)
     return AMODE == 0 || st == kb || grp == 0;
 }
 
-template <int AMODE, bool BRES>
+// PREC 1: 3xTF32 (fp32-class); PREC 0: bf16 operands (converted from the fp32
+// activations in shared memory, kind::f16), fp32 accumulation
+template <int PREC, int AMODE, bool BRES>
 __global__ void __launch_bounds__(TM_THREADS, 1)
     k_conv_tc3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const ConvArgs a)
@@ -132,7 +154,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     // warp index through a shuffle: the compiler then knows it (and every
     // role branch) is warp-uniform and keeps descriptors in uniform registers
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-    const uint32_t acc_cols = (uint32_t)(2 * np + 31) / 32 * 32;
+    const uint32_t acc_cols = (uint32_t)((PREC ? 2 : 1) * np + 31) / 32 * 32;
     uint32_t tcols = 32;
     while (tcols < 2 * acc_cols) tcols <<= 1;
 
@@ -234,9 +256,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         const uint32_t id2 = idesc(2u, 128u, (uint32_t)(2 * np)), id1 = idesc(2u, 128u, (uint32_t)np);
-        const uint32_t alay = rowb == 128 ? 2u : (rowb == 64 ? 4u : 6u);
-        const uint32_t sbo = (AMODE == 0 ? 8u : (uint32_t)a.halo_w) * rowb;
-        const uint32_t bstride = (uint32_t)(2 * np * 128);
+        const uint32_t idb = idesc(1u, 128u, (uint32_t)np);
+        // bf16 operand rows are half as wide as the fp32 rows they come from
+        const uint32_t arb = PREC ? rowb : rowb / 2;
+        const uint32_t alay = arb == 128 ? 2u : (arb == 64 ? 4u : 6u);
+        const uint32_t sbo = (AMODE == 0 ? 8u : (uint32_t)a.halo_w) * arb;
+        const uint32_t bstride = PREC ? (uint32_t)(2 * np * 128) : (uint32_t)(np * 64);
         if (BRES) mbar_wait(&b_full[0], 0);
         uint32_t ga = 0, gb = 0, uc = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
@@ -257,25 +282,34 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 if (!BRES) mbar_wait(&b_full[s], (gb / S) & 1);
                 tc_fence_after();
                 const int tap0 = grp * a.T, nt = min(a.T, a.taps - tap0);
-                const int nks = min(a.cpp, a.cin - cb * a.cpp + 7) >> 3;
+                const int live = min(a.cpp, a.cin - cb * a.cpp);
+                const int nks = PREC ? (live + 7) >> 3 : (live + 15) >> 4;
                 const uint32_t araw = smem_u32(aslots + sa * 2 * a.a_slot);
                 const uint32_t b0 = smem_u32(bst + s * a.b_stage);
                 int ky = tap0 / a.k, kx = tap0 - ky * a.k;
                 for (int j = 0; j < nt; ++j) {
                     uint32_t off = 0;
                     if (AMODE == 1)
-                        off = (uint32_t)((ky * a.halo_w + kx) * a.dil) * rowb;
+                        off = (uint32_t)((ky * a.halo_w + kx) * a.dil) * arb;
                     else if (AMODE == 2)
-                        off = (uint32_t)(((ky & 1) * 2 + (kx & 1)) * a.ph_bytes) +
-                              (uint32_t)((ky >> 1) * a.halo_w + (kx >> 1)) * rowb;
-                    const uint64_t ah = sdesc_sw(araw + off, sbo, alay);
-                    const uint64_t al = sdesc_sw(araw + a.a_slot + off, sbo, alay);
+                        off = (uint32_t)(((ky & 1) * 2 + (kx & 1)) * (PREC ? a.ph_bytes : a.ph_bytes / 2)) +
+                              (uint32_t)((ky >> 1) * a.halo_w + (kx >> 1)) * arb;
                     // B rows hold 32 channels: a narrow A row (cpp < 32) only
                     // ever meets channel block 0, whose first cpp channels align
-                    const uint64_t bd = sdesc_sw128(b0 + j * bstride);
-                    for (int i = 0; i < nks; ++i)  // +32 bytes of K = +2 in the address field
-                        mma_step(d, ah + 2 * i, al + 2 * i, bd + 2 * i, id2, id1,
-                                 (st > kb || j > 0 || i > 0) ? 1u : 0u);
+                    if (PREC) {
+                        const uint64_t ah = sdesc_sw(araw + off, sbo, alay);
+                        const uint64_t al = sdesc_sw(araw + a.a_slot + off, sbo, alay);
+                        const uint64_t bd = sdesc_sw128(b0 + j * bstride);
+                        for (int i = 0; i < nks; ++i)  // +32 bytes of K = +2 in the address field
+                            mma_step(d, ah + 2 * i, al + 2 * i, bd + 2 * i, id2, id1,
+                                     (st > kb || j > 0 || i > 0) ? 1u : 0u);
+                    } else {
+                        // bf16 copy of the tile lives in the second half of the slot
+                        const uint64_t ad = sdesc_sw(araw + a.a_slot + off, sbo, alay);
+                        const uint64_t bd = sdesc_sw(b0 + j * bstride, 512u, 4u);  // 64-byte rows
+                        for (int i = 0; i < nks; ++i)  // K = 16 bf16 = 32 bytes per MMA
+                            mma_step_bf16(d, ad + 2 * i, bd + 2 * i, idb, (st > kb || j > 0 || i > 0) ? 1u : 0u);
+                    }
                     if (++kx == a.k) {
                         kx = 0;
                         ++ky;
@@ -317,12 +351,15 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             }
             const uint32_t t0 = tmem + acc * acc_cols + ((uint32_t)(q * 32) << 16);
             for (int c0 = 0; c0 < np; c0 += 16) {
-                float v[16], w[16];
+                float v[16];
                 tmem_ld16(t0 + c0, v);
-                tmem_ld16(t0 + np + c0, w);
-                if (!ok) continue;
+                if (PREC) {
+                    float w[16];
+                    tmem_ld16(t0 + np + c0, w);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] += w[i];
+                    for (int i = 0; i < 16; ++i) v[i] += w[i];
+                }
+                if (!ok) continue;
                 if (a.ws) {
                     float *dst = a.ws + ((size_t)split * a.M + pix) * np + c0;
 #pragma unroll
@@ -367,14 +404,32 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 mbar_wait(&a_full[sa], (ga / NA) & 1);
                 ++ga;
                 float4 *ar = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot);
-                float4 *lo = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot + a.a_slot);
-                for (int j = t; j < n16; j += 128) {
-                    const float4 v = ar[j];
-                    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                if (PREC) {
+                    float4 *lo = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot + a.a_slot);
+                    for (int j = t; j < n16; j += 128) {
+                        const float4 v = ar[j];
+                        const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
 #if !SS_TF32_HW_TRUNCATES
-                    ar[j] = h;
+                        ar[j] = h;
 #endif
-                    lo[j] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                        lo[j] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                    }
+                } else {
+                    // fp32 row r (rowb bytes, swizzled) -> bf16 row r (rowb / 2
+                    // bytes, swizzled for that width) in the second half of the slot
+                    uint8_t *bf = aslots + sa * 2 * a.a_slot + a.a_slot;
+                    const int rb = (int)rowb, rb2 = rb / 2, cpr = rb / 16;
+                    for (int j = t; j < n16; j += 128) {
+                        const int r = j / cpr, pc = j - r * cpr;
+                        const int lc = swz_chunk(pc, r, rb);  // logical chunk: channels 4 lc .. 4 lc + 3
+                        const float4 v = ar[j];
+                        const __nv_bfloat162 b01 = __floats2bfloat162_rn(v.x, v.y), b23 = __floats2bfloat162_rn(v.z, v.w);
+                        uint2 q;
+                        q.x = *reinterpret_cast<const uint32_t *>(&b01);
+                        q.y = *reinterpret_cast<const uint32_t *>(&b23);
+                        const int bc = swz_chunk(lc >> 1, r, rb2);
+                        *reinterpret_cast<uint2 *>(bf + r * rb2 + bc * 16 + (lc & 1) * 8) = q;
+                    }
                 }
                 fence_proxy_async();
                 __syncwarp();
@@ -477,10 +532,34 @@ static int amode_for(int k, int stride, int dil, int cin)
     return 0;
 }
 
-int tma_taps_per_stage(int k, int stride, int dil, int cin, int np)
+int tma_taps_per_stage(int k, int stride, int dil, int cin, int np, int prec)
 {
     if (amode_for(k, stride, dil, cin) == 0) return 1;  // im2col: one tap per stage
-    return std::max(1, std::min(k * k, 36864 / (2 * np * 128)));
+    const int tap_bytes = prec ? 2 * np * 128 : np * 64;
+    return std::max(1, std::min(k * k, 36864 / tap_bytes));
+}
+
+// bf16 weight tensor map over [kblocks][rows = parts * np][32] bf16 (64-byte
+// rows, SWIZZLE_64B): per stage one box of 32 K x np rows x T kblocks
+int encode_weight_map_bf16(CUtensorMap *m, const void *wt, int kblocks, int rows, int np, int T)
+{
+    auto fn = tiled_fn();
+    if (!fn) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return SS_CUDA_ERROR;
+    }
+    const cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)kblocks};
+    const cuuint64_t strides[2] = {64, (cuuint64_t)rows * 64};
+    const cuuint32_t box[3] = {32, (cuuint32_t)np, (cuuint32_t)T};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(wt), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (bf16 weights) failed: " + std::to_string((int)r));
+        return SS_CUDA_ERROR;
+    }
+    return SS_OK;
 }
 
 // weight tensor map over [kblocks][rows = parts * 2 np][32] fp32: per stage
@@ -506,17 +585,30 @@ int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, in
     return SS_OK;
 }
 
+using ConvKernel = void (*)(CUtensorMap, CUtensorMap, ConvArgs);
+
+static ConvKernel conv_kernel(int prec, int amode, bool res)
+{
+    static const ConvKernel tab[2][3][2] = {
+        {{k_conv_tc3<0, 0, false>, k_conv_tc3<0, 0, true>},
+         {k_conv_tc3<0, 1, false>, k_conv_tc3<0, 1, true>},
+         {k_conv_tc3<0, 2, false>, k_conv_tc3<0, 2, true>}},
+        {{k_conv_tc3<1, 0, false>, k_conv_tc3<1, 0, true>},
+         {k_conv_tc3<1, 1, false>, k_conv_tc3<1, 1, true>},
+         {k_conv_tc3<1, 2, false>, k_conv_tc3<1, 2, true>}}};
+    return tab[prec][amode][res ? 1 : 0];
+}
+
 int prepare_conv_tma()
 {
     static bool done = false;
     if (done) return SS_OK;
     if (int rc = prepare_flow_kernels()) return rc;
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_conv_tc3<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+    for (int prec = 0; prec < 2; ++prec)
+        for (int am = 0; am < 3; ++am)
+            for (int res = 0; res < 2; ++res)
+                SS_CUDA_TRY(cudaFuncSetAttribute(conv_kernel(prec, am, res != 0),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
     int dev = 0;
     SS_CUDA_TRY(cudaGetDevice(&dev));
     SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm_tma, cudaDevAttrMultiProcessorCount, dev));
@@ -525,7 +617,7 @@ int prepare_conv_tma()
 }
 
 // one output-channel part (rows [part * 2 np, +2 np) of the weight tensor)
-static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int amode, int cpp, int halo_w,
+static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int prec, int amode, int cpp, int halo_w,
                        int halo_h, int part, int np, cudaStream_t st)
 {
     ConvArgs a;
@@ -569,13 +661,13 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int amode, i
     }
     a.nk_all = a.ncb * a.sp_cb;
     a.np = np;
-    a.part_row = part * 2 * np;
+    a.part_row = part * (prec ? 2 : 1) * np;
     a.Cout = std::min(np, p.Cout - part * np);
     a.act = p.act;
     a.out_ld = p.out_ld;
     a.bias = p.bias + part * np;
     a.out = p.out + part * np;
-    a.b_stage = a.T * 2 * np * 128;
+    a.b_stage = prec ? a.T * 2 * np * 128 : a.T * np * 64;  // [hi; lo] fp32 rows | bf16 rows
     const int bar_bytes = 1024 + 512;
     // weights resident for the whole launch when every stage fits
     static const bool res_on = getenv("SS_CONV_BRES") == nullptr || strcmp(getenv("SS_CONV_BRES"), "0");
@@ -608,23 +700,15 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int amode, i
     const int grid = std::min(a.units, n_sm_tma);
     const size_t smem = (size_t)2 * a.na * a.a_slot + (size_t)a.stages * a.b_stage + bar_bytes + a.stages * 16;
     const CUtensorMap &tmB = *static_cast<const CUtensorMap *>(p.tmB);
-    int rc;
-    if (amode == 1)
-        rc = a.b_res ? launch_pdl("k_conv_tc3", k_conv_tc3<1, true>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a)
-                     : launch_pdl("k_conv_tc3", k_conv_tc3<1, false>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a);
-    else if (amode == 2)
-        rc = a.b_res ? launch_pdl("k_conv_tc3", k_conv_tc3<2, true>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a)
-                     : launch_pdl("k_conv_tc3", k_conv_tc3<2, false>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a);
-    else
-        rc = a.b_res ? launch_pdl("k_conv_tc3", k_conv_tc3<0, true>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a)
-                     : launch_pdl("k_conv_tc3", k_conv_tc3<0, false>, dim3(grid), dim3(TM_THREADS), smem, st, tmA, tmB, a);
+    const int rc = launch_pdl("k_conv_tc3", conv_kernel(prec, amode, a.b_res != 0), dim3(grid), dim3(TM_THREADS),
+                              smem, st, tmA, tmB, a);
     if (rc) return rc;
     if (splits > 1)
         return launch_splitk_reduce(p.ws, splits, a.M, np, a.Cout, a.bias, p.act, a.out, p.out_ld, st);
     return SS_OK;
 }
 
-int launch_conv_tma(const ConvParams &p, cudaStream_t st)
+int launch_conv_tma(const ConvParams &p, int prec, cudaStream_t st)
 {
     if (int rc = prepare_conv_tma()) return rc;
     if (!p.tmB) {
@@ -640,14 +724,16 @@ int launch_conv_tma(const ConvParams &p, cudaStream_t st)
         return SS_VALUE_ERROR;
     }
     static const bool wide = getenv("SS_CONV_CPP32") != nullptr;
-    const int cpp = (wide && amode != 2) ? 32 : (p.Cin <= 8 ? 8 : (p.Cin <= 16 ? 16 : 32));
+    // bf16: a K = 16 MMA needs >= 16 channels per row
+    const int cmin = prec ? 8 : 16;
+    const int cpp = (wide && amode != 2) ? 32 : std::max(cmin, p.Cin <= 8 ? 8 : (p.Cin <= 16 ? 16 : 32));
     const int halo_w = HT_W + 2 * p.pad, halo_h = HT_H + 2 * p.pad;
     alignas(64) CUtensorMap tmA;
     if (int rc = encode_act_map(&tmA, p, amode, cpp, halo_w, halo_h)) return rc;
     const int parts = (p.Cout_pad + 127) / 128;
     const int np = p.Cout_pad / parts;
     for (int part = 0; part < parts; ++part)
-        if (int rc = launch_part(p, tmA, amode, cpp, halo_w, halo_h, part, np, st)) return rc;
+        if (int rc = launch_part(p, tmA, prec, amode, cpp, halo_w, halo_h, part, np, st)) return rc;
     return SS_OK;
 }
 
