@@ -318,17 +318,20 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     bf16_peak = float(peaks.get("bf16_tflops_sustained", 1412.7))
     k1_gbs = 130.0 * h * w / (med_blend * 1e-3) / 1e9
+    traffic = _traffic_table()
     solver_line = {
         "kernel": f"k_sgd_tma<{SOLVER_K}> (solver pass = {SOLVER_K} SGD-momentum iterations)",
         "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 2),
-        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": None,
+        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4),
+        "traffic": traffic.get("k_sgd_tma<8> solver pass") if SOLVER_K == 8 else None,
         "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1965 MHz non-FMA op rate "
                        "(MEASURED_PEAKS.json has no FP32 entry)",
         "launch_ms": round(per_pass_ms, 5), "stage_ms": round(med_solve, 4)}
     k1_line = {
         "kernel": "k_presolve (K1 fused warp+weights+blend)", "bound": "hbm",
         "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-        "frac": round(k1_gbs / hbm_peak, 4), "traffic": None, "launch_ms": round(med_blend, 5),
+        "frac": round(k1_gbs / hbm_peak, 4), "traffic": traffic.get("k_presolve K1"),
+        "launch_ms": round(med_blend, 5),
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
     if args.flow in ("constant", "dis"):
         roofline = dict(solver_line, secondary=[k1_line])
@@ -342,10 +345,11 @@ def main():
         # 3xTF32: tf32 runs at half the bf16 rate and each fp32 product is 3 MMAs
         conv_peak = bf16_peak if args.flow == "bf16" else bf16_peak / 6.0
         roofline = {
-            "kernel": "k_conv_tc<%d> est3_1 (1/8-res 3x3 conv, 147 live -> 128 ch, tcgen05/TMEM)"
-                      % (0 if args.flow == "bf16" else 1),
+            "kernel": "k_conv_tc3<%d,1,0> est3_1 (1/8-res 3x3 conv, 147 live -> 128 ch; TMA halo tiles, "
+                      "tcgen05/TMEM, %s)" % ((0, "bf16 operands") if args.flow == "bf16" else (1, "3xTF32")),
             "bound": "tensor", "achieved": round(conv_tf, 2), "peak": round(conv_peak, 1),
-            "unit": "TFLOP/s", "frac": round(conv_tf / conv_peak, 4), "traffic": None,
+            "unit": "TFLOP/s", "frac": round(conv_tf / conv_peak, 4),
+            "traffic": traffic.get("k_conv_tc3 est3_1 " + ("bf16" if args.flow == "bf16" else "fp32")),
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained" if args.flow == "bf16"
                             else "derived: MEASURED_PEAKS bf16 sustained / 2 (tf32 rate) / 3 "
                                  "(3xTF32 MMAs per fp32 product)"),
@@ -453,6 +457,17 @@ def run_e2e(args, L, state, pool, flow, torch, dist):
             "path": "C ABI: ss_session_compute_flow(0) + ss_push_pair(host pinned f32) + "
                     "ss_session_compute_flow(1) + ss_step + ss_output(host pinned)",
             "timer": "host wall clock around K steps, device synchronised at both ends"}
+
+
+def _traffic_table():
+    """DRAM bytes per launch of the roofline kernels, from the committed ncu
+    --set full captures (profiles/r01_traffic.json; tools/profile_round.sh)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            tab = json.load(f)["kernels"]
+    except (OSError, KeyError, ValueError):
+        return {}
+    return {k: v["traffic_bytes"] for k, v in tab.items()}
 
 
 def _check(rc, L):
