@@ -136,9 +136,10 @@ static int session_alloc(ss_session *s)
         SS_CUDA_TRY(cudaMalloc(&s->uv[k], px * 2 * sizeof(float)));
         SS_CUDA_TRY(cudaMalloc(&s->valid[k], px));
     }
-    SS_CUDA_TRY(cudaMalloc(&s->A, px * s->cp * sizeof(float)));
-    SS_CUDA_TRY(cudaMalloc(&s->lapP, px * s->cp * sizeof(float)));
-    SS_CUDA_TRY(cudaMalloc(&s->wc, px * sizeof(float)));
+    // A, dP, w_c in one block (planar solver inputs)
+    SS_CUDA_TRY(cudaMalloc(&s->A, px * (2 * s->cp + 1) * sizeof(float)));
+    s->lapP = s->A + px * s->cp;
+    s->wc = s->lapP + px * s->cp;
     for (auto &e : s->ev) SS_CUDA_TRY(cudaEventCreate(&e));
     for (auto &e : s->fev) SS_CUDA_TRY(cudaEventCreate(&e));
     return s->solver.ensure(s->h, s->w, s->cp, 150) == SS_OK ? SS_OK : SS_NO_MEMORY;
@@ -156,9 +157,7 @@ static void session_free(ss_session *s)
         cudaFree(s->uv[k]);
         cudaFree(s->valid[k]);
     }
-    cudaFree(s->A);
-    cudaFree(s->lapP);
-    cudaFree(s->wc);
+    cudaFree(s->A);  // also lapP, wc
     for (auto &e : s->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : s->fev)
