@@ -72,6 +72,9 @@ typedef struct ss_timing {
 
 /* ---- library ------------------------------------------------------------ */
 SS_API int ss_abi_version(void);
+/* Number of GPU kernels this library has launched in this process (graph
+ * replays count their kernels); a diagnostic for benchmarks. */
+SS_API long long ss_kernel_launches(void);
 SS_API const char *ss_status_string(int status);
 /* Last error text of the calling thread (empty string if none). */
 SS_API const char *ss_last_error(void);

@@ -28,7 +28,7 @@ SS_U8 = 1
 
 # every symbol include/streamstab_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "ss_abi_version", "ss_status_string", "ss_last_error", "ss_init", "ss_params_validate",
+    "ss_abi_version", "ss_kernel_launches", "ss_status_string", "ss_last_error", "ss_init", "ss_params_validate",
     "ss_backward_warp", "ss_occlusion_mask", "ss_warp_weight", "ss_local_blend",
     "ss_adaptive_blend", "ss_consistency_weight", "ss_laplacian", "ss_solve_screened_poisson",
     "ss_session_create", "ss_session_destroy", "ss_session_reset", "ss_push_pair",
@@ -68,6 +68,7 @@ def _declare(L):
     P = ctypes.POINTER
     sig = {
         "ss_abi_version": (i32, []),
+        "ss_kernel_launches": (ctypes.c_longlong, []),
         "ss_status_string": (ctypes.c_char_p, [i32]),
         "ss_last_error": (ctypes.c_char_p, []),
         "ss_init": (i32, [i32]),

@@ -3,6 +3,7 @@
 // (consistency.py:306-413).  The index logic (3-pair ring, consecutive
 // positions, one-frame latency, error texts) follows consistency.py:321-353
 // exactly; the per-frame math is K1 (k_presolve) + K2 (solve_planar).
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -16,6 +17,15 @@
 namespace ss {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+static thread_local bool g_capturing = false;
+
+void count_launches(long n)
+{
+    if (!g_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
+}
+
+void set_capturing(bool on) { g_capturing = on; }
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
@@ -201,6 +211,8 @@ static int copy_frame(ss_session *s, float *dst, const void *src, int c, int dty
 extern "C" {
 
 int ss_abi_version(void) { return SS_ABI_VERSION; }
+
+long long ss_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char *ss_status_string(int status)
 {

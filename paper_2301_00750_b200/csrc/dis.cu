@@ -487,6 +487,11 @@ int Estimator::run(const float *fa, const float *fb, int c, float *uv_out, uint8
         uv = full;
     }
     k_finish<<<blocks_for(n, T), T, 0, st>>>(uv, n, uv_out, valid);
+    // kernels of this call (k_finish counted by SS_LAUNCH_CHECK): luma x2, box
+    // pyramid, per level 4 blur passes + refine + 2 median + densify + 2
+    // uniform (+ a flow resize between levels), final resize
+    count_launches(2 + (opts.downscale > 1 ? 2 : 0) + 2 * (L - 1) + L * 10 + (L - 1) +
+                   (opts.downscale > 1 ? 1 : 0));
     SS_LAUNCH_CHECK("dis");
     return SS_OK;
 }

@@ -275,9 +275,9 @@ int Weights::upload(const float *host, int64_t n)
 Run::~Run()
 {
     for (auto &g : pyr_graphs)
-        if (g.second) cudaGraphExecDestroy(g.second);
+        if (g.second.first) cudaGraphExecDestroy(g.second.first);
     for (auto &g : flow_graphs)
-        if (g.second) cudaGraphExecDestroy(g.second);
+        if (g.second.first) cudaGraphExecDestroy(g.second.first);
     for (void *p : allocs) cudaFree(p);
 }
 
@@ -430,11 +430,15 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
 }
 
 // capture fn(st) into a graph (thread-local capture mode) and instantiate it
+// capture fn(st) into a graph (thread-local capture mode) and instantiate it;
+// *nodes = its kernel count (the launch counter counts them per replay)
 template <class F>
-static int capture(cudaStream_t st, cudaGraphExec_t *exec, F &&fn)
+static int capture(cudaStream_t st, cudaGraphExec_t *exec, long *nodes, F &&fn)
 {
     SS_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    set_capturing(true);
     const int rc = fn();
+    set_capturing(false);
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(st, &g);
     if (rc) {
@@ -442,6 +446,9 @@ static int capture(cudaStream_t st, cudaGraphExec_t *exec, F &&fn)
         return rc;
     }
     if (e != cudaSuccess) return cuda_status(e, "cudaStreamEndCapture");
+    size_t n = 0;
+    cudaGraphGetNodes(g, nullptr, &n);
+    *nodes = (long)n;
     const cudaError_t e2 = cudaGraphInstantiate(exec, g, 0);
     cudaGraphDestroy(g);
     if (e2 != cudaSuccess) return cuda_status(e2, "cudaGraphInstantiate");
@@ -456,11 +463,12 @@ int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st
     int rc;
     if (use_graphs && !prof.on) {
         auto &g = pyr_graphs[std::make_tuple(slot, (const void *)img, c)];
-        if (!g && (rc = capture(st, &g, [&] { return pyramid_impl(slot, img, c, st); }))) {
+        if (!g.first && (rc = capture(st, &g.first, &g.second, [&] { return pyramid_impl(slot, img, c, st); }))) {
             pyr_graphs.erase(std::make_tuple(slot, (const void *)img, c));
             return rc;
         }
-        SS_CUDA_TRY(cudaGraphLaunch(g, st));
+        SS_CUDA_TRY(cudaGraphLaunch(g.first, st));
+        count_launches(g.second);
     } else if ((rc = pyramid_impl(slot, img, c, st))) {
         return rc;
     }
@@ -476,11 +484,12 @@ int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st, int set)
         const auto k = std::make_tuple(a, b, (void *)uv, (void *)valid, set);
         auto &g = flow_graphs[k];
         int rc;
-        if (!g && (rc = capture(st, &g, [&] { return flow_impl(a, b, uv, valid, st); }))) {
+        if (!g.first && (rc = capture(st, &g.first, &g.second, [&] { return flow_impl(a, b, uv, valid, st); }))) {
             flow_graphs.erase(k);
             return rc;
         }
-        SS_CUDA_TRY(cudaGraphLaunch(g, st));
+        SS_CUDA_TRY(cudaGraphLaunch(g.first, st));
+        count_launches(g.second);
         return SS_OK;
     }
     return flow_impl(a, b, uv, valid, st);

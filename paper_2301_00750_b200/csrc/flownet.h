@@ -144,8 +144,9 @@ struct Run {
     // CUDA graphs (sessions: every buffer is fixed per ring slot, so the
     // ~60 launches of a pyramid / flow replay as one graph launch)
     bool use_graphs = false;
-    std::map<std::tuple<int, const void *, int>, cudaGraphExec_t> pyr_graphs;
-    std::map<std::tuple<int, int, void *, void *, int>, cudaGraphExec_t> flow_graphs;
+    // graph and its kernel-node count
+    std::map<std::tuple<int, const void *, int>, std::pair<cudaGraphExec_t, long>> pyr_graphs;
+    std::map<std::tuple<int, int, void *, void *, int>, std::pair<cudaGraphExec_t, long>> flow_graphs;
     ~Run();
     int init(const Weights *w, int h, int w_, int nsets = 1);
     // pyramid of img (h, w, c) into slot (skipped if key matches)

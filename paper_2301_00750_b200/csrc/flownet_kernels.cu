@@ -23,7 +23,12 @@ bool pdl_enabled()
     return on;
 }
 
-int pdl_status(cudaError_t e, const char *what) { return e == cudaSuccess ? SS_OK : cuda_status(e, what); }
+int pdl_status(cudaError_t e, const char *what)
+{
+    if (e != cudaSuccess) return cuda_status(e, what);
+    count_launches(1);
+    return SS_OK;
+}
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred)
 {

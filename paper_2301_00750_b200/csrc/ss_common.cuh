@@ -20,6 +20,11 @@ namespace ss {
 void set_error(const std::string &msg);
 int cuda_status(cudaError_t e, const char *what);
 
+// process-wide count of kernels this library launched (ss_kernel_launches);
+// launches recorded into a graph are counted when the graph is launched
+void count_launches(long n);
+void set_capturing(bool on);  // this thread is capturing a graph
+
 #define SS_CUDA_TRY(expr)                                            \
     do {                                                             \
         cudaError_t _e = (expr);                                     \
@@ -30,6 +35,7 @@ int cuda_status(cudaError_t e, const char *what);
     do {                                                             \
         cudaError_t _e = cudaGetLastError();                         \
         if (_e != cudaSuccess) return ::ss::cuda_status(_e, what);   \
+        ::ss::count_launches(1);                                     \
     } while (0)
 
 __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
