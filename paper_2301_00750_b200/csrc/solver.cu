@@ -279,6 +279,24 @@ __device__ __forceinline__ unsigned blk_tile(float2 (&X)[blk::R], float2 (&Y)[bl
     const bool odd = a.iters & 1;
     const bool interior_c = c0 >= K && c0 + 2 <= RW - K;
     bool nan_seen = false;
+    if (!a.hwc_out && (w & 1) == 0) {
+        // even width: the thread's column pair is wholly inside or outside
+        // the image and 8-byte aligned in the planar outputs -> float2 stores
+        const bool col_ok = interior_c && gx0 + 1 < w;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const float2 o = odd ? Y[r] : X[r];
+            const float2 op = odd ? X[r] : Y[r];
+            nan_seen |= track && (o.x != o.x || o.y != o.y);
+            const int gy = gy0 + r;
+            if (col_ok && r0 + r >= K && r0 + r < RH - K && gy < h) {
+                const long q = (long)gy * w + gx0;
+                *reinterpret_cast<float2 *>(a.Oout + plane + q) = o;
+                *reinterpret_cast<float2 *>(a.Oprev_out + plane + q) = op;
+            }
+        }
+        return nan_seen ? 0x7fffffffu : __float_as_uint(mx);
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int gy = gy0 + r;

@@ -127,3 +127,36 @@ def test_concurrent_flows_bitwise_equal_serial(ss, net, monkeypatch):
     assert sorted(conc) == sorted(serial) == list(range(1, 8))
     for t in conc:
         assert np.array_equal(conc[t], serial[t]), t
+
+
+def test_concurrent_sessions_threads_bitwise(ss, net):
+    """Independent streams on their own CUDA streams, driven from two host
+    threads at once (bench --streams), give exactly the sequential results."""
+    import threading
+
+    import torch
+
+    from paper_2301_00750_b200 import synthetic
+
+    seqs = [synthetic.translating_sequence(frames=5, height=64, width=96, seed=s) for s in (11, 12)]
+
+    def run(seq):
+        return dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"), net))
+
+    want = [run(q) for q in seqs]
+    got = [None, None]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+
+    def worker(k):
+        with torch.cuda.stream(streams[k]):
+            got[k] = run(seqs[k])
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for k in range(2):
+        assert sorted(got[k]) == sorted(want[k])
+        for t in want[k]:
+            assert np.array_equal(got[k][t], want[k][t]), (k, t)
