@@ -284,6 +284,9 @@ def main():
         flush.zero_()  # L2 flush between timed steps, outside the events
         ev[k][0].record(stream)
         step()
+        # the step's end event covers its side-stream work too (the flow the
+        # step started for the next step, overlapping its solver)
+        _check(L.ss_session_join(state.handle), L)
         ev[k][1].record(stream)
         tm = state.last_timing
         flow_ms.append(tm.flow_ms)
@@ -443,6 +446,7 @@ def run_multi(args, torch, dist, rank, world, local, L, ss, flow, pool):
                 ev0[s_].record(streams[s_])
                 for _ in range(args.steps):
                     step(s_)
+                _check(L.ss_session_join(states[s_].handle), L)
                 ev1[s_].record(streams[s_])
         except Exception as e:  # noqa: BLE001
             errors.append(e)

@@ -200,6 +200,10 @@ SS_API int ss_session_compute_flow(ss_session *s, int which);
  * FLOPs (live channels only). */
 SS_API int ss_session_time_conv(ss_session *s, int level, int reps, float *ms, double *flops);
 SS_API void *ss_session_stream(const ss_session *s);
+/* Make the session stream wait for the session's side-stream work (the flow
+ * to the previous frame runs there) -- e.g. before recording an event that
+ * must cover all of a step's work. */
+SS_API int ss_session_join(ss_session *s);
 
 #ifdef __cplusplus
 }

@@ -519,6 +519,8 @@ int ss_session_reset(ss_session *s)
 
 void *ss_session_stream(const ss_session *s) { return (void *)s->stream; }
 
+int ss_session_join(ss_session *s) { return join_side(s); }
+
 int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, int dtype,
                  int where)
 {
