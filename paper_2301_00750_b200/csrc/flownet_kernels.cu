@@ -185,42 +185,64 @@ int launch_conv_ffma(const ConvParams &p, cudaStream_t st)
 }
 
 // ---------------------------------------------------------------------------
-// depthwise 3x3 (dilated), NHWC, zero padding, no bias / activation
-__global__ void k_depthwise(const float *__restrict__ in, int ld, int H, int W, int C,
-                            const float *__restrict__ w, int dil, float *__restrict__ out,
-                            int ld_out)
+// depthwise 3x3 (dilated), NHWC, zero padding, no bias / activation.
+// A thread owns 4 channels x DW_PX horizontally adjacent pixels: its 9 weight
+// float4 stay in registers, and all 9 x DW_PX input loads of a row are issued
+// before the FMAs (memory-level parallelism; neighbours hit L1).
+constexpr int DW_PX = 4;
+
+__global__ void __launch_bounds__(256) k_depthwise(const float *__restrict__ in, int ld, int H, int W, int C,
+                                                  const float *__restrict__ w, int dil, float *__restrict__ out,
+                                                  int ld_out)
 {
     pdl_wait();
-    const int C4 = C / 4;
+    const int C4 = C / 4, WG = (W + DW_PX - 1) / DW_PX;
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (long)H * W * C4) return;
+    if (i >= (long)H * WG * C4) return;
     const int c = (int)(i % C4) * 4;
-    const long pix = i / C4;
-    const int y = (int)(pix / W), x = (int)(pix - (long)y * W);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const long g = i / C4;
+    const int y = (int)(g / WG), x0 = (int)(g - (long)y * WG) * DW_PX;
+    float4 k[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) k[t] = __ldg(reinterpret_cast<const float4 *>(w + t * C + c));
+    float4 acc[DW_PX];
+#pragma unroll
+    for (int p = 0; p < DW_PX; ++p) acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int ky = 0; ky < 3; ++ky) {
         const int iy = y + (ky - 1) * dil;
         if (iy < 0 || iy >= H) continue;
+        const float *row = in + (long)iy * W * ld + c;
+        float4 v[3][DW_PX];
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+            for (int p = 0; p < DW_PX; ++p) {
+                const int ix = x0 + p + (kx - 1) * dil;
+                v[kx][p] = (ix >= 0 && ix < W) ? __ldg(reinterpret_cast<const float4 *>(row + (long)ix * ld))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
 #pragma unroll
         for (int kx = 0; kx < 3; ++kx) {
-            const int ix = x + (kx - 1) * dil;
-            if (ix < 0 || ix >= W) continue;
-            const float4 v = *reinterpret_cast<const float4 *>(in + ((long)iy * W + ix) * ld + c);
-            const float4 k = *reinterpret_cast<const float4 *>(w + (ky * 3 + kx) * C + c);
-            acc.x = fmaf(v.x, k.x, acc.x);
-            acc.y = fmaf(v.y, k.y, acc.y);
-            acc.z = fmaf(v.z, k.z, acc.z);
-            acc.w = fmaf(v.w, k.w, acc.w);
+            const float4 kk = k[ky * 3 + kx];
+#pragma unroll
+            for (int p = 0; p < DW_PX; ++p) {
+                acc[p].x = fmaf(v[kx][p].x, kk.x, acc[p].x);
+                acc[p].y = fmaf(v[kx][p].y, kk.y, acc[p].y);
+                acc[p].z = fmaf(v[kx][p].z, kk.z, acc[p].z);
+                acc[p].w = fmaf(v[kx][p].w, kk.w, acc[p].w);
+            }
         }
     }
-    *reinterpret_cast<float4 *>(out + pix * ld_out + c) = acc;
+#pragma unroll
+    for (int p = 0; p < DW_PX; ++p)
+        if (x0 + p < W) *reinterpret_cast<float4 *>(out + ((long)y * W + x0 + p) * ld_out + c) = acc[p];
 }
 
 int launch_depthwise(const float *in, int ld, int H, int W, int C, const float *w, int dil,
                      float *out, int ld_out, cudaStream_t st)
 {
-    const long n = (long)H * W * (C / 4);
+    const long n = (long)H * ((W + DW_PX - 1) / DW_PX) * (C / 4);
     return launch_pdl("k_depthwise", k_depthwise, dim3(blocks_for(n, 256)), dim3(256), 0, st, in, ld, H, W, C,
                       w, dil, out, ld_out);
 }
