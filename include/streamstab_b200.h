@@ -149,6 +149,12 @@ SS_API int ss_session_reset(ss_session *s);
 SS_API int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, int dtype,
                  int where);
 /* Position the next step will solve (solved_through + 1) and the state. */
+/* Stage the next (I, P) pair: its host->device copy runs on a copy stream
+ * while the session computes; a later ss_push_pair with the same position and
+ * the same I / P pointers swaps the staged buffers into the ring instead of
+ * copying.  float32 only; the host buffers must stay valid until that push. */
+SS_API int ss_stage_pair(ss_session *s, int64_t position, const void *I, const void *P, int dtype,
+                         int where);
 SS_API int64_t ss_solved_through(const ss_session *s);
 SS_API int ss_pending(const ss_session *s, int64_t *t, int *has_prev, int *has_next);
 /* Provide the flows for the pending step t: which = 0 -> flow t->t-1,
@@ -169,6 +175,13 @@ SS_API int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_it
 SS_API int ss_output(const ss_session *s, void *dst, int dtype, int where);
 /* Device pointer of the current output (H, W, c_proc) float32; valid until
  * the next ss_step / ss_push_pair. */
+/* Asynchronous output: enqueue the copy of O_t (as ss_output) on a copy
+ * stream and return; it overlaps the next step (the next solver that would
+ * overwrite O_t's buffer waits for it).  dst must stay valid until
+ * ss_output_wait returns or the next ss_output_async call (which waits for
+ * the previous copy first). */
+SS_API int ss_output_async(ss_session *s, void *dst, int dtype, int where);
+SS_API int ss_output_wait(ss_session *s);
 SS_API const float *ss_output_device(const ss_session *s);
 SS_API int ss_last_timing(const ss_session *s, ss_timing *t);
 /* Copy the flows used by the last step (for feeding back into the

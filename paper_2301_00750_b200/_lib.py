@@ -31,9 +31,9 @@ EXPORTS = (
     "ss_abi_version", "ss_kernel_launches", "ss_status_string", "ss_last_error", "ss_init", "ss_params_validate",
     "ss_backward_warp", "ss_occlusion_mask", "ss_warp_weight", "ss_local_blend",
     "ss_adaptive_blend", "ss_consistency_weight", "ss_laplacian", "ss_solve_screened_poisson",
-    "ss_session_create", "ss_session_destroy", "ss_session_reset", "ss_push_pair",
+    "ss_session_create", "ss_session_destroy", "ss_session_reset", "ss_push_pair", "ss_stage_pair",
     "ss_solved_through", "ss_pending", "ss_set_flow", "ss_set_constant_flow", "ss_check_step",
-    "ss_step", "ss_output", "ss_output_device", "ss_last_timing", "ss_flows",
+    "ss_step", "ss_output", "ss_output_async", "ss_output_wait", "ss_output_device", "ss_last_timing", "ss_flows",
     "ss_session_stream", "ss_session_join", "ss_flownet_num_params", "ss_flownet_create", "ss_flownet_destroy",
     "ss_flownet_flow", "ss_session_attach_flownet", "ss_session_compute_flow",
     "ss_warping_error_sums", "ss_ssim", "ss_session_time_conv", "ss_dis_flow",
@@ -86,6 +86,7 @@ def _declare(L):
         "ss_session_destroy": (i32, [vp]),
         "ss_session_reset": (i32, [vp]),
         "ss_push_pair": (i32, [vp, i64, vp, vp, i32, i32]),
+        "ss_stage_pair": (i32, [vp, i64, vp, vp, i32, i32]),
         "ss_solved_through": (i64, [vp]),
         "ss_pending": (i32, [vp, P(i64), P(i32), P(i32)]),
         "ss_set_flow": (i32, [vp, i32, vp, vp, i32]),
@@ -93,6 +94,8 @@ def _declare(L):
         "ss_check_step": (i32, [vp, i32, P(i64)]),
         "ss_step": (i32, [vp, i32, P(SSParams), P(i32)]),
         "ss_output": (i32, [vp, vp, i32, i32]),
+        "ss_output_async": (i32, [vp, vp, i32, i32]),
+        "ss_output_wait": (i32, [vp]),
         "ss_output_device": (vp, [vp]),
         "ss_last_timing": (i32, [vp, P(SSTiming)]),
         "ss_flows": (i32, [vp, i32, vp, vp, i32]),

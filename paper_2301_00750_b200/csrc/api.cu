@@ -8,6 +8,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <utility>
 
 #include "dis.h"
 #include "flownet.h"
@@ -114,6 +115,20 @@ struct ss_session {
     cudaEvent_t fork = nullptr, join = nullptr;
     bool side_pending = false;
     int side_slots[2] = {-1, -1};  // ring slots whose pyramids the side flow reads
+    // asynchronous output (ss_output_async): device->host copy on its own
+    // stream, overlapping the next step; the solver that would next overwrite
+    // the copied buffer waits for it
+    cudaStream_t copy = nullptr;
+    cudaEvent_t out_src = nullptr, out_done = nullptr;
+    bool out_pending = false;
+    uint8_t *out_u8 = nullptr;
+    // input staging (ss_stage_pair): the next pair's host->device copy runs on
+    // the copy stream while the current step computes; ss_push_pair of that
+    // pair then swaps the staged buffers into the ring (no copy)
+    float *stI = nullptr, *stP = nullptr;
+    const void *st_hostI = nullptr, *st_hostP = nullptr;
+    int64_t staged_pos = -1;
+    cudaEvent_t st_src = nullptr, st_done = nullptr;
     std::unique_ptr<dis::Estimator> dis;  // built-in flow (BuiltinFlow)
 };
 
@@ -178,6 +193,17 @@ static void session_free(ss_session *s)
     }
     if (s->fork) cudaEventDestroy(s->fork);
     if (s->join) cudaEventDestroy(s->join);
+    if (s->copy) {
+        cudaStreamSynchronize(s->copy);
+        cudaStreamDestroy(s->copy);
+    }
+    if (s->out_src) cudaEventDestroy(s->out_src);
+    if (s->out_done) cudaEventDestroy(s->out_done);
+    cudaFree(s->out_u8);
+    if (s->st_src) cudaEventDestroy(s->st_src);
+    if (s->st_done) cudaEventDestroy(s->st_done);
+    cudaFree(s->stI);
+    cudaFree(s->stP);
     s->run.reset();
     s->dis.reset();
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
@@ -471,6 +497,7 @@ int ss_session_create(int h, int w, int c_in, int c_proc, void *stream, ss_sessi
     s->ci = c_in;
     s->cp = c_proc;
     s->n_pairs = 0;
+    s->staged_pos = -1;
     s->has_output = false;
     s->solved_through = 0;
     s->flow_for[0] = s->flow_for[1] = -1;
@@ -552,8 +579,16 @@ int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, 
     if (idx == s->side_slots[0] || idx == s->side_slots[1])
         if (int rc = join_side(s)) return rc;
     if (s->run) s->run->slots[idx].key = -1;  // the frame's cached pyramid is stale
-    if (int rc = copy_frame(s, sl.I, I, s->ci, dtype, where)) return rc;
-    if (int rc = copy_frame(s, sl.P, P, s->cp, dtype, where)) return rc;
+    if (s->staged_pos == position && I == s->st_hostI && P == s->st_hostP && dtype == SS_F32) {
+        // staged by ss_stage_pair: swap its buffers into the ring once copied
+        SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->st_done, 0));
+        std::swap(sl.I, s->stI);
+        std::swap(sl.P, s->stP);
+        s->staged_pos = -1;
+    } else {
+        if (int rc = copy_frame(s, sl.I, I, s->ci, dtype, where)) return rc;
+        if (int rc = copy_frame(s, sl.P, P, s->cp, dtype, where)) return rc;
+    }
     sl.pos = position;
     if (!s->has_output) {  // :338-340 (prev_output = first processed frame)
         SS_CUDA_TRY(cudaMemcpyAsync(s->O, sl.P, (size_t)s->h * s->w * s->cp * sizeof(float),
@@ -561,6 +596,39 @@ int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, 
         s->has_output = true;
         s->solved_through = position;
     }
+    return SS_OK;
+}
+
+int ss_stage_pair(ss_session *s, int64_t position, const void *I, const void *P, int dtype, int where)
+{
+    if (dtype != SS_F32) {
+        set_error("ss_stage_pair stages float32 frames");
+        return SS_VALUE_ERROR;
+    }
+    const size_t px = (size_t)s->h * s->w;
+    if (!s->copy) {
+        SS_CUDA_TRY(cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking));
+        SS_CUDA_TRY(cudaEventCreateWithFlags(&s->out_src, cudaEventDisableTiming));
+        SS_CUDA_TRY(cudaEventCreateWithFlags(&s->out_done, cudaEventDisableTiming));
+    }
+    if (!s->stI) {
+        SS_CUDA_TRY(cudaMalloc(&s->stI, px * s->ci * sizeof(float)));
+        SS_CUDA_TRY(cudaMalloc(&s->stP, px * s->cp * sizeof(float)));
+        SS_CUDA_TRY(cudaEventCreateWithFlags(&s->st_src, cudaEventDisableTiming));
+        SS_CUDA_TRY(cudaEventCreateWithFlags(&s->st_done, cudaEventDisableTiming));
+    }
+    if (s->staged_pos >= 0) SS_CUDA_TRY(cudaEventSynchronize(s->st_done));  // unconsumed: overwrite
+    // the staging buffers were a ring slot until the last push: order the copy
+    // after session work issued so far
+    SS_CUDA_TRY(cudaEventRecord(s->st_src, s->stream));
+    SS_CUDA_TRY(cudaStreamWaitEvent(s->copy, s->st_src, 0));
+    const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    SS_CUDA_TRY(cudaMemcpyAsync(s->stI, I, px * s->ci * sizeof(float), kind, s->copy));
+    SS_CUDA_TRY(cudaMemcpyAsync(s->stP, P, px * s->cp * sizeof(float), kind, s->copy));
+    SS_CUDA_TRY(cudaEventRecord(s->st_done, s->copy));
+    s->staged_pos = position;
+    s->st_hostI = I;
+    s->st_hostP = P;
     return SS_OK;
 }
 
@@ -658,6 +726,9 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
     }
     if (int rc = join_side(s)) return rc;
     s->side_pending = false;
+    // an asynchronous output copy of O_new's buffer (two steps old) must finish
+    // before this step's solver overwrites it
+    if (s->out_pending) SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->out_done, 0));
     SS_CUDA_TRY(cudaEventRecord(s->ev[0], s->stream));
     PresolveArgs a;
     a.h = s->h;
@@ -722,6 +793,45 @@ int ss_output(const ss_session *s, void *dst, int dtype, int where)
         return SS_VALUE_ERROR;
     }
     SS_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return SS_OK;
+}
+
+int ss_output_async(ss_session *s, void *dst, int dtype, int where)
+{
+    if (!s->has_output) {
+        set_error("no buffered frames");
+        return SS_VALUE_ERROR;
+    }
+    if (dtype != SS_F32 && dtype != SS_U8) {
+        set_error("unsupported dtype");
+        return SS_VALUE_ERROR;
+    }
+    const size_t n = (size_t)s->h * s->w * s->cp;
+    if (!s->copy) {
+        SS_CUDA_TRY(cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking));
+        SS_CUDA_TRY(cudaEventCreateWithFlags(&s->out_src, cudaEventDisableTiming));
+        SS_CUDA_TRY(cudaEventCreateWithFlags(&s->out_done, cudaEventDisableTiming));
+    }
+    if (s->out_pending) SS_CUDA_TRY(cudaEventSynchronize(s->out_done));  // one copy in flight
+    const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const void *src = s->O;
+    if (dtype == SS_U8) {
+        if (!s->out_u8) SS_CUDA_TRY(cudaMalloc(&s->out_u8, n));
+        k_f32_to_u8<<<blocks_for((long)n, 256), 256, 0, s->stream>>>(s->O, (long)n, s->out_u8);
+        SS_LAUNCH_CHECK("k_f32_to_u8");
+        src = s->out_u8;
+    }
+    SS_CUDA_TRY(cudaEventRecord(s->out_src, s->stream));
+    SS_CUDA_TRY(cudaStreamWaitEvent(s->copy, s->out_src, 0));
+    SS_CUDA_TRY(cudaMemcpyAsync(dst, src, n * (dtype == SS_F32 ? sizeof(float) : 1), kind, s->copy));
+    SS_CUDA_TRY(cudaEventRecord(s->out_done, s->copy));
+    s->out_pending = true;
+    return SS_OK;
+}
+
+int ss_output_wait(ss_session *s)
+{
+    if (s->out_pending) SS_CUDA_TRY(cudaEventSynchronize(s->out_done));
     return SS_OK;
 }
 

@@ -1,0 +1,110 @@
+"""Session I/O paths of the C ABI on the GPU: asynchronous output
+(ss_output_async / ss_output_wait) returns exactly what ss_output returns,
+for f32 and u8, while later steps run; the launch counter advances."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2301_00750_b200 import _lib
+
+    L = _lib.lib()
+    assert L.ss_init(0) == 0
+    return _lib, L
+
+
+def _params(_lib):
+    from paper_2301_00750_b200._dev import params_struct
+    from paper_2301_00750_b200.consistency import ConsistencyParams
+
+    return params_struct(ConsistencyParams(iterations=20))
+
+
+def test_output_async_matches_sync(lib):
+    _lib, L = lib
+    h, w = 48, 64
+    rng = np.random.default_rng(3)
+    frames = [rng.random((h, w, 3), dtype=np.float32) for _ in range(5)]
+    sess = ctypes.c_void_p()
+    assert L.ss_session_create(h, w, 3, 3, None, ctypes.byref(sess)) == 0
+    n0 = L.ss_kernel_launches()
+    prm = _params(_lib)
+    it = ctypes.c_int(0)
+    try:
+        for pos in (1, 2):
+            f = frames[pos - 1]
+            assert L.ss_push_pair(sess, pos, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+        pending = []
+        for pos in (3, 4, 5):
+            f = frames[pos - 1]
+            assert L.ss_push_pair(sess, pos, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+            assert L.ss_set_constant_flow(sess, 0, 1.0, 0.0, -1) == 0
+            assert L.ss_set_constant_flow(sess, 1, 1.0, 0.0, 1) == 0
+            assert L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)) == 0
+            want = np.empty((h, w, 3), np.float32)
+            assert L.ss_output(sess, want.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+            want8 = np.empty((h, w, 3), np.uint8)
+            assert L.ss_output(sess, want8.ctypes.data, _lib.SS_U8, _lib.SS_HOST) == 0
+            got = np.full((h, w, 3), np.nan, np.float32)
+            assert L.ss_output_async(sess, got.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+            pending.append((got, want))
+            assert L.ss_output_wait(sess) == 0
+            got8 = np.zeros((h, w, 3), np.uint8)
+            assert L.ss_output_async(sess, got8.ctypes.data, _lib.SS_U8, _lib.SS_HOST) == 0
+            assert L.ss_output_wait(sess) == 0
+            assert np.array_equal(got8, want8)
+        for got, want in pending:
+            assert np.array_equal(got, want)
+    finally:
+        L.ss_session_destroy(sess)
+    assert L.ss_kernel_launches() > n0
+
+
+def test_stage_pair_matches_push(lib):
+    """A pair staged with ss_stage_pair and then pushed gives bit-identical
+    steps to plain pushes (and a mismatched push still copies)."""
+    _lib, L = lib
+    h, w = 40, 56
+    rng = np.random.default_rng(5)
+    frames = [np.ascontiguousarray(rng.random((h, w, 3), dtype=np.float32)) for _ in range(6)]
+    prm = _params(_lib)
+
+    def run(stage):
+        sess = ctypes.c_void_p()
+        assert L.ss_session_create(h, w, 3, 3, None, ctypes.byref(sess)) == 0
+        outs = []
+        it = ctypes.c_int(0)
+        try:
+            for pos in range(1, 7):
+                f = frames[pos - 1]
+                assert L.ss_push_pair(sess, pos, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+                if stage and pos < 6:
+                    g = frames[pos]
+                    # stage the next pair; pos 3 stages a different pointer than it pushes
+                    src = g if pos != 3 else g.copy()
+                    assert L.ss_stage_pair(sess, pos + 1, src.ctypes.data, src.ctypes.data, _lib.SS_F32,
+                                           _lib.SS_HOST) == 0
+                if pos >= 3:
+                    assert L.ss_set_constant_flow(sess, 0, 1.0, 1.0, -1) == 0
+                    assert L.ss_set_constant_flow(sess, 1, 1.0, 1.0, 1) == 0
+                    assert L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)) == 0
+                    o = np.empty((h, w, 3), np.float32)
+                    assert L.ss_output(sess, o.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+                    outs.append(o)
+        finally:
+            L.ss_session_destroy(sess)
+        return outs
+
+    a, b = run(False), run(True)
+    assert len(a) == len(b) == 4
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
