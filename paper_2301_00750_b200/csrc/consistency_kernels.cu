@@ -170,25 +170,17 @@ __global__ void k_hwc_to_planar(const float *__restrict__ src, long hw, float *_
 // with f_next), the two warp weights, local / adaptive / input blends, the
 // consistency weight, and the Laplacian of P_t.  Writes the solver inputs in
 // the solver's planar layout: A[c][y][x], lapP[c][y][x], wc[y][x].
+// The per-pixel body: Ic / Pc are the pixel's I_t / P_t, fp / fn its flows,
+// vp / vn their validity; returns A[CP], w_c and the Laplacian of P_t.
 template <int CI, int CP, bool NEXT>
-__global__ void __launch_bounds__(256) k_presolve(PresolveArgs a)
+__device__ __forceinline__ void presolve_px(const PresolveArgs &a, long i, int y, int x, const float (&Ic)[CI],
+                                            const float (&Pc)[CP], float2 fp, bool vp, float2 fn, bool vn,
+                                            float (&Aout)[CP], float &wcv, float (&lap)[CP], float &wp_, float &wn_)
 {
-    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const int h = a.h, w = a.w;
-    const long hw = (long)h * w;
-    if (i >= hw) return;
-    const int y = (int)(i / w), x = (int)(i - (long)y * w);
-
-    float Ic[CI], Pc[CP];
-#pragma unroll
-    for (int k = 0; k < CI; ++k) Ic[k] = __ldg(a.I_cur + i * CI + k);
-#pragma unroll
-    for (int k = 0; k < CP; ++k) Pc[k] = __ldg(a.P_cur + i * CP + k);
-
     // ---- previous frame: consistency.py:387-389, :401
-    const float2 fp = __ldg(reinterpret_cast<const float2 *>(a.uv_prev) + i);
     float ys = fadd((float)y, fp.y), xs = fadd((float)x, fp.x);
-    const bool mp = inside(ys, xs, h, w) && (a.valid_prev == nullptr || a.valid_prev[i]);
+    const bool mp = inside(ys, xs, h, w) && vp;
     Taps tp = make_taps(ys, xs, h, w);
     float wIp[CI], wPp[CP], G[CP];
     gather<CI>(a.I_prev, tp, wIp);
@@ -201,10 +193,9 @@ __global__ void __launch_bounds__(256) k_presolve(PresolveArgs a)
     // ---- next frame: consistency.py:391-398
     float wIn[CI], wPn[CP], wn;
     if (NEXT) {
-        const float2 fn = __ldg(reinterpret_cast<const float2 *>(a.uv_next) + i);
         ys = fadd((float)y, fn.y);
         xs = fadd((float)x, fn.x);
-        const bool mn = inside(ys, xs, h, w) && (a.valid_next == nullptr || a.valid_next[i]);
+        const bool mn = inside(ys, xs, h, w) && vn;
         Taps tn = make_taps(ys, xs, h, w);
         gather<CI>(a.I_next, tn, wIn);
         gather<CP>(a.P_next, tn, wPn);
@@ -224,15 +215,15 @@ __global__ void __launch_bounds__(256) k_presolve(PresolveArgs a)
 #pragma unroll
     for (int k = 0; k < CP; ++k) {
         const float L = fadd(fadd(fmul(om, Pc[k]), fmul(wp, wPp[k])), fmul(wn, wPn[k]));
-        a.A[k * hw + i] = fadd(fmul(wp, G[k]), fmul(omp, L));
+        Aout[k] = fadd(fmul(wp, G[k]), fmul(omp, L));
     }
     float AI[CI];
 #pragma unroll
     for (int k = 0; k < CI; ++k)
         AI[k] = fadd(fadd(fmul(om, Ic[k]), fmul(wp, wIp[k])), fmul(wn, wIn[k]));
-    a.wc[i] = fmul(a.p.lam, expf(fmul(na, sq_dist<CI>(Ic, AI))));
+    wcv = fmul(a.p.lam, expf(fmul(na, sq_dist<CI>(Ic, AI))));
 
-    // ---- Laplacian of P_t (consistency.py:269, :211-221), planar
+    // ---- Laplacian of P_t (consistency.py:269, :211-221)
     const long up = y > 0 ? i - w : i, dn = y < h - 1 ? i + w : i;
     const long lf = x > 0 ? i - 1 : i, rt = x < w - 1 ? i + 1 : i;
 #pragma unroll
@@ -242,8 +233,37 @@ __global__ void __launch_bounds__(256) k_presolve(PresolveArgs a)
         v = fadd(v, __ldg(a.P_cur + dn * CP + k));
         v = fadd(v, __ldg(a.P_cur + lf * CP + k));
         v = fadd(v, __ldg(a.P_cur + rt * CP + k));
-        a.lapP[k * hw + i] = v;
+        lap[k] = v;
     }
+    wp_ = wp;
+    wn_ = wn;
+}
+
+template <int CI, int CP, bool NEXT>
+__global__ void __launch_bounds__(256) k_presolve(PresolveArgs a)
+{
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int h = a.h, w = a.w;
+    const long hw = (long)h * w;
+    if (i >= hw) return;
+    const int y = (int)(i / w), x = (int)(i - (long)y * w);
+    float Ic[CI], Pc[CP];
+#pragma unroll
+    for (int k = 0; k < CI; ++k) Ic[k] = __ldg(a.I_cur + i * CI + k);
+#pragma unroll
+    for (int k = 0; k < CP; ++k) Pc[k] = __ldg(a.P_cur + i * CP + k);
+    const float2 fp = __ldg(reinterpret_cast<const float2 *>(a.uv_prev) + i);
+    const float2 fn = NEXT ? __ldg(reinterpret_cast<const float2 *>(a.uv_next) + i) : make_float2(0.f, 0.f);
+    const bool vp = a.valid_prev == nullptr || a.valid_prev[i];
+    const bool vn = !NEXT || a.valid_next == nullptr || a.valid_next[i];
+    float A[CP], wcv, lap[CP], wp, wn;
+    presolve_px<CI, CP, NEXT>(a, i, y, x, Ic, Pc, fp, vp, fn, vn, A, wcv, lap, wp, wn);
+#pragma unroll
+    for (int k = 0; k < CP; ++k) {
+        a.A[k * hw + i] = A[k];
+        a.lapP[k * hw + i] = lap[k];
+    }
+    a.wc[i] = wcv;
     if (a.wp_out) a.wp_out[i] = wp;
     if (a.wn_out) a.wn_out[i] = wn;
 }
