@@ -178,27 +178,33 @@ __device__ __forceinline__ void presolve_px(const PresolveArgs &a, long i, int y
                                             float (&Aout)[CP], float &wcv, float (&lap)[CP], float &wp_, float &wn_)
 {
     const int h = a.h, w = a.w;
+    // both directions' tap sets first, then every gather (prev: I, P, O; next:
+    // I, P), then the math -- all the dependent loads are in flight together
+    const float ysp = fadd((float)y, fp.y), xsp = fadd((float)x, fp.x);
+    const bool mp = inside(ysp, xsp, h, w) && vp;
+    const Taps tp = make_taps(ysp, xsp, h, w);
+    bool mn = false;
+    Taps tn = tp;
+    if (NEXT) {
+        const float ysn = fadd((float)y, fn.y), xsn = fadd((float)x, fn.x);
+        mn = inside(ysn, xsn, h, w) && vn;
+        tn = make_taps(ysn, xsn, h, w);
+    }
     // ---- previous frame: consistency.py:387-389, :401
-    float ys = fadd((float)y, fp.y), xs = fadd((float)x, fp.x);
-    const bool mp = inside(ys, xs, h, w) && vp;
-    Taps tp = make_taps(ys, xs, h, w);
     float wIp[CI], wPp[CP], G[CP];
     gather<CI>(a.I_prev, tp, wIp);
     gather<CP>(a.P_prev, tp, wPp);
     gather<CP>(a.O_prev, tp, G);
-    const float na = -a.p.alpha;
-    float wp = fminf(a.p.k1, expf(fmul(na, sq_dist<CI>(Ic, wIp))));
-    wp = fmul(wp, mp ? 1.0f : 0.0f);
-
     // ---- next frame: consistency.py:391-398
     float wIn[CI], wPn[CP], wn;
     if (NEXT) {
-        ys = fadd((float)y, fn.y);
-        xs = fadd((float)x, fn.x);
-        const bool mn = inside(ys, xs, h, w) && vn;
-        Taps tn = make_taps(ys, xs, h, w);
         gather<CI>(a.I_next, tn, wIn);
         gather<CP>(a.P_next, tn, wPn);
+    }
+    const float na = -a.p.alpha;
+    float wp = fminf(a.p.k1, expf(fmul(na, sq_dist<CI>(Ic, wIp))));
+    wp = fmul(wp, mp ? 1.0f : 0.0f);
+    if (NEXT) {
         wn = fminf(a.p.k2, expf(fmul(na, sq_dist<CI>(Ic, wIn))));
         wn = fmul(wn, mn ? 1.0f : 0.0f);
     } else {
