@@ -356,15 +356,19 @@ int launch_up2_warp(const float *coarse, int cld, int Hc, int Wc, const float *f
 constexpr int CR_TW = 16, CR_TH = 8, CR_CK = 16, CR_HALO = 4;
 constexpr int CR_PX = CR_CK + 4;                          // floats per staged pixel
 constexpr int CR_WW = CR_TW + 2 * CR_HALO;                // 24 w2 columns
-constexpr int CR_WR = CR_TH + 2;                          // w2 rows per dy group
+constexpr int CR_WR = CR_TH + 2;                          // w2 rows per dy group (of 3)
 constexpr int CR_W2P = CR_WW * CR_PX + 4;                 // w2 row pitch (odd # of 16 B)
 constexpr int CR_F1P = CR_TW * CR_PX + 4;                 // f1 row pitch
 constexpr int CR_W2F = CR_WR * CR_W2P, CR_F1F = CR_TH * CR_F1P;
 
+// DY dy rows per CTA (grid z = 9 / DY): 3 for the fine level, 1 for the
+// coarse ones (three times the CTAs where the image alone gives too few)
+template <int DY>
 __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const float *__restrict__ w2,
                                              int C, int H, int W, float *__restrict__ x, int xld,
                                              int copy_f1)
 {
+    constexpr int WR = CR_TH + DY - 1;  // w2 rows staged
     pdl_wait();
     extern __shared__ __align__(16) float cr_smem[];
     float(*sw)[CR_W2F] = reinterpret_cast<float(*)[CR_W2F]>(cr_smem);
@@ -372,11 +376,11 @@ __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const
     const int t = threadIdx.x;
     const int ty = t & 7, cx = (t >> 3) * 2;  // tile row, first of 2 columns
     const int bx = blockIdx.x * CR_TW, by = blockIdx.y * CR_TH;
-    const int dy0 = (int)blockIdx.z * 3 - CR_HALO;  // dy rows dy0 .. dy0 + 2
+    const int dy0 = (int)blockIdx.z * DY - CR_HALO;  // dy rows dy0 .. dy0 + DY - 1
 
     auto load = [&](int buf, int c0) {
-        // w2: CR_WR rows x 24 columns x 4 float4
-        for (int i = t; i < CR_WR * CR_WW * 4; i += 64) {
+        // w2: WR rows x 24 columns x 4 float4
+        for (int i = t; i < WR * CR_WW * 4; i += 64) {
             const int q = i & 3, px = (i >> 2) % CR_WW, r = (i >> 2) / CR_WW;
             const int gy = by + r + dy0, gx = bx - CR_HALO + px;
             const bool ok = gy >= 0 && gy < H && gx >= 0 && gx < W;
@@ -393,11 +397,11 @@ __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const
         cp_async_commit();
     };
 
-    float acc[2][3][9];
+    float acc[2][DY][9];
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < DY; ++j)
 #pragma unroll
             for (int d = 0; d < 9; ++d) acc[p][j][d] = 0.f;
 
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const
             cp_async_wait<0>();
         }
         __syncthreads();
-        if (copy_f1 && blockIdx.z == 1) {  // f1 -> x[:, 96 + c], one dy group does it
+        if (copy_f1 && (int)blockIdx.z == 4 / DY) {  // f1 -> x[:, 96 + c], one dy group does it
             for (int i = t; i < CR_TH * CR_TW * 4; i += 64) {
                 const int q = i & 3, px = (i >> 2) % CR_TW, r = (i >> 2) / CR_TW;
                 const int gy = by + r, gx = bx + px;
@@ -428,7 +432,7 @@ __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const
             const float4 a0 = *reinterpret_cast<const float4 *>(a + c);
             const float4 a1 = *reinterpret_cast<const float4 *>(a + CR_PX + c);
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
+            for (int j = 0; j < DY; ++j) {
                 float4 b[10];
 #pragma unroll
                 for (int d = 0; d < 10; ++d) b[d] = *reinterpret_cast<const float4 *>(w + j * CR_W2P + d * CR_PX + c);
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const
         if (y >= H || xx >= W) continue;
         float *dst = x + ((long)y * W + xx) * xld + (dy0 + CR_HALO) * 9;
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < DY; ++j)
 #pragma unroll
             for (int d = 0; d < 9; ++d) dst[j * 9 + d] = leaky(acc[p][j][d] * inv);
     }
@@ -461,7 +465,9 @@ int prepare_flow_kernels()
 {
     static bool done = false;
     if (done) return SS_OK;
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(2 * (CR_W2F + CR_F1F) * sizeof(float))));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(2 * (CR_W2F + CR_F1F) * sizeof(float))));
     done = true;
     return SS_OK;
@@ -474,10 +480,15 @@ int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x,
         set_error("correlation needs C % 16 == 0");
         return SS_VALUE_ERROR;
     }
-    const dim3 grid((W + CR_TW - 1) / CR_TW, (H + CR_TH - 1) / CR_TH, 3);
-    const size_t smem = 2 * (CR_W2F + CR_F1F) * sizeof(float);
+    const size_t smem = 2 * (CR_W2F + CR_F1F) * sizeof(float);  // sized for DY = 3
     if (int rc = prepare_flow_kernels()) return rc;
-    return launch_pdl("k_corr", k_corr, grid, dim3(64), smem, st, f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
+    const int tiles = ((W + CR_TW - 1) / CR_TW) * ((H + CR_TH - 1) / CR_TH);
+    if (tiles < 64) {
+        const dim3 grid((W + CR_TW - 1) / CR_TW, (H + CR_TH - 1) / CR_TH, 9);
+        return launch_pdl("k_corr", k_corr<1>, grid, dim3(64), smem, st, f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
+    }
+    const dim3 grid((W + CR_TW - 1) / CR_TW, (H + CR_TH - 1) / CR_TH, 3);
+    return launch_pdl("k_corr", k_corr<3>, grid, dim3(64), smem, st, f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
 }
 
 // ---------------------------------------------------------------------------
