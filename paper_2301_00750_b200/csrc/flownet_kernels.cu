@@ -287,14 +287,20 @@ __device__ __forceinline__ void src_coord(int d, float inv_scale, int n, int &i0
     f = s - (float)i0;
 }
 
-// up = 2 * bilinear_x2(coarse flow) -> x[:, 88:90]; w2 = warp_zero(f2, up)
+// up = 2 * bilinear_x2(coarse flow) -> x[:, 88:90]; w2 = warp_zero(f2, up).
+// One thread per (pixel, 16-channel group): the (cheap) upsampled flow is
+// recomputed per group, and the 4 taps x 4 float4 of a group are all loaded
+// before the FMAs.
 __global__ void k_up2_warp(const float *__restrict__ coarse, int cld, int Hc, int Wc,
                            const float *__restrict__ f2, int C, int H, int W,
                            float *__restrict__ x, int xld, float *__restrict__ w2)
 {
     pdl_wait();
-    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (long)H * W) return;
+    const int G = C / 16;
+    const long j = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= (long)H * W * G) return;
+    const long i = j / G;
+    const int g = (int)(j - i * G);
     const int y = (int)(i / W), xx = (int)(i - (long)y * W);
     int y0, y1, x0, x1;
     float fy, fx;
@@ -303,42 +309,54 @@ __global__ void k_up2_warp(const float *__restrict__ coarse, int cld, int Hc, in
     float up[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const float a = coarse[((long)y0 * Wc + x0) * cld + k], b = coarse[((long)y0 * Wc + x1) * cld + k];
-        const float c = coarse[((long)y1 * Wc + x0) * cld + k], d = coarse[((long)y1 * Wc + x1) * cld + k];
+        const float a = __ldg(coarse + ((long)y0 * Wc + x0) * cld + k), b = __ldg(coarse + ((long)y0 * Wc + x1) * cld + k);
+        const float c = __ldg(coarse + ((long)y1 * Wc + x0) * cld + k), d = __ldg(coarse + ((long)y1 * Wc + x1) * cld + k);
         const float top = a * (1.f - fx) + b * fx, bot = c * (1.f - fx) + d * fx;
         up[k] = 2.f * (top * (1.f - fy) + bot * fy);
     }
-    x[i * xld + 88] = up[0];
-    x[i * xld + 89] = up[1];
+    if (g == 0) {
+        x[i * xld + 88] = up[0];
+        x[i * xld + 89] = up[1];
+    }
     const float sx = (float)xx + up[0], sy = (float)y + up[1];
     const float gx0 = floorf(sx), gy0 = floorf(sy);
     const int ix = (int)gx0, iy = (int)gy0;
     const float ax = sx - gx0, ay = sy - gy0;
     const float wt[4] = {(1.f - ay) * (1.f - ax), (1.f - ay) * ax, ay * (1.f - ax), ay * ax};
     const int ty[4] = {iy, iy, iy + 1, iy + 1}, tx[4] = {ix, ix + 1, ix, ix + 1};
-    bool ok[4];
+    float4 v[4][4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) ok[t] = ty[t] >= 0 && ty[t] < H && tx[t] >= 0 && tx[t] < W;
-    for (int c = 0; c < C; c += 4) {
+    for (int t = 0; t < 4; ++t) {
+        const bool ok = ty[t] >= 0 && ty[t] < H && tx[t] >= 0 && tx[t] < W;
+        const float4 *src = reinterpret_cast<const float4 *>(f2 + ((long)(ok ? ty[t] : 0) * W + (ok ? tx[t] : 0)) * C + g * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[t][q] = ok ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float4 *dst = reinterpret_cast<float4 *>(w2 + i * C + g * 16);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            if (!ok[t]) continue;
-            const float4 v = *reinterpret_cast<const float4 *>(f2 + ((long)ty[t] * W + tx[t]) * C + c);
-            acc.x = fmaf(wt[t], v.x, acc.x);
-            acc.y = fmaf(wt[t], v.y, acc.y);
-            acc.z = fmaf(wt[t], v.z, acc.z);
-            acc.w = fmaf(wt[t], v.w, acc.w);
+            acc.x = fmaf(wt[t], v[t][q].x, acc.x);
+            acc.y = fmaf(wt[t], v[t][q].y, acc.y);
+            acc.z = fmaf(wt[t], v[t][q].z, acc.z);
+            acc.w = fmaf(wt[t], v[t][q].w, acc.w);
         }
-        *reinterpret_cast<float4 *>(w2 + i * C + c) = acc;
+        dst[q] = acc;
     }
 }
 
 int launch_up2_warp(const float *coarse, int cld, int Hc, int Wc, const float *f2, int C, int H,
                     int W, float *x, int xld, float *w2, cudaStream_t st)
 {
-    return launch_pdl("k_up2_warp", k_up2_warp, dim3(blocks_for((long)H * W, 128)), dim3(128), 0, st, coarse,
-                      cld, Hc, Wc, f2, C, H, W, x, xld, w2);
+    if (C % 16 != 0) {
+        set_error("feature warp needs C % 16 == 0");
+        return SS_VALUE_ERROR;
+    }
+    const long n = (long)H * W * (C / 16);
+    return launch_pdl("k_up2_warp", k_up2_warp, dim3(blocks_for(n, 128)), dim3(128), 0, st, coarse, cld, Hc,
+                      Wc, f2, C, H, W, x, xld, w2);
 }
 
 // ---------------------------------------------------------------------------
