@@ -129,6 +129,7 @@ struct ss_session {
     const void *st_hostI = nullptr, *st_hostP = nullptr;
     int64_t staged_pos = -1;
     cudaEvent_t st_src = nullptr, st_done = nullptr;
+    cudaStream_t up = nullptr;
     std::unique_ptr<dis::Estimator> dis;  // built-in flow (BuiltinFlow)
 };
 
@@ -200,6 +201,10 @@ static void session_free(ss_session *s)
     if (s->out_src) cudaEventDestroy(s->out_src);
     if (s->out_done) cudaEventDestroy(s->out_done);
     cudaFree(s->out_u8);
+    if (s->up) {
+        cudaStreamSynchronize(s->up);
+        cudaStreamDestroy(s->up);
+    }
     if (s->st_src) cudaEventDestroy(s->st_src);
     if (s->st_done) cudaEventDestroy(s->st_done);
     cudaFree(s->stI);
@@ -618,14 +623,17 @@ int ss_stage_pair(ss_session *s, int64_t position, const void *I, const void *P,
         SS_CUDA_TRY(cudaEventCreateWithFlags(&s->st_done, cudaEventDisableTiming));
     }
     if (s->staged_pos >= 0) SS_CUDA_TRY(cudaEventSynchronize(s->st_done));  // unconsumed: overwrite
-    // the staging buffers were a ring slot until the last push: order the copy
-    // after session work issued so far
+    // the staging buffers were the ring slot the last push evicted: order the
+    // upload after session work issued so far (flows may still read it).
+    // Uploads use their own stream, so they never queue behind result
+    // downloads on the copy stream.
+    if (!s->up) SS_CUDA_TRY(cudaStreamCreateWithFlags(&s->up, cudaStreamNonBlocking));
     SS_CUDA_TRY(cudaEventRecord(s->st_src, s->stream));
-    SS_CUDA_TRY(cudaStreamWaitEvent(s->copy, s->st_src, 0));
+    SS_CUDA_TRY(cudaStreamWaitEvent(s->up, s->st_src, 0));
     const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    SS_CUDA_TRY(cudaMemcpyAsync(s->stI, I, px * s->ci * sizeof(float), kind, s->copy));
-    SS_CUDA_TRY(cudaMemcpyAsync(s->stP, P, px * s->cp * sizeof(float), kind, s->copy));
-    SS_CUDA_TRY(cudaEventRecord(s->st_done, s->copy));
+    SS_CUDA_TRY(cudaMemcpyAsync(s->stI, I, px * s->ci * sizeof(float), kind, s->up));
+    SS_CUDA_TRY(cudaMemcpyAsync(s->stP, P, px * s->cp * sizeof(float), kind, s->up));
+    SS_CUDA_TRY(cudaEventRecord(s->st_done, s->up));
     s->staged_pos = position;
     s->st_hostI = I;
     s->st_hostP = P;

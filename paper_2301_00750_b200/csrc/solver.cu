@@ -722,6 +722,7 @@ SolverWork::~SolverWork()
     cudaFree(sums);
     cudaFree(d_result);
     cudaFreeHost(h_result);
+    cudaFreeHost(h_maxbits);
 }
 
 int SolverWork::ensure(int h_, int w_, int c_, int iterations)
@@ -740,10 +741,14 @@ int SolverWork::ensure(int h_, int w_, int c_, int iterations)
     if (iterations > maxiters) {
         cudaFree(maxbits);
         cudaFree(sums);
+        cudaFreeHost(h_maxbits);
         maxbits = nullptr;
         sums = nullptr;
+        h_maxbits = d_maxbits_map = nullptr;
         maxiters = iterations;
         SS_CUDA_TRY(cudaMalloc(&maxbits, (size_t)maxiters * sizeof(unsigned)));
+        SS_CUDA_TRY(cudaHostAlloc(&h_maxbits, (size_t)maxiters * sizeof(unsigned), cudaHostAllocMapped));
+        SS_CUDA_TRY(cudaHostGetDevicePointer(&d_maxbits_map, h_maxbits, 0));
         SS_CUDA_TRY(cudaMalloc(&sums, (size_t)maxiters * sizeof(float)));
     }
     if (!h_result) {
@@ -815,6 +820,11 @@ static int write_output(const float *planar, int h, int w, int c, float *out_hwc
         k_planar_clamp_to_hwc<3><<<blocks_for(hw, 256), 256, 0, st>>>(planar, hw, out_hwc);
     SS_LAUNCH_CHECK("k_planar_clamp_to_hwc");
     return SS_OK;
+}
+
+__global__ void k_copy_u32(unsigned *__restrict__ dst, const unsigned *__restrict__ src, int n)
+{
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
 int solve_planar(SolverWork &wk, const float *A, const float *init, const float *lapP,
@@ -908,14 +918,17 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
 
     // grey-zone test on the per-pass maxima (blocked) -- the streaming path
     // always takes the exact check below
-    static thread_local std::vector<unsigned> hb;
     const float thr = (float)(FLT_MAX / (2.0 * (double)n));
     unsigned thr_bits;
     std::memcpy(&thr_bits, &thr, sizeof thr_bits);
     int first_grey_pass = -1;
     if (variant) {
-        hb.resize(n_pass);
-        SS_CUDA_TRY(cudaMemcpyAsync(hb.data(), wk.maxbits, n_pass * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        // the per-pass maxima reach the host through mapped pinned memory,
+        // written by a one-block kernel: a copy-engine readback would queue
+        // behind unrelated device->host copies in flight (an async output)
+        unsigned *hb = wk.h_maxbits;
+        k_copy_u32<<<1, 128, 0, st>>>(wk.d_maxbits_map, wk.maxbits, n_pass);
+        SS_LAUNCH_CHECK("k_copy_u32");
         SS_CUDA_TRY(cudaStreamSynchronize(st));
         for (int ps = 0; ps < n_pass; ++ps)
             if (hb[ps] > thr_bits) {

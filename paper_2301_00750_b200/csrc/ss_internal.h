@@ -68,6 +68,8 @@ struct SolverWork {
     int maxiters = 0;
     float *sums = nullptr;        // exact pairwise sums (replay path)
     int *h_result = nullptr;      // pinned: [first_gray_iter, first_nonfinite_iter]
+    unsigned *h_maxbits = nullptr;      // mapped pinned readback of the per-pass maxima
+    unsigned *d_maxbits_map = nullptr;  // its device alias
     int *d_result = nullptr;
     PairwisePlan plan;
     ~SolverWork();

@@ -11,6 +11,7 @@ from paper_2301_00750_b200.consistency import ConsistencyParams
 from paper_2301_00750_b200.synthetic import DeviceSequence
 
 prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+mode = sys.argv[2] if len(sys.argv) > 2 else "full"  # full | nostage | noout | devpush
 h, w = 1080, 1920
 L = _lib.lib()
 seq = DeviceSequence(h, w, step=(2, 1), seed=0)
@@ -18,7 +19,12 @@ pool = [seq.frame(k + 1) for k in range(4)]
 host_i = [p[0].cpu().pin_memory() for p in pool]
 host_p = [p[1].cpu().pin_memory() for p in pool]
 outs = [torch.empty((h, w, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+douts = [torch.empty((h, w, 3), dtype=torch.float32, device="cuda") for _ in range(2)]
+outs8 = [torch.empty((h, w, 3), dtype=torch.uint8).pin_memory() for _ in range(2)]
 net = ss.LiteFlowNet(seed=0, precision=prec)
+if os.environ.get("E2E_OWN_STREAM"):
+    _strm = torch.cuda.Stream()
+    torch.cuda.set_stream(_strm)
 st = ss.SessionState(params=ConsistencyParams())
 st.push_pair(1, pool[0][0], pool[0][1])
 st.push_pair(2, pool[1][0], pool[1][1])
@@ -32,14 +38,23 @@ def tcall(name, f):
 for k in range(30):
     pos += 1
     tcall("flow0", lambda: L.ss_session_compute_flow(sess, 0))
-    tcall("push", lambda: L.ss_push_pair(sess, pos, host_i[k % 4].data_ptr(), host_p[k % 4].data_ptr(), 0, 0))
+    if mode == "devpush":
+        tcall("push", lambda: L.ss_push_pair(sess, pos, pool[k % 4][0].data_ptr(), pool[k % 4][1].data_ptr(), 0, 1))
+    else:
+        tcall("push", lambda: L.ss_push_pair(sess, pos, host_i[k % 4].data_ptr(), host_p[k % 4].data_ptr(), 0, 0))
     tcall("flow1", lambda: L.ss_session_compute_flow(sess, 1))
-    tcall("stage", lambda: L.ss_stage_pair(sess, pos + 1, host_i[(k + 1) % 4].data_ptr(), host_p[(k + 1) % 4].data_ptr(), 0, 0))
+    if mode in ("full", "noout"):
+        tcall("stage", lambda: L.ss_stage_pair(sess, pos + 1, host_i[(k + 1) % 4].data_ptr(), host_p[(k + 1) % 4].data_ptr(), 0, 0))
     prm = params_struct(ConsistencyParams()); it = ctypes.c_int(0)
     tcall("step", lambda: L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)))
-    tcall("out", lambda: L.ss_output_async(sess, outs[k % 2].data_ptr(), 0, 0))
+    if mode == "outdev":
+        tcall("out", lambda: L.ss_output_async(sess, douts[k % 2].data_ptr(), 0, 1))
+    elif mode == "outu8":
+        tcall("out", lambda: L.ss_output_async(sess, outs8[k % 2].data_ptr(), 1, 0))
+    elif mode != "noout" and mode != "devpush":
+        tcall("out", lambda: L.ss_output_async(sess, outs[k % 2].data_ptr(), 0, 0))
 torch.cuda.synchronize()
 for n, v in acc.items():
     v = v[10:]
     print(f"{n:6s} mean {1e3 * sum(v) / len(v):7.3f} ms  max {1e3 * max(v):7.3f}")
-print("total per step", sum(1e3 * sum(v[10:]) / len(v[10:]) for v in acc.values()))
+print(mode, "total per step", sum(1e3 * sum(v[10:]) / len(v[10:]) for v in acc.values()))
