@@ -30,6 +30,7 @@
 
 #include "ss_common.cuh"
 #include "ss_internal.h"
+#include "flownet.h"  // launch_pdl
 
 namespace ss {
 
@@ -454,13 +455,19 @@ __global__ void __launch_bounds__(blk::THREADS, 1)
         tma_load_2d(stage + 4 * STAGE, &maps.W, x, y, bar);
     };
 
+    // programmatic dependent launch: the next pass may launch now -- its CTAs
+    // take the SMs this pass's tail leaves idle and run their prologue there
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // zero the O buffers once (pads stay finite), init the barrier
     for (int i = tid; i < 2 * SH2 * SW2 + SW2; i += THREADS) sm0[i] = 0.0f;
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if ((int)blockIdx.x < ntiles) issue(blockIdx.x);
     }
+    // the previous pass's iterates (and everything before it) are complete
+    // and visible past this point
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
     __syncthreads();
 
     const int p = threadIdx.x, s = threadIdx.y;
@@ -512,9 +519,9 @@ static int launch_tma(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st
     constexpr int OW = blk::RW - 2 * K, OH = blk::RH - 2 * K;
     const int ntiles = ((a.w + OW - 1) / OW) * ((a.h + OH - 1) / OH) * a.c;
     const int grid = std::min(ntiles, n_sm);
-    k_sgd_tma<K><<<grid, dim3(blk::PAIRS, blk::STRIPS), blk::SMEM_TMA, st>>>(maps, a);
-    SS_LAUNCH_CHECK("k_sgd_tma");
-    return SS_OK;
+    // a programmatic dependent of the previous pass (SS_FLOW_PDL=0: plain launch)
+    return fn::launch_pdl("k_sgd_tma", k_sgd_tma<K>, dim3(grid), dim3(blk::PAIRS, blk::STRIPS), blk::SMEM_TMA,
+                          st, maps, a);
 }
 
 // tensor maps over planar (c, h, w) float32 arrays (cuTensorMapEncodeTiled
