@@ -284,9 +284,11 @@ def main():
         flush.zero_()  # L2 flush between timed steps, outside the events
         ev[k][0].record(stream)
         step()
-        # the step's end event covers its side-stream work too (the flow the
-        # step started for the next step, overlapping its solver)
-        _check(L.ss_session_join(state.handle), L)
+        # ss_step pre-launches the next step's flow t+1 -> t on the session's
+        # side stream behind its solver; the region ends with it joined, so
+        # it holds exactly K such flows (the first one ran during warm-up)
+        if k == args.steps - 1:
+            _check(L.ss_session_join(state.handle), L)
         ev[k][1].record(stream)
         tm = state.last_timing
         flow_ms.append(tm.flow_ms)

@@ -115,6 +115,17 @@ struct ss_session {
     cudaEvent_t fork = nullptr, join = nullptr;
     bool side_pending = false;
     int side_slots[2] = {-1, -1};  // ring slots whose pyramids the side flow reads
+    // pre-launch: once a step's solver is enqueued (before the host waits for
+    // it), the NEXT step's flow t+1 -> t -- both pyramids already cached -- is
+    // launched on the side stream behind the solver, into spare buffers; the
+    // next ss_session_compute_flow(0) claims it by swapping pointers.  The GPU
+    // starts it the moment the solver ends instead of after the host's return
+    // trip (and graph launch).  Spare buffers: a diverged step keeps its flows.
+    float *uv_pre = nullptr;
+    uint8_t *valid_pre = nullptr;
+    cudaEvent_t pre_start = nullptr;
+    int64_t pre_for = -1;  // step position the pre-launched flow is for
+    int pre_slots[2] = {-1, -1};
     // asynchronous output (ss_output_async): device->host copy on its own
     // stream, overlapping the next step; the solver that would next overwrite
     // the copied buffer waits for it
@@ -194,6 +205,9 @@ static void session_free(ss_session *s)
     }
     if (s->fork) cudaEventDestroy(s->fork);
     if (s->join) cudaEventDestroy(s->join);
+    if (s->pre_start) cudaEventDestroy(s->pre_start);
+    cudaFree(s->uv_pre);
+    cudaFree(s->valid_pre);
     if (s->copy) {
         cudaStreamSynchronize(s->copy);
         cudaStreamDestroy(s->copy);
@@ -541,6 +555,7 @@ int ss_session_reset(ss_session *s)
     if (int rc = join_side(s)) return rc;
     s->side_pending = false;
     s->flow_timed = false;
+    s->pre_for = -1;
     s->n_pairs = 0;
     s->has_output = false;
     s->solved_through = 0;
@@ -759,8 +774,32 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
     a.wp_out = a.wn_out = nullptr;
     if (int rc = launch_presolve(a, s->ci, s->cp, with_next != 0, s->stream)) return rc;
     SS_CUDA_TRY(cudaEventRecord(s->ev[1], s->stream));
+    // the next step's flow t+1 -> t, launched once the solver is enqueued
+    auto prelaunch = [&]() -> int {
+        static const bool on = getenv("SS_FLOW_PRELAUNCH") == nullptr || strcmp(getenv("SS_FLOW_PRELAUNCH"), "0");
+        if (!on || !with_next || !s->run || !s->side) return SS_OK;
+        const int64_t tn = t + 1;
+        const int ia = (int)(next - s->slot), ib = (int)(cur - s->slot);
+        if (s->run->slots[ia].key != tn || s->run->slots[ib].key != t) return SS_OK;  // pyramids not cached
+        const size_t px = (size_t)s->h * s->w;
+        if (!s->uv_pre) {
+            SS_CUDA_TRY(cudaMalloc(&s->uv_pre, px * 2 * sizeof(float)));
+            SS_CUDA_TRY(cudaMalloc(&s->valid_pre, px));
+            SS_CUDA_TRY(cudaEventCreate(&s->pre_start));
+        }
+        // behind the solver (ev[2] marks its end): the flow would only slow it
+        SS_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev[2], 0));
+        SS_CUDA_TRY(cudaEventRecord(s->pre_start, s->side));
+        if (int rc = s->run->flow(ia, ib, s->uv_pre, s->valid_pre, s->side, 1)) return rc;
+        SS_CUDA_TRY(cudaEventRecord(s->join, s->side));
+        s->side_pending = true;
+        s->side_slots[0] = s->pre_slots[0] = ia;
+        s->side_slots[1] = s->pre_slots[1] = ib;
+        s->pre_for = tn;
+        return SS_OK;
+    };
     int rc = solve_planar(s->solver, s->A, s->A, s->lapP, s->wc, *p, s->O_new, div_iter, s->stream,
-                          s->ev[2]);
+                          s->ev[2], prelaunch);
     if (rc) return rc;  // divergence: state not advanced (consistency.py:293, :410)
     SS_CUDA_TRY(cudaEventSynchronize(s->ev[2]));
     float t_blend = 0.f, t_solve = 0.f;
@@ -1009,6 +1048,18 @@ int ss_session_compute_flow(ss_session *s, int which)
         return SS_VALUE_ERROR;
     }
     const int ia = (int)(a - s->slot), ib = (int)(b - s->slot);
+    if (which == 0 && s->pre_for == t && s->pre_slots[0] == ia && s->pre_slots[1] == ib &&
+        s->run->slots[ia].key == t && s->run->slots[ib].key == other) {
+        // pre-launched by the previous ss_step: claim it (it may still be
+        // running on the side stream; side_pending stays set)
+        std::swap(s->uv[0], s->uv_pre);
+        std::swap(s->valid[0], s->valid_pre);
+        std::swap(s->fev[0], s->pre_start);
+        s->pre_for = -1;
+        s->flow_timed = true;
+        s->flow_for[0] = t;
+        return SS_OK;
+    }
     if (which == 0 || !s->flow_timed) {
         if (which == 0 && s->side_pending) {  // a second flow to the previous frame
             if (int rc = join_side(s)) return rc;

@@ -836,7 +836,7 @@ __global__ void k_copy_u32(unsigned *__restrict__ dst, const unsigned *__restric
 
 int solve_planar(SolverWork &wk, const float *A, const float *init, const float *lapP,
                  const float *wc, const ss_params &p, float *out_hwc, int *div_iter,
-                 cudaStream_t st, cudaEvent_t done_ev)
+                 cudaStream_t st, cudaEvent_t done_ev, const std::function<int()> &after_enqueue)
 {
     const int iters = p.iterations;
     if (div_iter) *div_iter = 0;
@@ -922,6 +922,7 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
         if (rc) return rc;
         if (done_ev) SS_CUDA_TRY(cudaEventRecord(done_ev, st));
     }
+    if (after_enqueue && (rc = after_enqueue())) return rc;
 
     // grey-zone test on the per-pass maxima (blocked) -- the streaming path
     // always takes the exact check below

@@ -1,6 +1,8 @@
 // Internal (non-ABI) interfaces between the streamstab B200 translation units.
 #pragma once
 
+#include <functional>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -80,9 +82,12 @@ struct SolverWork {
 // O = O_prev = A (init == target) or from init, on planar A / lapP / wc, then
 // write clamp(O, 0, 1) as HWC into out.  Synchronises st.  Returns
 // SS_SOLVER_DIVERGENCE with *div_iter set exactly as the reference would.
+// after_enqueue (optional) runs once the solve is enqueued (done_ev recorded),
+// before the host waits for it.
 int solve_planar(SolverWork &wk, const float *A, const float *init_planar, const float *lapP,
                  const float *wc, const ss_params &p, float *out_hwc, int *div_iter,
-                 cudaStream_t st, cudaEvent_t done_ev = nullptr);
+                 cudaStream_t st, cudaEvent_t done_ev = nullptr,
+                 const std::function<int()> &after_enqueue = {});
 
 int solver_variant();  // 0 = streaming, 1 = temporally blocked (env SS_SOLVER)
 
