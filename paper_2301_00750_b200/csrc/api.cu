@@ -113,6 +113,8 @@ struct ss_session {
     // the next frame's pyramid and the flow to it on the session stream
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t hi = nullptr;  // highest priority: pyramid + flow to the next frame
+    cudaEvent_t hfork = nullptr, hjoin = nullptr;
     bool side_pending = false;
     int side_slots[2] = {-1, -1};  // ring slots whose pyramids the side flow reads
     // pre-launch: once a step's solver is enqueued (before the host waits for
@@ -205,6 +207,12 @@ static void session_free(ss_session *s)
     }
     if (s->fork) cudaEventDestroy(s->fork);
     if (s->join) cudaEventDestroy(s->join);
+    if (s->hi) {
+        cudaStreamSynchronize(s->hi);
+        cudaStreamDestroy(s->hi);
+    }
+    if (s->hfork) cudaEventDestroy(s->hfork);
+    if (s->hjoin) cudaEventDestroy(s->hjoin);
     if (s->pre_start) cudaEventDestroy(s->pre_start);
     cudaFree(s->uv_pre);
     cudaFree(s->valid_pre);
@@ -983,6 +991,18 @@ int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
         SS_CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
         SS_CUDA_TRY(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming));
         SS_CUDA_TRY(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming));
+        // the critical chain (pyramid of the new frame -> flow to it) runs on
+        // a highest-priority stream: the concurrent flow to the previous frame
+        // (side stream, lowest priority) then fills the SMs it leaves idle
+        // instead of holding them while the chain's small kernels queue
+        static const bool prio = getenv("SS_FLOW_PRIO") == nullptr || strcmp(getenv("SS_FLOW_PRIO"), "0");
+        if (prio) {
+            int least = 0, greatest = 0;
+            SS_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            SS_CUDA_TRY(cudaStreamCreateWithPriority(&s->hi, cudaStreamNonBlocking, greatest));
+            SS_CUDA_TRY(cudaEventCreateWithFlags(&s->hfork, cudaEventDisableTiming));
+            SS_CUDA_TRY(cudaEventCreateWithFlags(&s->hjoin, cudaEventDisableTiming));
+        }
     }
     if (int rc = fn::prepare_conv_tma()) return rc;
     return fn::prepare_conv_tc();
@@ -1076,13 +1096,21 @@ int ss_session_compute_flow(ss_session *s, int which)
             s->run->slots[sl].key != pos)
             if (int rc = join_side(s)) return rc;
     }
-    if (int rc = s->run->pyramid(ia, t, a->I, s->ci, s->stream)) return rc;
-    if (int rc = s->run->pyramid(ib, other, b->I, s->ci, s->stream)) return rc;
+    // pyramids and the flow to the next frame: on the high-priority stream
+    // (forked from and joined back to the session stream) when there is one
+    cudaStream_t ws = s->stream;
+    if (s->hi) {
+        SS_CUDA_TRY(cudaEventRecord(s->hfork, s->stream));
+        SS_CUDA_TRY(cudaStreamWaitEvent(s->hi, s->hfork, 0));
+        ws = s->hi;
+    }
+    if (int rc = s->run->pyramid(ia, t, a->I, s->ci, ws)) return rc;
+    if (int rc = s->run->pyramid(ib, other, b->I, s->ci, ws)) return rc;
     if (which == 0 && s->side) {
         // fork: the flow to t-1 (estimator buffer set 1) overlaps whatever the
         // session stream does next -- typically the pyramid of t+1 and the flow
         // to it (set 0); ss_step / any conflicting call joins it
-        SS_CUDA_TRY(cudaEventRecord(s->fork, s->stream));
+        SS_CUDA_TRY(cudaEventRecord(s->fork, ws));
         SS_CUDA_TRY(cudaStreamWaitEvent(s->side, s->fork, 0));
         if (int rc = s->run->flow(ia, ib, s->uv[0], s->valid[0], s->side, 1)) return rc;
         SS_CUDA_TRY(cudaEventRecord(s->join, s->side));
@@ -1090,8 +1118,16 @@ int ss_session_compute_flow(ss_session *s, int which)
         s->side_pending = true;
         s->side_slots[0] = ia;
         s->side_slots[1] = ib;
+        if (s->hi) {
+            SS_CUDA_TRY(cudaEventRecord(s->hjoin, s->hi));
+            SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->hjoin, 0));
+        }
     } else {
-        if (int rc = s->run->flow(ia, ib, s->uv[which], s->valid[which], s->stream, 0)) return rc;
+        if (int rc = s->run->flow(ia, ib, s->uv[which], s->valid[which], ws, 0)) return rc;
+        if (s->hi) {
+            SS_CUDA_TRY(cudaEventRecord(s->hjoin, s->hi));
+            SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->hjoin, 0));
+        }
         if (int rc = join_side(s)) return rc;  // fev[1] marks the end of both flows
         SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->stream));
     }

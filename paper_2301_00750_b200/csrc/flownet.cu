@@ -346,6 +346,22 @@ int Run::init(const Weights *wt, int h_, int w_, int nsets_)
 }
 
 static thread_local int conv_mode_ = CONV_TC_TF32X3;  // set by the Run issuing the convs
+// persistent conv grids of the concurrent flow (estimator set 1, the side
+// stream) leave SS_SIDE_RESERVE SMs free, so the critical chain's small
+// kernels (high-priority stream) find SMs instead of queueing behind them
+static thread_local int grid_cap_ = 0;
+static int side_grid_cap()
+{
+    static const int cap = [] {
+        const char *e = getenv("SS_SIDE_RESERVE");
+        const int r = e ? atoi(e) : 48;
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return r > 0 && r < n ? n - r : 0;
+    }();
+    return cap;
+}
 static thread_local float *ws_ = nullptr;
 static thread_local size_t ws_floats_ = 0;
 // SS_CONV_TMA=0: the fp32 path uses the register-gather tcgen05 kernel
@@ -423,6 +439,7 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
     p.act = L.act;
     const bool bf = conv_mode_ == CONV_TC_BF16;
     p.tmB = bf ? &L.tmB_bf : &L.tmB;
+    p.grid_cap = grid_cap_;
     p.tma_T = bf ? L.tma_T_bf : L.tma_T;
     if (conv_mode_ == CONV_FFMA) return launch_conv_ffma(p, st);
     if (use_tma_) return launch_conv_tma(p, bf ? 0 : 1, st);
@@ -459,6 +476,7 @@ int Run::pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st
 {
     Slot &sl = slots[slot];
     if (key >= 0 && sl.key == key) return SS_OK;  // key < 0: never cached
+    grid_cap_ = 0;  // pyramids run on the critical chain: the full grid
     sl.key = -1;
     int rc;
     if (use_graphs && !prof.on) {
@@ -480,6 +498,10 @@ int Run::flow(int a, int b, float *uv, uint8_t *valid, cudaStream_t st, int set)
 {
     set = set < nsets ? set : 0;
     select_set(set);
+    grid_cap_ = set == 1 ? side_grid_cap() : 0;
+    struct Reset {
+        ~Reset() { grid_cap_ = 0; }
+    } reset_cap;
     if (use_graphs && !prof.on) {
         const auto k = std::make_tuple(a, b, (void *)uv, (void *)valid, set);
         auto &g = flow_graphs[k];

@@ -57,6 +57,7 @@ struct ConvParams {
     float *ws = nullptr;        // split-K workspace (tensor-core path), may be null
     size_t ws_floats = 0;
     int k_per_split = 0;        // set by the launcher
+    int grid_cap = 0;           // > 0: at most this many CTAs (persistent kernels)
     int n_full = 0, n_off = 0;  // N-split (set by the launcher): weight rows [n_off, n_off + Cout_pad)
     const void *tmB = nullptr;  // TMA weight map (CUtensorMap, flownet_tma.cu), fp32 path
     int tma_T = 1;              // taps per weight stage of that map

@@ -685,6 +685,17 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int prec, in
         set_error("conv stage does not fit in shared memory");
         return SS_VALUE_ERROR;
     }
+    // halo tiles: with the weights resident, spend the spare shared memory on
+    // more A slots -- thin layers are bound by the per-tile chain (TMA
+    // round trip, conversion, MMAs) that two slots barely overlap
+    static const int na_max = [] {
+        const char *e = getenv("SS_CONV_NA");
+        return e ? std::max(2, std::min(8, atoi(e))) : 6;
+    }();
+    if (amode != 0 && a.b_res)
+        while (a.na < na_max &&
+               2 * (a.na + 1) * a.a_slot + a.nk_all * a.b_stage + bar_bytes + a.nk_all * 16 <= SMEM_MAX)
+            ++a.na;
     // split K when the tiles alone leave SMs idle (>= 2 stages per split)
     int splits = 1;
     if (p.ws && a.n_tiles < n_sm_tma && a.nk_all >= 4) {
@@ -697,7 +708,7 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int prec, in
     splits = (a.nk_all + a.k_per_split - 1) / a.k_per_split;
     a.ws = splits > 1 ? p.ws : nullptr;
     a.units = a.n_tiles * splits;
-    const int grid = std::min(a.units, n_sm_tma);
+    const int grid = std::min(a.units, p.grid_cap > 0 ? std::min(p.grid_cap, n_sm_tma) : n_sm_tma);
     const size_t smem = (size_t)2 * a.na * a.a_slot + (size_t)a.stages * a.b_stage + bar_bytes + a.stages * 16;
     const CUtensorMap &tmB = *static_cast<const CUtensorMap *>(p.tmB);
     const int rc = launch_pdl("k_conv_tc3", conv_kernel(prec, amode, a.b_res != 0), dim3(grid), dim3(TM_THREADS),
