@@ -378,34 +378,47 @@ constexpr int CR_WR = CR_TH + 2;                          // w2 rows per dy grou
 constexpr int CR_W2P = CR_WW * CR_PX + 4;                 // w2 row pitch (odd # of 16 B)
 constexpr int CR_F1P = CR_TW * CR_PX + 4;                 // f1 row pitch
 constexpr int CR_W2F = CR_WR * CR_W2P, CR_F1F = CR_TH * CR_F1P;
+#ifndef CR_CS_COARSE
+#define CR_CS_COARSE 4
+#endif
+#ifndef CR_CS_FINE
+#define CR_CS_FINE 2
+#endif
 
 // DY dy rows per CTA (grid z = 9 / DY): 3 for the fine level, 1 for the
 // coarse ones (three times the CTAs where the image alone gives too few)
-template <int DY>
-__global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const float *__restrict__ w2,
-                                             int C, int H, int W, float *__restrict__ x, int xld,
-                                             int copy_f1)
+// CS channel groups of 64 threads: group g takes channels [g * 16 / CS,
+// (g + 1) * 16 / CS) of every 16-channel chunk (CS x the warps for the same
+// shared memory: the kernel is latency bound at 2 warps per CTA); the groups'
+// partial sums are added in group order at the end (deterministic).
+template <int DY, int CS>
+__global__ void __launch_bounds__(64 * CS) k_corr(const float *__restrict__ f1, const float *__restrict__ w2,
+                                                  int C, int H, int W, float *__restrict__ x, int xld,
+                                                  int copy_f1)
 {
     constexpr int WR = CR_TH + DY - 1;  // w2 rows staged
+    constexpr int NT = 64 * CS, CPG = CR_CK / CS;  // threads, channels per group per chunk
+    static_assert(CPG % 4 == 0, "channel groups are float4 multiples");
     pdl_wait();
     extern __shared__ __align__(16) float cr_smem[];
     float(*sw)[CR_W2F] = reinterpret_cast<float(*)[CR_W2F]>(cr_smem);
     float(*sf)[CR_F1F] = reinterpret_cast<float(*)[CR_F1F]>(cr_smem + 2 * CR_W2F);
-    const int t = threadIdx.x;
+    const int tid = threadIdx.x, grp = tid >> 6;
+    const int t = tid & 63;
     const int ty = t & 7, cx = (t >> 3) * 2;  // tile row, first of 2 columns
     const int bx = blockIdx.x * CR_TW, by = blockIdx.y * CR_TH;
     const int dy0 = (int)blockIdx.z * DY - CR_HALO;  // dy rows dy0 .. dy0 + DY - 1
 
     auto load = [&](int buf, int c0) {
         // w2: WR rows x 24 columns x 4 float4
-        for (int i = t; i < WR * CR_WW * 4; i += 64) {
+        for (int i = tid; i < WR * CR_WW * 4; i += NT) {
             const int q = i & 3, px = (i >> 2) % CR_WW, r = (i >> 2) / CR_WW;
             const int gy = by + r + dy0, gx = bx - CR_HALO + px;
             const bool ok = gy >= 0 && gy < H && gx >= 0 && gx < W;
             cp_async16(&sw[buf][r * CR_W2P + px * CR_PX + q * 4],
                        w2 + ((long)(ok ? gy : 0) * W + (ok ? gx : 0)) * C + c0 + q * 4, ok);
         }
-        for (int i = t; i < CR_TH * CR_TW * 4; i += 64) {
+        for (int i = tid; i < CR_TH * CR_TW * 4; i += NT) {
             const int q = i & 3, px = (i >> 2) % CR_TW, r = (i >> 2) / CR_TW;
             const int gy = by + r, gx = bx + px;
             const bool ok = gy < H && gx < W;
@@ -435,7 +448,7 @@ __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const
         }
         __syncthreads();
         if (copy_f1 && (int)blockIdx.z == 4 / DY) {  // f1 -> x[:, 96 + c], one dy group does it
-            for (int i = t; i < CR_TH * CR_TW * 4; i += 64) {
+            for (int i = tid; i < CR_TH * CR_TW * 4; i += NT) {
                 const int q = i & 3, px = (i >> 2) % CR_TW, r = (i >> 2) / CR_TW;
                 const int gy = by + r, gx = bx + px;
                 if (gy < H && gx < W)
@@ -446,7 +459,7 @@ __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const
         const float *w = &sw[buf][ty * CR_W2P + cx * CR_PX];
         const float *a = &sf[buf][ty * CR_F1P + cx * CR_PX];
 #pragma unroll
-        for (int c = 0; c < CR_CK; c += 4) {
+        for (int c = grp * CPG; c < grp * CPG + CPG; c += 4) {
             const float4 a0 = *reinterpret_cast<const float4 *>(a + c);
             const float4 a1 = *reinterpret_cast<const float4 *>(a + CR_PX + c);
 #pragma unroll
@@ -463,6 +476,31 @@ __global__ void __launch_bounds__(64) k_corr(const float *__restrict__ f1, const
             }
         }
         __syncthreads();
+    }
+    if (CS > 1) {
+        // groups 1.. hand their partial sums to group 0 through the (now
+        // idle) staging buffers, which group 0 adds in group order
+        float *red = cr_smem;
+        constexpr int NV = 2 * DY * 9;
+        static_assert((CS - 1) * NV * 64 <= 2 * (CR_W2F + CR_F1F), "reduction fits the staging buffers");
+        if (grp > 0) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int j = 0; j < DY; ++j)
+#pragma unroll
+                    for (int d = 0; d < 9; ++d) red[((grp - 1) * NV + (p * DY + j) * 9 + d) * 64 + t] = acc[p][j][d];
+        }
+        __syncthreads();
+        if (grp > 0) return;
+#pragma unroll
+        for (int g = 1; g < CS; ++g)
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int j = 0; j < DY; ++j)
+#pragma unroll
+                    for (int d = 0; d < 9; ++d) acc[p][j][d] += red[((g - 1) * NV + (p * DY + j) * 9 + d) * 64 + t];
     }
     const float inv = 1.f / (float)C;
     const int y = by + ty;
@@ -483,9 +521,9 @@ int prepare_flow_kernels()
 {
     static bool done = false;
     if (done) return SS_OK;
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr<3, CR_CS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(2 * (CR_W2F + CR_F1F) * sizeof(float))));
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr<1, CR_CS_COARSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(2 * (CR_W2F + CR_F1F) * sizeof(float))));
     done = true;
     return SS_OK;
@@ -503,10 +541,12 @@ int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x,
     const int tiles = ((W + CR_TW - 1) / CR_TW) * ((H + CR_TH - 1) / CR_TH);
     if (tiles < 64) {
         const dim3 grid((W + CR_TW - 1) / CR_TW, (H + CR_TH - 1) / CR_TH, 9);
-        return launch_pdl("k_corr", k_corr<1>, grid, dim3(64), smem, st, f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
+        return launch_pdl("k_corr", k_corr<1, CR_CS_COARSE>, grid, dim3(64 * CR_CS_COARSE), smem, st, f1, w2, C, H,
+                          W, x, xld, copy_f1 ? 1 : 0);
     }
     const dim3 grid((W + CR_TW - 1) / CR_TW, (H + CR_TH - 1) / CR_TH, 3);
-    return launch_pdl("k_corr", k_corr<3>, grid, dim3(64), smem, st, f1, w2, C, H, W, x, xld, copy_f1 ? 1 : 0);
+    return launch_pdl("k_corr", k_corr<3, CR_CS_FINE>, grid, dim3(64 * CR_CS_FINE), smem, st, f1, w2, C, H, W, x,
+                      xld, copy_f1 ? 1 : 0);
 }
 
 // ---------------------------------------------------------------------------
