@@ -297,9 +297,26 @@ __global__ void k_splitk_reduce(const float *__restrict__ ws, int splits, int M,
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long)M * n4) return;
     const int m = (int)(i / n4), n = (int)(i - (long)m * n4) * 4;
-    float4 acc = *reinterpret_cast<const float4 *>(ws + (size_t)m * N + n);
-    for (int s = 1; s < splits; ++s) {
-        const float4 v = *reinterpret_cast<const float4 *>(ws + ((size_t)s * M + m) * N + n);
+    // partials are added in split order; their loads are issued eight at a
+    // time (a serial load -> add chain would pay one L2 round trip per split)
+    const float *src = ws + (size_t)m * N + n;
+    const size_t stride = (size_t)M * N;
+    float4 acc = *reinterpret_cast<const float4 *>(src);
+    int s = 1;
+    for (; s + 8 <= splits; s += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldcg(reinterpret_cast<const float4 *>(src + (s + j) * stride));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            acc.x += v[j].x;
+            acc.y += v[j].y;
+            acc.z += v[j].z;
+            acc.w += v[j].w;
+        }
+    }
+    for (; s < splits; ++s) {
+        const float4 v = __ldcg(reinterpret_cast<const float4 *>(src + s * stride));
         acc.x += v.x;
         acc.y += v.y;
         acc.z += v.z;
@@ -319,7 +336,7 @@ int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, co
                          int act, float *out, int out_ld, cudaStream_t st)
 {
     const long n = (long)M * ((Cout + 3) / 4);
-    return launch_pdl("k_splitk_reduce", k_splitk_reduce, dim3(blocks_for(n, 256)), dim3(256), 0, st, ws, splits,
+    return launch_pdl("k_splitk_reduce", k_splitk_reduce, dim3(blocks_for(n, 128)), dim3(128), 0, st, ws, splits,
                       M, N, Cout, bias, act, out, out_ld);
 }
 
