@@ -263,6 +263,12 @@ def main():
     def step():
         _start_flow_to_prev(state, flow)  # stabilize_stream's order
         push()
+        # stage the next pair (device -> device on the session's upload
+        # stream, overlapping this step): ss_step then also computes its
+        # pyramid behind the solver, and the next push swaps it in
+        i2, p2 = pool[pos % pool_n]
+        _check(L.ss_stage_pair(state.handle, pos + 1, i2.data_ptr(), p2.data_ptr(), _lib.SS_F32,
+                               _lib.SS_DEVICE), L)
         state.params = params_for(pos)
         _run_step(state, flow, with_next=True, return_host=False)
 

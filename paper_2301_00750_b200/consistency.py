@@ -273,6 +273,7 @@ class SessionState:
         self._out_cache = None
         self._squeeze = False
         self._flow0_for = None  # step whose flow t -> t-1 was started early
+        self._inflight: list = []  # device push sources, alive until the next step
 
     # -- device session ------------------------------------------------------
     def _ensure_session(self, input_frame, processed_frame):
@@ -371,9 +372,10 @@ class SessionState:
             p = _dev.to_dev(processed_frame)
             _dev.check(L.ss_push_pair(self._handle, position, i.data_ptr(), p.data_ptr(),
                                       _lib.SS_F32, _lib.SS_DEVICE))
-            # the copy is stream-ordered on the session stream (= torch's
-            # current stream at creation); keep the sources alive until then
-            _dev.torch().cuda.current_stream().synchronize()
+            # the copy is stream-ordered on the session stream: keep the
+            # sources (and any converted temporaries) referenced until the next
+            # step, which waits for that stream -- no host wait here
+            self._inflight.append((i, p))
         else:
             i = np.ascontiguousarray(np.asarray(input_frame), dtype=np.float32)
             p = np.ascontiguousarray(np.asarray(processed_frame), dtype=np.float32)
@@ -442,6 +444,7 @@ def _run_step(state: SessionState, flow_backend, with_next: bool, return_host: b
     prm = _dev.params_struct(params)
     t1 = time.perf_counter()
     rc = _lib.lib().ss_step(state.handle, int(with_next), ctypes.byref(prm), ctypes.byref(it))
+    state._inflight.clear()  # ss_step waited for the session stream (pushes included)
     _dev.check(rc, it.value)
     solve_ms = (time.perf_counter() - t1) * 1e3
     tm = _lib.SSTiming()

@@ -606,8 +606,11 @@ int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, 
     // copy into this slot overlaps it unless it evicts one of them
     if (idx == s->side_slots[0] || idx == s->side_slots[1])
         if (int rc = join_side(s)) return rc;
-    if (s->run) s->run->slots[idx].key = -1;  // the frame's cached pyramid is stale
-    if (s->staged_pos == position && I == s->st_hostI && P == s->st_hostP && dtype == SS_F32) {
+    const bool staged = s->staged_pos == position && I == s->st_hostI && P == s->st_hostP && dtype == SS_F32;
+    // the slot's cached pyramid is stale -- unless it is this staged pair's,
+    // computed by ss_step from the staging buffers (keyed by its position)
+    if (s->run && !(staged && s->run->slots[idx].key == position)) s->run->slots[idx].key = -1;
+    if (staged) {
         // staged by ss_stage_pair: swap its buffers into the ring once copied
         SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->st_done, 0));
         std::swap(sl.I, s->stI);
@@ -646,6 +649,10 @@ int ss_stage_pair(ss_session *s, int64_t position, const void *I, const void *P,
         SS_CUDA_TRY(cudaEventCreateWithFlags(&s->st_done, cudaEventDisableTiming));
     }
     if (s->staged_pos >= 0) SS_CUDA_TRY(cudaEventSynchronize(s->st_done));  // unconsumed: overwrite
+    // a pyramid ss_step computed from an earlier staging of this position is stale
+    if (s->run)
+        for (int k = 0; k < 3; ++k)
+            if (s->run->slots[k].key == position) s->run->slots[k].key = -1;
     // the staging buffers were the ring slot the last push evicted: order the
     // upload after session work issued so far (flows may still read it).
     // Uploads use their own stream, so they never queue behind result
@@ -804,6 +811,17 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
         s->side_slots[0] = s->pre_slots[0] = ia;
         s->side_slots[1] = s->pre_slots[1] = ib;
         s->pre_for = tn;
+        // the caller staged frame t+2 (ss_stage_pair): its pyramid too, into
+        // the pyramid slot ss_push_pair will give it -- that of the ring's
+        // oldest frame (t-1), which neither upcoming flow reads -- so the
+        // critical chain of the next step starts when the solver ends
+        if (s->staged_pos == t + 2 && s->n_pairs == 3 && s->slot[s->order[0]].pos == t - 1) {
+            const int idx = s->order[0];
+            cudaStream_t ps = s->hi ? s->hi : s->stream;
+            if (s->hi) SS_CUDA_TRY(cudaStreamWaitEvent(s->hi, s->ev[2], 0));
+            SS_CUDA_TRY(cudaStreamWaitEvent(ps, s->st_done, 0));
+            if (int rc = s->run->pyramid(idx, t + 2, s->stI, s->ci, ps)) return rc;
+        }
         return SS_OK;
     };
     int rc = solve_planar(s->solver, s->A, s->A, s->lapP, s->wc, *p, s->O_new, div_iter, s->stream,

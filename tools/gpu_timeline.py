@@ -56,10 +56,11 @@ for e in evs:
     ks.append({"name": e.name, "start": e.time_range.start, "end": e.time_range.end,
                "stream": getattr(e, "device_resource_id", -1)})
 ks.sort(key=lambda r: r["start"])
-# keep the last step: from the last k_flow_final-free boundary -- use the final third
-t0, t1 = ks[0]["start"], ks[-1]["end"]
-span = (t1 - t0) / 3
-last = [r for r in ks if r["start"] >= t1 - span - 1]
+# the last full step: from the previous step's final kernel (the solver's
+# per-pass maxima readback, k_copy_u32) to the last one
+marks = [r["start"] for r in ks if "k_copy_u32" in r["name"]]
+t_from = marks[-2] if len(marks) >= 2 else ks[0]["start"]
+last = [r for r in ks if r["start"] >= t_from]
 base = last[0]["start"]
 print(f"{len(ks)} kernels in 3 steps; last step {len(last)} kernels, {last[-1]['end'] - base:.1f} us")
 busy = 0.0
