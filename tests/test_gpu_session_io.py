@@ -108,3 +108,62 @@ def test_stage_pair_matches_push(lib):
     assert len(a) == len(b) == 4
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_pipelined_cnn_session_matches_plain(lib):
+    """With the lite CNN attached, ss_step pre-launches the next step's flow to
+    its previous frame and, when the pair after next is staged, that frame's
+    pyramid.  Driving the session that way (flow 0 claimed, staged pushes, a
+    re-staged position, a staged pointer the push does not use) gives outputs
+    bit-identical to plain pushes with every flow computed on demand."""
+    _lib, L = lib
+    import paper_2301_00750_b200 as ss
+
+    h, w = 72, 96
+    rng = np.random.default_rng(11)
+    frames = [np.ascontiguousarray(rng.random((h, w, 3), dtype=np.float32)) for _ in range(8)]
+    alt = np.ascontiguousarray(rng.random((h, w, 3), dtype=np.float32))  # first staging of pos 6
+    net = ss.LiteFlowNet(seed=0)
+    prm = _params(_lib)
+
+    def run(pipelined):
+        sess = ctypes.c_void_p()
+        assert L.ss_session_create(h, w, 3, 3, None, ctypes.byref(sess)) == 0
+        assert L.ss_session_attach_flownet(sess, net.handle()) == 0
+        outs = []
+        it = ctypes.c_int(0)
+        try:
+            for pos in (1, 2):
+                f = frames[pos - 1]
+                assert L.ss_push_pair(sess, pos, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+            for pos in range(3, 9):
+                f = frames[pos - 1]
+                if pipelined:
+                    assert L.ss_session_compute_flow(sess, 0) == 0  # claims the pre-launched flow
+                assert L.ss_push_pair(sess, pos, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+                if not pipelined:
+                    assert L.ss_session_compute_flow(sess, 0) == 0
+                assert L.ss_session_compute_flow(sess, 1) == 0
+                if pipelined and pos < 8:
+                    g = frames[pos]
+                    # pos 6 is first staged with other data (re-staged after
+                    # the step); pos 7's staged copy is not what gets pushed
+                    src = alt if pos == 5 else (g.copy() if pos == 6 else g)
+                    assert L.ss_stage_pair(sess, pos + 1, src.ctypes.data, src.ctypes.data, _lib.SS_F32,
+                                           _lib.SS_HOST) == 0
+                assert L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)) == 0
+                if pipelined and pos == 5:
+                    g = frames[pos]
+                    assert L.ss_stage_pair(sess, pos + 1, g.ctypes.data, g.ctypes.data, _lib.SS_F32,
+                                           _lib.SS_HOST) == 0
+                o = np.empty((h, w, 3), np.float32)
+                assert L.ss_output(sess, o.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+                outs.append(o)
+        finally:
+            L.ss_session_destroy(sess)
+        return outs
+
+    a, b = run(False), run(True)
+    assert len(a) == len(b) == 6
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
