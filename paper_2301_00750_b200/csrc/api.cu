@@ -143,6 +143,9 @@ struct ss_session {
     int64_t staged_pos = -1;
     cudaEvent_t st_src = nullptr, st_done = nullptr;
     cudaStream_t up = nullptr;
+    // the staging buffers have no reader left (their frame's last step
+    // completed): an upload into them needs no ordering after the session
+    bool stage_idle = true;
     std::unique_ptr<dis::Estimator> dis;  // built-in flow (BuiltinFlow)
 };
 
@@ -602,6 +605,8 @@ int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, 
         s->order[2] = idx;
     }
     auto &sl = s->slot[idx];
+    // the evicted frame (position q) is read only by steps <= q + 1
+    const bool evicted_idle = s->n_pairs == 3 && sl.pos + 1 <= s->solved_through;
     // the pending side flow reads the pyramids of two other ring slots; the
     // copy into this slot overlaps it unless it evicts one of them
     if (idx == s->side_slots[0] || idx == s->side_slots[1])
@@ -616,6 +621,7 @@ int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, 
         std::swap(sl.I, s->stI);
         std::swap(sl.P, s->stP);
         s->staged_pos = -1;
+        s->stage_idle = evicted_idle;  // the staging buffers now hold the evicted frame
     } else {
         if (int rc = copy_frame(s, sl.I, I, s->ci, dtype, where)) return rc;
         if (int rc = copy_frame(s, sl.P, P, s->cp, dtype, where)) return rc;
@@ -653,13 +659,16 @@ int ss_stage_pair(ss_session *s, int64_t position, const void *I, const void *P,
     if (s->run)
         for (int k = 0; k < 3; ++k)
             if (s->run->slots[k].key == position) s->run->slots[k].key = -1;
-    // the staging buffers were the ring slot the last push evicted: order the
-    // upload after session work issued so far (flows may still read it).
-    // Uploads use their own stream, so they never queue behind result
-    // downloads on the copy stream.
+    // the staging buffers were the ring slot the last push evicted: unless
+    // that frame's last step has completed (stage_idle), order the upload
+    // after session work issued so far (it may still read them).  Uploads use
+    // their own stream, so they never queue behind result downloads on the
+    // copy stream.
     if (!s->up) SS_CUDA_TRY(cudaStreamCreateWithFlags(&s->up, cudaStreamNonBlocking));
-    SS_CUDA_TRY(cudaEventRecord(s->st_src, s->stream));
-    SS_CUDA_TRY(cudaStreamWaitEvent(s->up, s->st_src, 0));
+    if (!s->stage_idle) {
+        SS_CUDA_TRY(cudaEventRecord(s->st_src, s->stream));
+        SS_CUDA_TRY(cudaStreamWaitEvent(s->up, s->st_src, 0));
+    }
     const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     SS_CUDA_TRY(cudaMemcpyAsync(s->stI, I, px * s->ci * sizeof(float), kind, s->up));
     SS_CUDA_TRY(cudaMemcpyAsync(s->stP, P, px * s->cp * sizeof(float), kind, s->up));
