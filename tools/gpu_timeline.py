@@ -32,11 +32,15 @@ pos = 2
 
 
 def step(k):
+    # bench.py's order: flow 0 (claims the pre-launched one), push (swaps the
+    # staged pair in), flow 1, stage the pair after next, step
     global pos
     pos += 1
     for name, rc in (("flow0", L.ss_session_compute_flow(sess, 0)),
                      ("push", L.ss_push_pair(sess, pos, pool[k % 4][0].data_ptr(), pool[k % 4][1].data_ptr(), 0, 1)),
-                     ("flow1", L.ss_session_compute_flow(sess, 1))):
+                     ("flow1", L.ss_session_compute_flow(sess, 1)),
+                     ("stage", L.ss_stage_pair(sess, pos + 1, pool[(k + 1) % 4][0].data_ptr(),
+                                               pool[(k + 1) % 4][1].data_ptr(), 0, 1))):
         assert rc == 0, (name, L.ss_last_error())
     prm = params_struct(ConsistencyParams())
     it = ctypes.c_int(0)
