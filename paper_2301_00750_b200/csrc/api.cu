@@ -798,7 +798,8 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
     a.wp_out = a.wn_out = nullptr;
     if (int rc = launch_presolve(a, s->ci, s->cp, with_next != 0, s->stream)) return rc;
     SS_CUDA_TRY(cudaEventRecord(s->ev[1], s->stream));
-    // the next step's flow t+1 -> t, launched once the solver is enqueued
+    // the next step's pyramid(t+2) (if staged) and flow t+1 -> t, launched
+    // once the solver is enqueued
     auto prelaunch = [&]() -> int {
         static const bool on = getenv("SS_FLOW_PRELAUNCH") == nullptr || strcmp(getenv("SS_FLOW_PRELAUNCH"), "0");
         if (!on || !with_next || !s->run || !s->side) return SS_OK;
@@ -811,15 +812,6 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
             SS_CUDA_TRY(cudaMalloc(&s->valid_pre, px));
             SS_CUDA_TRY(cudaEventCreate(&s->pre_start));
         }
-        // behind the solver (ev[2] marks its end): the flow would only slow it
-        SS_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev[2], 0));
-        SS_CUDA_TRY(cudaEventRecord(s->pre_start, s->side));
-        if (int rc = s->run->flow(ia, ib, s->uv_pre, s->valid_pre, s->side, 1)) return rc;
-        SS_CUDA_TRY(cudaEventRecord(s->join, s->side));
-        s->side_pending = true;
-        s->side_slots[0] = s->pre_slots[0] = ia;
-        s->side_slots[1] = s->pre_slots[1] = ib;
-        s->pre_for = tn;
         // the caller staged frame t+2 (ss_stage_pair): its pyramid too, into
         // the pyramid slot ss_push_pair will give it -- that of the ring's
         // oldest frame (t-1), which neither upcoming flow reads -- so the
@@ -831,6 +823,17 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
             SS_CUDA_TRY(cudaStreamWaitEvent(ps, s->st_done, 0));
             if (int rc = s->run->pyramid(idx, t + 2, s->stI, s->ci, ps)) return rc;
         }
+        // (flow t+1 -> t gated on the pyramid instead of the solver: 341 -> 330
+        // frames/s -- it then competes with the flow to t+2, the critical one)
+        // behind the solver (ev[2] marks its end): the flow would only slow it
+        SS_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev[2], 0));
+        SS_CUDA_TRY(cudaEventRecord(s->pre_start, s->side));
+        if (int rc = s->run->flow(ia, ib, s->uv_pre, s->valid_pre, s->side, 1)) return rc;
+        SS_CUDA_TRY(cudaEventRecord(s->join, s->side));
+        s->side_pending = true;
+        s->side_slots[0] = s->pre_slots[0] = ia;
+        s->side_slots[1] = s->pre_slots[1] = ib;
+        s->pre_for = tn;
         return SS_OK;
     };
     int rc = solve_planar(s->solver, s->A, s->A, s->lapP, s->wc, *p, s->O_new, div_iter, s->stream,
