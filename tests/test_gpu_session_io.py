@@ -167,3 +167,55 @@ def test_pipelined_cnn_session_matches_plain(lib):
     assert len(a) == len(b) == 6
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_pipelined_cnn_session_divergence_retry(lib):
+    """A step that diverges after its pre-launches (next flow t+1 -> t, staged
+    pyramid) keeps its own flows: retrying it with sane params, then
+    continuing the pipelined loop, matches a session that never diverged."""
+    _lib, L = lib
+    import paper_2301_00750_b200 as ss
+    from paper_2301_00750_b200._dev import params_struct
+    from paper_2301_00750_b200.consistency import ConsistencyParams
+
+    h, w = 72, 96
+    rng = np.random.default_rng(13)
+    frames = [np.ascontiguousarray(rng.random((h, w, 3), dtype=np.float32)) for _ in range(7)]
+    net = ss.LiteFlowNet(seed=0)
+    good = _params(_lib)
+    bad = params_struct(ConsistencyParams(eta=0.9999, lam=1e6, alpha=0.0, iterations=300, k1=0.1, k2=0.1))
+
+    def run(diverge_at):
+        sess = ctypes.c_void_p()
+        assert L.ss_session_create(h, w, 3, 3, None, ctypes.byref(sess)) == 0
+        assert L.ss_session_attach_flownet(sess, net.handle()) == 0
+        outs = []
+        it = ctypes.c_int(0)
+        try:
+            for pos in (1, 2):
+                f = frames[pos - 1]
+                assert L.ss_push_pair(sess, pos, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+            for pos in range(3, 8):
+                f = frames[pos - 1]
+                assert L.ss_session_compute_flow(sess, 0) == 0
+                assert L.ss_push_pair(sess, pos, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+                assert L.ss_session_compute_flow(sess, 1) == 0
+                if pos < 7:
+                    g = frames[pos]
+                    assert L.ss_stage_pair(sess, pos + 1, g.ctypes.data, g.ctypes.data, _lib.SS_F32,
+                                           _lib.SS_HOST) == 0
+                if pos == diverge_at:
+                    rc = L.ss_step(sess, 1, ctypes.byref(bad), ctypes.byref(it))
+                    assert rc == _lib.SS_SOLVER_DIVERGENCE and it.value >= 1
+                assert L.ss_step(sess, 1, ctypes.byref(good), ctypes.byref(it)) == 0
+                o = np.empty((h, w, 3), np.float32)
+                assert L.ss_output(sess, o.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+                outs.append(o)
+        finally:
+            L.ss_session_destroy(sess)
+        return outs
+
+    a, b = run(None), run(4)
+    assert len(a) == len(b) == 5
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
