@@ -77,7 +77,7 @@ int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, in
 int tma_taps_per_stage(int k, int stride, int dil, int cin, int np, int prec);
 int encode_weight_map_bf16(CUtensorMap *m, const void *wt, int kblocks, int rows, int np, int T);
 int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,
-                         int act, float *out, int out_ld, cudaStream_t st);
+                         int act, float *out, int out_ld, cudaStream_t st, int parts = 1);
 int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,
                      float *out, int ld_out, cudaStream_t st);
 int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st);

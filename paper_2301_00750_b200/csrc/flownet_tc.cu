@@ -288,6 +288,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvParams p)
 }
 
 // out[m, n] = act(sum_s ws[s, m, n] + bias[n])
+// ws: [part][split][M][N]; output channel c of part c / N (N % 4 == 0, so a
+// float4 group never straddles parts)
 __global__ void k_splitk_reduce(const float *__restrict__ ws, int splits, int M, int N, int Cout,
                                 const float *__restrict__ bias, int act, float *__restrict__ out,
                                 int out_ld)
@@ -297,9 +299,10 @@ __global__ void k_splitk_reduce(const float *__restrict__ ws, int splits, int M,
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long)M * n4) return;
     const int m = (int)(i / n4), n = (int)(i - (long)m * n4) * 4;
+    const int part = n / N, nn = n - part * N;
     // partials are added in split order; their loads are issued eight at a
     // time (a serial load -> add chain would pay one L2 round trip per split)
-    const float *src = ws + (size_t)m * N + n;
+    const float *src = ws + ((size_t)part * splits * M + m) * N + nn;
     const size_t stride = (size_t)M * N;
     float4 acc = *reinterpret_cast<const float4 *>(src);
     int s = 1;
@@ -333,8 +336,12 @@ __global__ void k_splitk_reduce(const float *__restrict__ ws, int splits, int M,
 }
 
 int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,
-                         int act, float *out, int out_ld, cudaStream_t st)
+                         int act, float *out, int out_ld, cudaStream_t st, int parts)
 {
+    if (parts > 1 && N % 4 != 0) {
+        set_error("split-K reduce: part width must be a multiple of 4");
+        return SS_VALUE_ERROR;
+    }
     const long n = (long)M * ((Cout + 3) / 4);
     return launch_pdl("k_splitk_reduce", k_splitk_reduce, dim3(blocks_for(n, 128)), dim3(128), 0, st, ws, splits,
                       M, N, Cout, bias, act, out, out_ld);

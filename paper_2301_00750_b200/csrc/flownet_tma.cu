@@ -71,10 +71,26 @@ struct ConvArgs {
     int tiles_x, n_tiles, nk_all, k_per_split, units;
     int a_box, a_slot, na, halo_w, ph_bytes;  // ph_bytes: one phase region (amode 2)
     int np, part_row, Cout, act, out_ld, stages, b_stage, b_res;
+    int parts, splits, part_rows;  // output-channel parts of np channels; weight rows per part
     const float *bias;
     float *out;
-    float *ws;  // split-K partials [split][M][np] (null: final output)
+    float *ws;  // split-K partials [part][split][M][np] (null: final output)
 };
+
+// unit u -> (part, split, tile): units = parts * splits * n_tiles
+struct ConvUnit {
+    int tile, split, part;
+};
+__device__ __forceinline__ ConvUnit conv_unit(const ConvArgs &a, int u)
+{
+    const int per = a.n_tiles * a.splits;
+    ConvUnit r;
+    r.part = u / per;
+    const int rem = u - r.part * per;
+    r.split = rem / a.n_tiles;
+    r.tile = rem - r.split * a.n_tiles;
+    return r;
+}
 
 __device__ __forceinline__ float lk(float v) { return v >= 0.f ? v : 0.1f * v; }
 
@@ -200,7 +216,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         pdl_wait();  // the activations are the previous kernel's output
         uint32_t ga = 0, gb = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const int tile = u % a.n_tiles, split = u / a.n_tiles;
+            const ConvUnit cu = conv_unit(a, u);
+            const int tile = cu.tile, split = cu.split, prow = a.part_row + cu.part * a.part_rows;
             int x0, y0;
             if (AMODE == 0) {
                 const int m0 = tile * 128, oy = m0 / a.W, ox = m0 - oy * a.W;
@@ -242,7 +259,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     mbar_wait(&b_empty[s], ((gb / S) & 1) ^ 1);
                     if (elect_one()) {
                         mbar_expect_tx(&b_full[s], (uint32_t)a.b_stage);
-                        tma_tile_3d(smem_u32(bst + s * a.b_stage), &tmB, 0, a.part_row, cb * a.taps + tap0,
+                        tma_tile_3d(smem_u32(bst + s * a.b_stage), &tmB, 0, prow, cb * a.taps + tap0,
                                     &b_full[s]);
                     }
                     __syncwarp();
@@ -265,7 +282,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         if (BRES) mbar_wait(&b_full[0], 0);
         uint32_t ga = 0, gb = 0, uc = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
-            const int split = u / a.n_tiles;
+            const int split = conv_unit(a, u).split;
             const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
             const uint32_t acc = uc & 1;
             mbar_wait(&acc_empty[acc], ((uc >> 1) & 1) ^ 1);
@@ -336,7 +353,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             const uint32_t acc = uc & 1;
             mbar_wait(&acc_full[acc], (uc >> 1) & 1);
             tc_fence_after();
-            const int tile = u % a.n_tiles, split = u / a.n_tiles;
+            const ConvUnit cu = conv_unit(a, u);
+            const int tile = cu.tile, split = cu.split;
+            const int cout = min(np, a.Cout - cu.part * np);  // this part's live channels
+            const float *bias = a.bias + cu.part * np;
+            float *outp = a.out + cu.part * np;
             const int m = q * 32 + lane;
             bool ok;
             size_t pix;
@@ -361,25 +382,25 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 }
                 if (!ok) continue;
                 if (a.ws) {
-                    float *dst = a.ws + ((size_t)split * a.M + pix) * np + c0;
+                    float *dst = a.ws + (((size_t)cu.part * a.splits + split) * a.M + pix) * np + c0;
 #pragma unroll
                     for (int i = 0; i < 16; i += 4)
                         *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                } else if (c0 < a.Cout) {
-                    float *dst = a.out + pix * a.out_ld + c0;
+                } else if (c0 < cout) {
+                    float *dst = outp + pix * a.out_ld + c0;
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
-                        const float x = v[i] + (c0 + i < a.Cout ? __ldg(a.bias + c0 + i) : 0.f);
+                        const float x = v[i] + (c0 + i < cout ? __ldg(bias + c0 + i) : 0.f);
                         v[i] = a.act ? lk(x) : x;
                     }
-                    if (c0 + 16 <= a.Cout) {
+                    if (c0 + 16 <= cout) {
 #pragma unroll
                         for (int i = 0; i < 16; i += 4)
                             *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                     } else {
 #pragma unroll
                         for (int i = 0; i < 16; ++i)
-                            if (i < a.Cout - c0) dst[i] = v[i];
+                            if (i < cout - c0) dst[i] = v[i];
                     }
                 }
             }
@@ -393,7 +414,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         const int n16 = a.a_slot / 16;  // whole slot (phase padding included)
         uint32_t ga = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const int split = u / a.n_tiles;
+            const int split = conv_unit(a, u).split;
             const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
             int grp = kb % a.sp_cb;
             for (int st = kb; st < ke; ++st) {
@@ -617,8 +638,10 @@ int prepare_conv_tma()
 }
 
 // one output-channel part (rows [part * 2 np, +2 np) of the weight tensor)
-static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int prec, int amode, int cpp, int halo_w,
-                       int halo_h, int part, int np, cudaStream_t st)
+// all output-channel parts of np channels in one launch (units cover parts x
+// splits x tiles; part p uses weight rows [p * part_rows, +part_rows))
+static int launch_parts(const ConvParams &p, const CUtensorMap &tmA, int prec, int amode, int cpp, int halo_w,
+                        int halo_h, int parts, int np, cudaStream_t st)
 {
     ConvArgs a;
     a.amode = amode;
@@ -661,17 +684,20 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int prec, in
     }
     a.nk_all = a.ncb * a.sp_cb;
     a.np = np;
-    a.part_row = part * (prec ? 2 : 1) * np;
-    a.Cout = std::min(np, p.Cout - part * np);
+    a.parts = parts;
+    a.part_row = 0;
+    a.part_rows = (prec ? 2 : 1) * np;
+    a.Cout = p.Cout;  // all parts
     a.act = p.act;
     a.out_ld = p.out_ld;
-    a.bias = p.bias + part * np;
-    a.out = p.out + part * np;
+    a.bias = p.bias;
+    a.out = p.out;
     a.b_stage = prec ? a.T * 2 * np * 128 : a.T * np * 64;  // [hi; lo] fp32 rows | bf16 rows
     const int bar_bytes = 1024 + 512;
     // weights resident for the whole launch when every stage fits
     static const bool res_on = getenv("SS_CONV_BRES") == nullptr || strcmp(getenv("SS_CONV_BRES"), "0");
-    a.b_res = res_on && 2 * a.na * a.a_slot + a.nk_all * a.b_stage + bar_bytes + a.nk_all * 16 <= SMEM_MAX;
+    a.b_res = res_on && parts == 1 &&
+              2 * a.na * a.a_slot + a.nk_all * a.b_stage + bar_bytes + a.nk_all * 16 <= SMEM_MAX;
     if (a.b_res) {
         a.stages = a.nk_all;
     } else {
@@ -704,16 +730,18 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int prec, in
     int splits = 1;
     static const int sk_f = getenv("SS_SPLITK_F") ? std::max(1, atoi(getenv("SS_SPLITK_F"))) : 4;
     static const int sk_max = getenv("SS_SPLITK_MAX") ? std::max(1, atoi(getenv("SS_SPLITK_MAX"))) : 8;
-    if (p.ws && a.n_tiles * sk_f < n_sm_tma && a.nk_all >= 4) {
-        splits = std::min(std::min((n_sm_tma + a.n_tiles - 1) / a.n_tiles, a.nk_all / 2), sk_max);
-        const size_t need = (size_t)splits * a.M * np;
-        if (need > p.ws_floats) splits = (int)(p.ws_floats / ((size_t)a.M * np));
+    const int tiles_all = a.n_tiles * parts;
+    if (p.ws && tiles_all * sk_f < n_sm_tma && a.nk_all >= 4) {
+        splits = std::min(std::min((n_sm_tma + tiles_all - 1) / tiles_all, a.nk_all / 2), sk_max);
+        const size_t need = (size_t)parts * splits * a.M * np;
+        if (need > p.ws_floats) splits = (int)(p.ws_floats / ((size_t)parts * a.M * np));
         splits = std::max(splits, 1);
     }
     a.k_per_split = (a.nk_all + splits - 1) / splits;
     splits = (a.nk_all + a.k_per_split - 1) / a.k_per_split;
+    a.splits = splits;
     a.ws = splits > 1 ? p.ws : nullptr;
-    a.units = a.n_tiles * splits;
+    a.units = tiles_all * splits;
     const int grid = std::min(a.units, p.grid_cap > 0 ? std::min(p.grid_cap, n_sm_tma) : n_sm_tma);
     const size_t smem = (size_t)2 * a.na * a.a_slot + (size_t)a.stages * a.b_stage + bar_bytes + a.stages * 16;
     const CUtensorMap &tmB = *static_cast<const CUtensorMap *>(p.tmB);
@@ -721,7 +749,7 @@ static int launch_part(const ConvParams &p, const CUtensorMap &tmA, int prec, in
                               smem, st, tmA, tmB, a);
     if (rc) return rc;
     if (splits > 1)
-        return launch_splitk_reduce(p.ws, splits, a.M, np, a.Cout, a.bias, p.act, a.out, p.out_ld, st);
+        return launch_splitk_reduce(p.ws, splits, a.M, np, p.Cout, p.bias, p.act, p.out, p.out_ld, st, parts);
     return SS_OK;
 }
 
@@ -749,9 +777,7 @@ int launch_conv_tma(const ConvParams &p, int prec, cudaStream_t st)
     if (int rc = encode_act_map(&tmA, p, amode, cpp, halo_w, halo_h)) return rc;
     const int parts = (p.Cout_pad + 127) / 128;
     const int np = p.Cout_pad / parts;
-    for (int part = 0; part < parts; ++part)
-        if (int rc = launch_part(p, tmA, prec, amode, cpp, halo_w, halo_h, part, np, st)) return rc;
-    return SS_OK;
+    return launch_parts(p, tmA, prec, amode, cpp, halo_w, halo_h, parts, np, st);
 }
 
 }  // namespace fn
