@@ -539,7 +539,8 @@ int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x,
     const size_t smem = 2 * (CR_W2F + CR_F1F) * sizeof(float);  // sized for DY = 3
     if (int rc = prepare_flow_kernels()) return rc;
     const int tiles = ((W + CR_TW - 1) / CR_TW) * ((H + CR_TH - 1) / CR_TH);
-    if (tiles < 64) {
+    static const int coarse_tiles = getenv("SS_CORR_COARSE_TILES") ? atoi(getenv("SS_CORR_COARSE_TILES")) : 64;
+    if (tiles < coarse_tiles) {
         const dim3 grid((W + CR_TW - 1) / CR_TW, (H + CR_TH - 1) / CR_TH, 9);
         return launch_pdl("k_corr", k_corr<1, CR_CS_COARSE>, grid, dim3(64 * CR_CS_COARSE), smem, st, f1, w2, C, H,
                           W, x, xld, copy_f1 ? 1 : 0);
