@@ -577,7 +577,17 @@ int ss_session_reset(ss_session *s)
 
 void *ss_session_stream(const ss_session *s) { return (void *)s->stream; }
 
-int ss_session_join(ss_session *s) { return join_side(s); }
+int ss_session_join(ss_session *s)
+{
+    // everything the session has in flight on its internal streams (the side
+    // flow, and the high-priority chain incl. a pre-launched pyramid)
+    if (int rc = join_side(s)) return rc;
+    if (s->hi) {
+        SS_CUDA_TRY(cudaEventRecord(s->hjoin, s->hi));
+        SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->hjoin, 0));
+    }
+    return SS_OK;
+}
 
 int ss_push_pair(ss_session *s, int64_t position, const void *I, const void *P, int dtype,
                  int where)

@@ -16,6 +16,7 @@ from paper_2301_00750_b200.consistency import ConsistencyParams
 from paper_2301_00750_b200.synthetic import DeviceSequence
 
 prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+E2E = os.environ.get("TL_E2E") is not None  # bench.py's e2e loop: pinned host staging + async output
 h = int(sys.argv[2]) if len(sys.argv) > 2 else 1080
 w = int(sys.argv[3]) if len(sys.argv) > 3 else 1920
 out_path = sys.argv[4] if len(sys.argv) > 4 else None
@@ -29,9 +30,28 @@ st.push_pair(2, pool[1][0], pool[1][1])
 sess = st.handle
 L.ss_session_attach_flownet(sess, net.handle())
 pos = 2
+host = [(p[0].cpu().pin_memory(), p[1].cpu().pin_memory()) for p in pool]
+outs = [torch.empty((h, w, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+
+
+def step_e2e(k):
+    global pos
+    pos += 1
+    for name, rc in (("flow0", L.ss_session_compute_flow(sess, 0)),
+                     ("push", L.ss_push_pair(sess, pos, host[k % 4][0].data_ptr(), host[k % 4][1].data_ptr(), 0, 0)),
+                     ("flow1", L.ss_session_compute_flow(sess, 1)),
+                     ("stage", L.ss_stage_pair(sess, pos + 1, host[(k + 1) % 4][0].data_ptr(),
+                                               host[(k + 1) % 4][1].data_ptr(), 0, 0))):
+        assert rc == 0, (name, L.ss_last_error())
+    prm = params_struct(ConsistencyParams())
+    it = ctypes.c_int(0)
+    assert L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)) == 0, L.ss_last_error()
+    assert L.ss_output_async(sess, outs[k % 2].data_ptr(), 0, 0) == 0
 
 
 def step(k):
+    if E2E:
+        return step_e2e(k)
     # bench.py's order: flow 0 (claims the pre-launched one), push (swaps the
     # staged pair in), flow 1, stage the pair after next, step
     global pos
