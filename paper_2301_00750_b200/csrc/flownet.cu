@@ -555,15 +555,30 @@ int Run::pyramid_impl(int slot, const float *img, int c, cudaStream_t st)
     ws_floats_ = ws_floats;
     int rc;
     prof.mark("start", st);
-    if ((rc = launch_prep(img, h, w, c, H[0], W[0], prep, st))) return rc;
-    prof.mark("prep", st);
+    // the frame -> level-1 "a" layer in one FFMA pass (SS_PYR1A_FUSED=0: the
+    // 8-channel padded copy + tensor-core conv)
+    static const bool fused = getenv("SS_PYR1A_FUSED") == nullptr || strcmp(getenv("SS_PYR1A_FUSED"), "0");
+    if (fused) {
+        const LayerDev &L1a = wts->L(pyr_idx(1, 0));
+        if ((rc = launch_prep_pyr1a(img, h, w, c, H[0], W[0], H[1], W[1], L1a.w, L1a.cout_pad, L1a.b, s0, st)))
+            return rc;
+        prof.mark("prep+pyr1a", st);
+    } else {
+        if ((rc = launch_prep(img, h, w, c, H[0], W[0], prep, st))) return rc;
+        prof.mark("prep", st);
+    }
     const float *in = prep;
     int in_ld = 8;
     for (int l = 1; l <= 6; ++l) {
         const int C = PYR_CH[l - 1];
         const std::string tag = "pyr" + std::to_string(l);
         float *a = in == s0 ? s1 : s0;
-        if ((rc = convp((tag + "a").c_str(), wts->L(pyr_idx(l, 0)), in, in_ld, H[l - 1], W[l - 1], a, C, st))) return rc;
+        if (l == 1 && fused) {
+            a = s0;  // written by k_prep_pyr1a
+        } else if ((rc = convp((tag + "a").c_str(), wts->L(pyr_idx(l, 0)), in, in_ld, H[l - 1], W[l - 1], a, C,
+                               st))) {
+            return rc;
+        }
         float *b = a == s0 ? s1 : s0;
         if ((rc = convp((tag + "b").c_str(), wts->L(pyr_idx(l, 1)), a, C, H[l], W[l], b, C, st))) return rc;
         float *c3 = l <= 2 ? a : sl.lvl[l];

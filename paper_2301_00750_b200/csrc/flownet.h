@@ -80,6 +80,8 @@ int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, co
                          int act, float *out, int out_ld, cudaStream_t st, int parts = 1);
 int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,
                      float *out, int ld_out, cudaStream_t st);
+int launch_prep_pyr1a(const float *img, int h, int w, int c, int H0, int W0, int H1, int W1, const float *wgt,
+                      int cout_pad, const float *bias, float *out, cudaStream_t st);  // k_prep + pyr1a fused
 int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out, cudaStream_t st);
 int launch_up2_warp(const float *coarse, int cld, int Hc, int Wc, const float *f2, int C, int H,
                     int W, float *x, int xld, float *w2, cudaStream_t st);

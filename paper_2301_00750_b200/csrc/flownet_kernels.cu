@@ -189,7 +189,11 @@ int launch_conv_ffma(const ConvParams &p, cudaStream_t st)
 // A thread owns 4 channels x DW_PX horizontally adjacent pixels: its 9 weight
 // float4 stay in registers, and all 9 x DW_PX input loads of a row are issued
 // before the FMAs (memory-level parallelism; neighbours hit L1).
+#ifndef DW_PX_OVERRIDE
 constexpr int DW_PX = 4;
+#else
+constexpr int DW_PX = DW_PX_OVERRIDE;
+#endif
 
 __global__ void __launch_bounds__(256) k_depthwise(const float *__restrict__ in, int ld, int H, int W, int C,
                                                   const float *__restrict__ w, int dil, float *__restrict__ out,
@@ -274,6 +278,78 @@ int launch_prep(const float *img, int h, int w, int c, int H, int W, float *out,
 {
     return launch_pdl("k_prep", k_prep, dim3(blocks_for((long)H * W, 256)), dim3(256), 0, st, img, h, w, c, H, W,
                       out);
+}
+
+// ---------------------------------------------------------------------------
+// Network input + first pyramid layer in one pass: pyr1a is a stride-2 3x3
+// conv from the 3 live input channels (RGB - 0.5, replicate-padded to the
+// 64-multiple size H0 x W0, zero conv padding outside it) to 16 channels +
+// LeakyReLU.  One thread per level-1 pixel, fp32 FFMA over its 27 live taps,
+// weights (rows of the 8-channel padded table: channels 0..2) in shared
+// memory.  Replaces k_prep (an 8-channel padded copy of the frame) and a
+// tensor-core launch that padded K from 27 to 72.
+__global__ void __launch_bounds__(256) k_prep_pyr1a(const float *__restrict__ img, int h, int w, int c, int H0,
+                                                   int W0, int H1, int W1, const float *__restrict__ wgt,
+                                                   int cout_pad, const float *__restrict__ bias,
+                                                   float *__restrict__ out)
+{
+    __shared__ __align__(16) float ws[27 * 16];
+    __shared__ float bs[16];
+    for (int i = threadIdx.x; i < 27 * 16; i += blockDim.x) {
+        const int tc = i / 16, co = i - tc * 16, tap = tc / 3, ch = tc - tap * 3;
+        ws[i] = wgt[(long)(tap * 8 + ch) * cout_pad + co];
+    }
+    if (threadIdx.x < 16) bs[threadIdx.x] = bias[threadIdx.x];
+    pdl_wait();
+    __syncthreads();
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)H1 * W1) return;
+    const int oy = (int)(i / W1), ox = (int)(i - (long)oy * W1);
+    float acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = 0.f;
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky) {
+        const int iy = 2 * oy + ky - 1;
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+            const int ix = 2 * ox + kx - 1;
+            if (iy < 0 || iy >= H0 || ix < 0 || ix >= W0) continue;  // conv zero padding
+            const long q = (long)min(iy, h - 1) * w + min(ix, w - 1);  // replicate padding
+            float v[3];
+            if (c == 3) {
+                v[0] = __ldg(img + q * 3) - 0.5f;
+                v[1] = __ldg(img + q * 3 + 1) - 0.5f;
+                v[2] = __ldg(img + q * 3 + 2) - 0.5f;
+            } else {
+                v[0] = v[1] = v[2] = __ldg(img + q) - 0.5f;
+            }
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                const float4 *wr = reinterpret_cast<const float4 *>(ws + ((ky * 3 + kx) * 3 + ch) * 16);
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4) {
+                    const float4 u = wr[k4];
+                    acc[4 * k4] = fmaf(v[ch], u.x, acc[4 * k4]);
+                    acc[4 * k4 + 1] = fmaf(v[ch], u.y, acc[4 * k4 + 1]);
+                    acc[4 * k4 + 2] = fmaf(v[ch], u.z, acc[4 * k4 + 2]);
+                    acc[4 * k4 + 3] = fmaf(v[ch], u.w, acc[4 * k4 + 3]);
+                }
+            }
+        }
+    }
+    float4 *dst = reinterpret_cast<float4 *>(out + i * 16);
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4)
+        dst[k4] = make_float4(leaky(acc[4 * k4] + bs[4 * k4]), leaky(acc[4 * k4 + 1] + bs[4 * k4 + 1]),
+                              leaky(acc[4 * k4 + 2] + bs[4 * k4 + 2]), leaky(acc[4 * k4 + 3] + bs[4 * k4 + 3]));
+}
+
+int launch_prep_pyr1a(const float *img, int h, int w, int c, int H0, int W0, int H1, int W1, const float *wgt,
+                      int cout_pad, const float *bias, float *out, cudaStream_t st)
+{
+    return launch_pdl("k_prep_pyr1a", k_prep_pyr1a, dim3(blocks_for((long)H1 * W1, 256)), dim3(256), 0, st, img, h,
+                      w, c, H0, W0, H1, W1, wgt, cout_pad, bias, out);
 }
 
 // ---------------------------------------------------------------------------
