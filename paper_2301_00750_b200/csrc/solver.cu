@@ -464,10 +464,26 @@ __global__ void __launch_bounds__(blk::THREADS, 1)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // the previous pass's iterates (and everything before it) are complete
-    // and visible past this point
+    // the first tile's constant inputs (A, lapP, w_c: written before the
+    // first pass) load while the previous pass drains; its iterates only
+    // after the wait, which makes them complete and visible
+    if (tid == 0 && (int)blockIdx.x < ntiles) {
+        const int t = blockIdx.x;
+        const int ch = t / (ntx * nty), rem = t - ch * ntx * nty;
+        const int ty = rem / ntx, tx = rem - ty * ntx;
+        const int x = tx * OW - K, y = ty * OH - K;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :
+                     : "r"(smem_u32(bar)), "r"((uint32_t)(5 * STAGE * sizeof(float)))
+                     : "memory");
+        tma_load_3d(stage + 2 * STAGE, &maps.A, x, y, ch, bar);
+        tma_load_3d(stage + 3 * STAGE, &maps.L, x, y, ch, bar);
+        tma_load_2d(stage + 4 * STAGE, &maps.W, x, y, bar);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        tma_load_3d(stage + 0 * STAGE, &maps.O, x, y, ch, bar);
+        tma_load_3d(stage + 1 * STAGE, &maps.Op, x, y, ch, bar);
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (tid == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
     __syncthreads();
 
     const int p = threadIdx.x, s = threadIdx.y;
