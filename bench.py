@@ -49,8 +49,8 @@ SOLVER_K = 8  # iterations per temporally-blocked solver pass (csrc/solver.cu)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--flow", default="fp32", choices=["fp32", "bf16", "dis", "constant"])
     ap.add_argument("--height", type=int, default=H)
