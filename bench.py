@@ -187,6 +187,9 @@ def run_reference(args, rank, world):
         return
     h, w = args.height, args.width
     steps = max(1, min(args.steps, 3))
+    warm = 1 if args.warmup > 0 else 0  # one untimed sample (each is ~4 s of CPU work)
+    for _ in range(warm):
+        _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
     secs, cores, sample = [], 0, ""
     for _ in range(steps):
         s, cores, sample = _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
@@ -195,7 +198,7 @@ def run_reference(args, rank, world):
     fps = 1.0 / sec
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(fps, 5), "unit": "frames/s",
-        "n_gpus": world, "steps": len(secs), "warmup": 0, "ms_per_step": round(sec * 1e3, 1),
+        "n_gpus": world, "steps": len(secs), "warmup": warm, "ms_per_step": round(sec * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": f"{w}x{h} single stream, default preset, 150 iterations, "
