@@ -146,7 +146,8 @@ struct ss_session {
     // the staging buffers have no reader left (their frame's last step
     // completed): an upload into them needs no ordering after the session
     bool stage_idle = true;
-    std::unique_ptr<dis::Estimator> dis;  // built-in flow (BuiltinFlow)
+    std::unique_ptr<dis::Estimator> dis;   // built-in flow (BuiltinFlow)
+    std::unique_ptr<dis::Estimator> dis0;  // its flow to t-1, on the side stream
 };
 
 // session-stream work that touches what the side-stream flow reads or writes
@@ -236,6 +237,7 @@ static void session_free(ss_session *s)
     cudaFree(s->stP);
     s->run.reset();
     s->dis.reset();
+    s->dis0.reset();
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
 
@@ -1062,18 +1064,43 @@ int ss_session_compute_dis_flow(ss_session *s, int which, int levels, int patch,
                   " are not buffered");
         return SS_VALUE_ERROR;
     }
-    if (int rc = join_side(s)) return rc;
+    // the flow to t-1 runs on the side stream with its own estimator,
+    // concurrently with the flow to t+1 on the session stream
+    // (SS_DIS_CONCURRENT=0: both on the session stream)
+    static const bool conc = getenv("SS_DIS_CONCURRENT") == nullptr || strcmp(getenv("SS_DIS_CONCURRENT"), "0");
+    const bool side = conc && which == 0;
+    if (which == 0 || !conc)
+        if (int rc = join_side(s)) return rc;  // a pending side flow (its buffers / slots)
+    if (which == 0) s->side_pending = false;
     const dis::Options o = dis_options(levels, patch, iters, downscale);
-    if (!s->dis || !same_opts(s->dis->opts, o)) {
-        s->dis.reset(new dis::Estimator());
-        if (int rc = s->dis->init(s->h, s->w, o)) {
-            s->dis.reset();
+    std::unique_ptr<dis::Estimator> &est = side ? s->dis0 : s->dis;
+    if (!est || !same_opts(est->opts, o)) {
+        est.reset(new dis::Estimator());
+        if (int rc = est->init(s->h, s->w, o)) {
+            est.reset();
             return rc;
         }
     }
     if (which == 0 || !s->flow_timed) SS_CUDA_TRY(cudaEventRecord(s->fev[0], s->stream));
-    if (int rc = s->dis->run(a->I, b->I, s->ci, s->uv[which], s->valid[which], s->stream)) return rc;
-    SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->stream));
+    if (side) {
+        if (!s->side) {
+            SS_CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+            SS_CUDA_TRY(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming));
+            SS_CUDA_TRY(cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming));
+        }
+        SS_CUDA_TRY(cudaEventRecord(s->fork, s->stream));
+        SS_CUDA_TRY(cudaStreamWaitEvent(s->side, s->fork, 0));
+        if (int rc = est->run(a->I, b->I, s->ci, s->uv[0], s->valid[0], s->side)) return rc;
+        SS_CUDA_TRY(cudaEventRecord(s->join, s->side));
+        SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->side));
+        s->side_pending = true;
+        s->side_slots[0] = (int)(a - s->slot);
+        s->side_slots[1] = (int)(b - s->slot);
+    } else {
+        if (int rc = est->run(a->I, b->I, s->ci, s->uv[which], s->valid[which], s->stream)) return rc;
+        if (int rc = join_side(s)) return rc;  // fev[1] marks the end of both flows
+        SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->stream));
+    }
     s->flow_timed = true;
     s->flow_for[which] = t;
     return SS_OK;
