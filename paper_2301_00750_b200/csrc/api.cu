@@ -128,6 +128,8 @@ struct ss_session {
     cudaEvent_t pre_start = nullptr;
     int64_t pre_for = -1;  // step position the pre-launched flow is for
     int pre_slots[2] = {-1, -1};
+    int pre_kind = 0;        // 1: lite CNN, 2: DIS (s->dis0)
+    bool dis_used = false;   // this step's flow to t-1 came from ss_session_compute_dis_flow
     // asynchronous output (ss_output_async): device->host copy on its own
     // stream, overlapping the next step; the solver that would next overwrite
     // the copied buffer waits for it
@@ -569,6 +571,7 @@ int ss_session_reset(ss_session *s)
     s->side_pending = false;
     s->flow_timed = false;
     s->pre_for = -1;
+    s->dis_used = false;
     s->n_pairs = 0;
     s->has_output = false;
     s->solved_through = 0;
@@ -716,6 +719,7 @@ int ss_set_flow(ss_session *s, int which, const float *uv, const uint8_t *valid,
         return SS_VALUE_ERROR;
     }
     if (int rc = join_side(s)) return rc;
+    if (which == 0) s->dis_used = false;
     const size_t px = (size_t)s->h * s->w;
     const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     SS_CUDA_TRY(cudaMemcpyAsync(s->uv[which], uv, px * 2 * sizeof(float), kind, s->stream));
@@ -737,6 +741,7 @@ int ss_set_constant_flow(ss_session *s, int which, double u, double v, int steps
     const float fu = (float)(u * steps), fv = (float)(v * steps);
     const long px = (long)s->h * s->w;
     if (int rc = join_side(s)) return rc;
+    if (which == 0) s->dis_used = false;
     k_fill_flow<<<blocks_for(px, 256), 256, 0, s->stream>>>(s->uv[which], s->valid[which], px, fu, fv);
     SS_LAUNCH_CHECK("k_fill_flow");
     s->flow_for[which] = s->solved_through + 1;
@@ -814,9 +819,29 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
     // once the solver is enqueued
     auto prelaunch = [&]() -> int {
         static const bool on = getenv("SS_FLOW_PRELAUNCH") == nullptr || strcmp(getenv("SS_FLOW_PRELAUNCH"), "0");
-        if (!on || !with_next || !s->run || !s->side) return SS_OK;
+        if (!on || !with_next || !s->side) return SS_OK;
         const int64_t tn = t + 1;
         const int ia = (int)(next - s->slot), ib = (int)(cur - s->slot);
+        const size_t npx = (size_t)s->h * s->w;
+        if (!s->run) {
+            // DIS provider: its flow t+1 -> t on the side estimator, behind the solver
+            if (!s->dis_used || !s->dis0) return SS_OK;
+            if (!s->uv_pre) {
+                SS_CUDA_TRY(cudaMalloc(&s->uv_pre, npx * 2 * sizeof(float)));
+                SS_CUDA_TRY(cudaMalloc(&s->valid_pre, npx));
+                SS_CUDA_TRY(cudaEventCreate(&s->pre_start));
+            }
+            SS_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev[2], 0));
+            SS_CUDA_TRY(cudaEventRecord(s->pre_start, s->side));
+            if (int rc = s->dis0->run(next->I, cur->I, s->ci, s->uv_pre, s->valid_pre, s->side)) return rc;
+            SS_CUDA_TRY(cudaEventRecord(s->join, s->side));
+            s->side_pending = true;
+            s->side_slots[0] = s->pre_slots[0] = ia;
+            s->side_slots[1] = s->pre_slots[1] = ib;
+            s->pre_for = tn;
+            s->pre_kind = 2;
+            return SS_OK;
+        }
         if (s->run->slots[ia].key != tn || s->run->slots[ib].key != t) return SS_OK;  // pyramids not cached
         const size_t px = (size_t)s->h * s->w;
         if (!s->uv_pre) {
@@ -846,6 +871,7 @@ int ss_step(ss_session *s, int with_next, const ss_params *p, int *div_iter)
         s->side_slots[0] = s->pre_slots[0] = ia;
         s->side_slots[1] = s->pre_slots[1] = ib;
         s->pre_for = tn;
+        s->pre_kind = 1;
         return SS_OK;
     };
     int rc = solve_planar(s->solver, s->A, s->A, s->lapP, s->wc, *p, s->O_new, div_iter, s->stream,
@@ -1069,6 +1095,20 @@ int ss_session_compute_dis_flow(ss_session *s, int which, int levels, int patch,
     // (SS_DIS_CONCURRENT=0: both on the session stream)
     static const bool conc = getenv("SS_DIS_CONCURRENT") == nullptr || strcmp(getenv("SS_DIS_CONCURRENT"), "0");
     const bool side = conc && which == 0;
+    const dis::Options o0 = dis_options(levels, patch, iters, downscale);
+    if (which == 0 && s->pre_for == t && s->pre_kind == 2 && s->pre_slots[0] == (int)(a - s->slot) &&
+        s->pre_slots[1] == (int)(b - s->slot) && s->dis0 && same_opts(s->dis0->opts, o0)) {
+        // pre-launched by the previous ss_step: claim it (side_pending stays set)
+        std::swap(s->uv[0], s->uv_pre);
+        std::swap(s->valid[0], s->valid_pre);
+        std::swap(s->fev[0], s->pre_start);
+        s->pre_for = -1;
+        s->flow_timed = true;
+        s->flow_for[0] = t;
+        s->dis_used = true;
+        return SS_OK;
+    }
+    if (which == 0) s->dis_used = side;
     if (which == 0 || !conc)
         if (int rc = join_side(s)) return rc;  // a pending side flow (its buffers / slots)
     if (which == 0) s->side_pending = false;
@@ -1135,7 +1175,7 @@ int ss_session_compute_flow(ss_session *s, int which)
         return SS_VALUE_ERROR;
     }
     const int ia = (int)(a - s->slot), ib = (int)(b - s->slot);
-    if (which == 0 && s->pre_for == t && s->pre_slots[0] == ia && s->pre_slots[1] == ib &&
+    if (which == 0 && s->pre_for == t && s->pre_kind == 1 && s->pre_slots[0] == ia && s->pre_slots[1] == ib &&
         s->run->slots[ia].key == t && s->run->slots[ib].key == other) {
         // pre-launched by the previous ss_step: claim it (it may still be
         // running on the side stream; side_pending stays set)
@@ -1147,6 +1187,7 @@ int ss_session_compute_flow(ss_session *s, int which)
         s->flow_for[0] = t;
         return SS_OK;
     }
+    s->dis_used = false;
     if (which == 0 || !s->flow_timed) {
         if (which == 0 && s->side_pending) {  // a second flow to the previous frame
             if (int rc = join_side(s)) return rc;

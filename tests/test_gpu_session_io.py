@@ -219,3 +219,58 @@ def test_pipelined_cnn_session_divergence_retry(lib):
     assert len(a) == len(b) == 5
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_pipelined_dis_session_matches_stateless_flows(lib):
+    """With the built-in DIS flow, ss_step pre-launches the next step's flow
+    t+1 -> t on the side estimator and ss_session_compute_dis_flow(0) claims
+    it.  That loop gives outputs bit-identical to flows computed by the
+    stateless estimator and installed with ss_set_flow (no pre-launch)."""
+    _lib, L = lib
+    torch = pytest.importorskip("torch")
+    h, w = 64, 96
+    gen = torch.Generator(device="cpu").manual_seed(17)
+    I = [torch.rand(h, w, 3, generator=gen).cuda().contiguous() for _ in range(7)]
+    P = [torch.rand(h, w, 3, generator=gen).cuda().contiguous() for _ in range(7)]
+    opts = (5, 9, 4, 1)  # levels, patch, iterations, downscale (FlowOptions defaults)
+    prm = _params(_lib)
+
+    def run(pipelined):
+        sess = ctypes.c_void_p()
+        assert L.ss_session_create(h, w, 3, 3, None, ctypes.byref(sess)) == 0
+        uv = [torch.empty(h, w, 2, device="cuda") for _ in range(2)]
+        vd = [torch.empty(h, w, dtype=torch.uint8, device="cuda") for _ in range(2)]
+        outs = []
+        it = ctypes.c_int(0)
+        try:
+            for pos in (1, 2):
+                assert L.ss_push_pair(sess, pos, I[pos - 1].data_ptr(), P[pos - 1].data_ptr(), _lib.SS_F32,
+                                      _lib.SS_DEVICE) == 0
+            for pos in range(3, 8):
+                t = pos - 1  # the step solved after pushing pos
+                if pipelined:
+                    assert L.ss_session_compute_dis_flow(sess, 0, *opts) == 0  # claims the pre-launch
+                assert L.ss_push_pair(sess, pos, I[pos - 1].data_ptr(), P[pos - 1].data_ptr(), _lib.SS_F32,
+                                      _lib.SS_DEVICE) == 0
+                if pipelined:
+                    assert L.ss_session_compute_dis_flow(sess, 1, *opts) == 0
+                else:
+                    for which, other in ((0, t - 1), (1, t + 1)):
+                        assert L.ss_dis_flow(I[t - 1].data_ptr(), I[other - 1].data_ptr(), h, w, 3, *opts,
+                                             uv[which].data_ptr(), vd[which].data_ptr(), None) == 0
+                    torch.cuda.synchronize()
+                    for which in (0, 1):
+                        assert L.ss_set_flow(sess, which, uv[which].data_ptr(), vd[which].data_ptr(),
+                                             _lib.SS_DEVICE) == 0
+                assert L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)) == 0
+                o = np.empty((h, w, 3), np.float32)
+                assert L.ss_output(sess, o.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+                outs.append(o)
+        finally:
+            L.ss_session_destroy(sess)
+        return outs
+
+    a, b = run(False), run(True)
+    assert len(a) == len(b) == 5
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
