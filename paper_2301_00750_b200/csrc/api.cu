@@ -1120,6 +1120,7 @@ int ss_session_compute_dis_flow(ss_session *s, int which, int levels, int patch,
             est.reset();
             return rc;
         }
+        est->use_graphs = true;
     }
     if (which == 0 || !s->flow_timed) SS_CUDA_TRY(cudaEventRecord(s->fev[0], s->stream));
     if (side) {

@@ -12,6 +12,8 @@
 // Compiled with -fmad=false: the float32 op sequence follows numpy.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "dis.h"
@@ -344,6 +346,8 @@ static int centers(int extent, int r, int stride)
 
 Estimator::~Estimator()
 {
+    for (auto &g : graphs)
+        if (g.second.first) cudaGraphExecDestroy(g.second.first);
     for (void *p : allocs) cudaFree(p);
 }
 
@@ -406,6 +410,43 @@ int Estimator::init(int h_, int w_, const Options &o)
 
 int Estimator::run(const float *fa, const float *fb, int c, float *uv_out, uint8_t *valid,
                    cudaStream_t st)
+{
+    static const bool use = getenv("SS_DIS_GRAPHS") == nullptr || strcmp(getenv("SS_DIS_GRAPHS"), "0");
+    if (!use || !use_graphs || !warmed) {  // the first call runs eagerly (one-time constant upload)
+        warmed = true;
+        return run_impl(fa, fb, c, uv_out, valid, st);
+    }
+    auto &g = graphs[std::make_tuple(fa, fb, c, uv_out, valid)];
+    if (!g.first) {
+        SS_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        set_capturing(true);
+        const int rc = run_impl(fa, fb, c, uv_out, valid, st);
+        set_capturing(false);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(st, &graph);
+        if (rc || e != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            graphs.erase(std::make_tuple(fa, fb, c, uv_out, valid));
+            return rc ? rc : cuda_status(e, "cudaStreamEndCapture");
+        }
+        size_t n = 0;
+        cudaGraphGetNodes(graph, nullptr, &n);
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t e2 = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e2 != cudaSuccess) {
+            graphs.erase(std::make_tuple(fa, fb, c, uv_out, valid));
+            return cuda_status(e2, "cudaGraphInstantiate");
+        }
+        g = {exec, (long)n};
+    }
+    SS_CUDA_TRY(cudaGraphLaunch(g.first, st));
+    count_launches(g.second);
+    return SS_OK;
+}
+
+int Estimator::run_impl(const float *fa, const float *fb, int c, float *uv_out, uint8_t *valid,
+                        cudaStream_t st)
 {
     static bool wset = false;
     if (!wset) {  // scipy _gaussian_kernel1d(sigma=1, order=0, radius=4), float64

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <tuple>
+#include <utility>
 #include <vector>
 
 namespace ss {
@@ -24,11 +27,19 @@ struct Estimator {
     float *gu = nullptr, *gv = nullptr, *gu2 = nullptr, *gv2 = nullptr;
     float *lum1 = nullptr, *lum2 = nullptr;
     std::vector<void *> allocs;
+    // one CUDA graph per (frames, outputs) pointer set: a flow is ~60 short
+    // kernels whose eager launches would otherwise pace the GPU
+    std::map<std::tuple<const float *, const float *, int, float *, uint8_t *>,
+             std::pair<cudaGraphExec_t, long>>
+        graphs;
+    bool warmed = false;
+    bool use_graphs = false;  // sessions only: their pointer sets are few and fixed
     ~Estimator();
     int init(int h, int w, const Options &o);
     // flow from frame a toward frame b ((h, w, c) float32 device) into
     // uv (h, w, 2) and valid (h, w) (may be null)
     int run(const float *fa, const float *fb, int c, float *uv, uint8_t *valid, cudaStream_t st);
+    int run_impl(const float *fa, const float *fb, int c, float *uv, uint8_t *valid, cudaStream_t st);
 };
 
 }  // namespace dis
