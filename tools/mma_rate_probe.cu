@@ -1,0 +1,83 @@
+// Probe: cycles per tcgen05.mma kind::tf32 (cta_group::1) issued back to back
+// by one elected thread, as a function of M, N and the A row width / swizzle
+// mode -- is a thin MMA bound by a fixed per-instruction cost or by reading A
+// from shared memory?  (Decides whether a 2-SM cta_group::2 tile can speed up
+// the thin 3xTF32 conv layers.)  Operand contents are irrelevant here.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/mma_rate_probe tools/mma_rate_probe.cu -lcuda
+#include <cuda_runtime.h>
+#include <cstdio>
+
+#include "../paper_2301_00750_b200/csrc/tc_common.cuh"
+
+using namespace ss::tc;
+
+// layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B, 6 = SWIZZLE_32B; K-major rows of rowb bytes
+__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t sbo, uint32_t layout)
+{
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+
+__global__ void probe(int M, int N, int rowb, int reps, long long *out)
+{
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint8_t *base = (uint8_t *)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+    uint8_t *as = base;              // 128 rows x rowb
+    uint8_t *bs = base + 128 * 128;  // 256 rows x rowb
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (128 * 128 + 256 * 128) / 4; i += blockDim.x) reinterpret_cast<float *>(base)[i] = 0.001f;
+    if (tid == 0) {
+        mbar_init(&mbar, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc_rt(&tslot, 256);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (tid == 0) {
+        const uint32_t lay = rowb == 128 ? 2 : (rowb == 64 ? 4 : 6);
+        const uint64_t ad = desc(smem_u32(as), 8 * rowb, lay), bd = desc(smem_u32(bs), 8 * rowb, lay);
+        const uint32_t id = idesc(2u, (uint32_t)M, (uint32_t)N);
+        long long t0 = clock64();
+        for (int r = 0; r < reps; ++r) mma_tf32(tmem, ad, bd, id, r > 0 ? 1u : 0u);
+        mma_commit(&mbar);
+        mbar_wait(&mbar, 0);
+        long long t1 = clock64();
+        out[0] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc_rt(tmem, 256);
+}
+
+int main()
+{
+    long long *d;
+    cudaMalloc(&d, sizeof(long long));
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    const int reps = 1000;
+    printf("cycles per tcgen05.mma.cta_group::1.kind::tf32 (K = 8), %d back to back\n", reps);
+    for (int rowb : {32, 64, 128})
+        for (int M : {64, 128})
+            for (int N : {16, 32, 48, 64, 128, 256}) {
+                probe<<<1, 128, 64 * 1024>>>(M, N, rowb, reps, d);
+                if (cudaDeviceSynchronize() != cudaSuccess) {
+                    printf("error M=%d N=%d rowb=%d\n", M, N, rowb);
+                    return 1;
+                }
+                long long c;
+                cudaMemcpy(&c, d, sizeof c, cudaMemcpyDeviceToHost);
+                printf("rowb=%3d M=%3d N=%3d : %6.1f clk/MMA  (%5.1f MAC/clk)\n", rowb, M, N, (double)c / reps,
+                       (double)M * N * 8 * reps / (double)c);
+            }
+    return 0;
+}
