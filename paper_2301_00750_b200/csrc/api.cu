@@ -1138,7 +1138,28 @@ int ss_session_compute_dis_flow(ss_session *s, int which, int levels, int patch,
         s->side_slots[0] = (int)(a - s->slot);
         s->side_slots[1] = (int)(b - s->slot);
     } else {
-        if (int rc = est->run(a->I, b->I, s->ci, s->uv[which], s->valid[which], s->stream)) return rc;
+        // the flow to t+1 is on the critical chain: run it on a highest-priority
+        // stream (forked from / joined to the session stream), ahead of the
+        // side flow's kernels (SS_FLOW_PRIO=0: on the session stream)
+        static const bool prio = getenv("SS_FLOW_PRIO") == nullptr || strcmp(getenv("SS_FLOW_PRIO"), "0");
+        cudaStream_t ws = s->stream;
+        if (prio && conc) {
+            if (!s->hi) {
+                int least = 0, greatest = 0;
+                SS_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+                SS_CUDA_TRY(cudaStreamCreateWithPriority(&s->hi, cudaStreamNonBlocking, greatest));
+                SS_CUDA_TRY(cudaEventCreateWithFlags(&s->hfork, cudaEventDisableTiming));
+                SS_CUDA_TRY(cudaEventCreateWithFlags(&s->hjoin, cudaEventDisableTiming));
+            }
+            SS_CUDA_TRY(cudaEventRecord(s->hfork, s->stream));
+            SS_CUDA_TRY(cudaStreamWaitEvent(s->hi, s->hfork, 0));
+            ws = s->hi;
+        }
+        if (int rc = est->run(a->I, b->I, s->ci, s->uv[which], s->valid[which], ws)) return rc;
+        if (ws != s->stream) {
+            SS_CUDA_TRY(cudaEventRecord(s->hjoin, s->hi));
+            SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->hjoin, 0));
+        }
         if (int rc = join_side(s)) return rc;  // fev[1] marks the end of both flows
         SS_CUDA_TRY(cudaEventRecord(s->fev[1], s->stream));
     }
