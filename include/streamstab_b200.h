@@ -217,6 +217,17 @@ SS_API void *ss_session_stream(const ss_session *s);
  * to the previous frame runs there) -- e.g. before recording an event that
  * must cover all of a step's work. */
 SS_API int ss_session_join(ss_session *s);
+/* Cross-stream ordering with a caller stream (NULL = legacy default stream).
+ * ss_session_wait_stream: session work issued after this call starts only
+ * once the caller's stream has finished what it had issued -- call it before
+ * ss_push_pair / ss_set_flow / ss_stage_pair from device buffers the caller's
+ * stream produced.  ss_session_signal_stream: the caller's stream waits for
+ * the session work issued so far (e.g. those copies) -- call it before
+ * freeing or reusing the source buffers on the caller's stream.  The
+ * reference has no streams; these replace the implicit ordering of numpy
+ * (consistency.py:321-340 keeps references to the caller's frames). */
+SS_API int ss_session_wait_stream(ss_session *s, void *stream);
+SS_API int ss_session_signal_stream(ss_session *s, void *stream);
 
 #ifdef __cplusplus
 }

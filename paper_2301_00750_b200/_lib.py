@@ -37,7 +37,7 @@ EXPORTS = (
     "ss_session_stream", "ss_session_join", "ss_flownet_num_params", "ss_flownet_create", "ss_flownet_destroy",
     "ss_flownet_flow", "ss_session_attach_flownet", "ss_session_compute_flow",
     "ss_warping_error_sums", "ss_ssim", "ss_session_time_conv", "ss_dis_flow",
-    "ss_session_compute_dis_flow",
+    "ss_session_compute_dis_flow", "ss_session_wait_stream", "ss_session_signal_stream",
 )
 SS_FLOW_FP32 = 0
 SS_FLOW_BF16 = 1
@@ -113,6 +113,8 @@ def _declare(L):
         "ss_session_time_conv": (i32, [vp, i32, i32, P(f32), P(ctypes.c_double)]),
         "ss_dis_flow": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, vp]),
         "ss_session_compute_dis_flow": (i32, [vp, i32, i32, i32, i32, i32]),
+        "ss_session_wait_stream": (i32, [vp, vp]),
+        "ss_session_signal_stream": (i32, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

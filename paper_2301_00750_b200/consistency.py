@@ -325,6 +325,15 @@ class SessionState:
         _dev.check(_lib.lib().ss_output(self._handle, out.ctypes.data, _lib.SS_F32, _lib.SS_HOST))
         return out[:, :, 0] if self._squeeze else out
 
+    def output_u8(self) -> np.ndarray:
+        """The current output quantized on the device as the reference's
+        writers do: rint(clip(O, 0, 1) * 255) -> uint8 (imgio.py:132,
+        service.py:101-102)."""
+        h, w, c = self._out_shape()
+        out = np.empty((h, w, c), np.uint8)
+        _dev.check(_lib.lib().ss_output(self._handle, out.ctypes.data, _lib.SS_U8, _lib.SS_HOST))
+        return out[:, :, 0] if self._squeeze else out
+
     def output_device(self):
         """The current output as a CUDA tensor (copy)."""
         t = _dev.torch()
@@ -363,18 +372,43 @@ class SessionState:
         if len(self.pairs) > 3:
             self.pairs.pop(0)
         if first:
-            self._first_output = processed_frame
+            # the first output *is* the pushed P_1 object (consistency.py:338-340);
+            # an 8-bit frame is stored as its float32 load (x / 255), read back
+            self._first_output = None if _is_u8(processed_frame) else processed_frame
 
     def _push_device(self, position, input_frame, processed_frame):
         L = _lib.lib()
+        if _is_u8(input_frame) and _is_u8(processed_frame):
+            # 8-bit frames (the live path's decoded PNG/PPM bytes): the device
+            # widens them exactly as imgio.load_frame does (uint8 / 255 in
+            # float32, imgio.py:72) -- 4x less host->device traffic
+            if _dev.is_torch(input_frame):
+                i, p = input_frame.contiguous(), processed_frame.contiguous()
+                where = _lib.SS_DEVICE if i.is_cuda else _lib.SS_HOST
+                if where == _lib.SS_DEVICE:
+                    _dev.check(L.ss_session_wait_stream(self._handle, _dev.stream_ptr()))
+                    self._inflight.append((i, p))
+                _dev.check(L.ss_push_pair(self._handle, position, i.data_ptr(), p.data_ptr(),
+                                          _lib.SS_U8, where))
+                if where == _lib.SS_HOST:  # pageable host copies complete before return
+                    _dev.check(L.ss_session_signal_stream(self._handle, _dev.stream_ptr()))
+            else:
+                i = np.ascontiguousarray(input_frame)
+                p = np.ascontiguousarray(processed_frame)
+                _dev.check(L.ss_push_pair(self._handle, position, i.ctypes.data, p.ctypes.data,
+                                          _lib.SS_U8, _lib.SS_HOST))
+            return
         if _dev.is_torch(input_frame) and input_frame.is_cuda:
             i = _dev.to_dev(input_frame)
             p = _dev.to_dev(processed_frame)
+            # the sources (and any converted temporaries) come from torch's
+            # current stream: the session stream waits for it before copying
+            _dev.check(L.ss_session_wait_stream(self._handle, _dev.stream_ptr()))
             _dev.check(L.ss_push_pair(self._handle, position, i.data_ptr(), p.data_ptr(),
                                       _lib.SS_F32, _lib.SS_DEVICE))
             # the copy is stream-ordered on the session stream: keep the
-            # sources (and any converted temporaries) referenced until the next
-            # step, which waits for that stream -- no host wait here
+            # sources referenced until the next step, which waits for that
+            # stream -- no host wait here
             self._inflight.append((i, p))
         else:
             i = np.ascontiguousarray(np.asarray(input_frame), dtype=np.float32)
@@ -388,6 +422,11 @@ class SessionState:
         t = ctypes.c_int64(0)
         _dev.check(_lib.lib().ss_check_step(self._handle, int(want_next), ctypes.byref(t)))
         return int(t.value)
+
+
+def _is_u8(x) -> bool:
+    dt = getattr(x, "dtype", None)
+    return dt is not None and str(dt) in ("uint8", "torch.uint8")
 
 
 def _provide_flow(state: SessionState, flow_backend, which: int, t: int, other: int):
@@ -404,9 +443,14 @@ def _provide_flow(state: SessionState, flow_backend, which: int, t: int, other: 
     if getattr(f, "on_device", False):
         uv = f.uv.to(_dev.torch().float32).contiguous()
         vd = f.valid.to(_dev.torch().uint8).contiguous()
+        # produced on torch's current stream: the session copies after it,
+        # and torch's stream (which may reuse the temporaries once they are
+        # dropped) continues only after the copies
+        sp = _dev.stream_ptr()
+        _dev.check(L.ss_session_wait_stream(state.handle, sp))
         _dev.check(L.ss_set_flow(state.handle, which, uv.data_ptr(), vd.data_ptr(),
                                  _lib.SS_DEVICE))
-        _dev.torch().cuda.current_stream().synchronize()
+        _dev.check(L.ss_session_signal_stream(state.handle, sp))
     else:
         uv = np.ascontiguousarray(f.uv, dtype=np.float32)
         vd = np.ascontiguousarray(f.valid, dtype=np.uint8)

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <utility>
 
@@ -68,13 +69,16 @@ __global__ void k_f32_to_u8(const float *__restrict__ src, long n, uint8_t *__re
     if (i < n) dst[i] = (uint8_t)rintf(__fmul_rn(fminf(fmaxf(src[i], 0.0f), 1.0f), 255.0f));
 }
 
+// ConstantFlow (flow.py:406-425): FlowField(uv) marks a pixel invalid when
+// max(|u|, |v|) > 1e9 or a component is NaN (imgio.py:172-174; NaN compares
+// false, and 1e9 is exact in float32)
 __global__ void k_fill_flow(float *__restrict__ uv, uint8_t *__restrict__ valid, long n, float u,
                             float v)
 {
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
         reinterpret_cast<float2 *>(uv)[i] = make_float2(u, v);
-        valid[i] = 1;
+        valid[i] = fabsf(u) <= 1e9f && fabsf(v) <= 1e9f;
     }
 }
 
@@ -148,6 +152,7 @@ struct ss_session {
     // the staging buffers have no reader left (their frame's last step
     // completed): an upload into them needs no ordering after the session
     bool stage_idle = true;
+    cudaEvent_t xev = nullptr;  // ss_session_wait_stream / ss_session_signal_stream
     std::unique_ptr<dis::Estimator> dis;   // built-in flow (BuiltinFlow)
     std::unique_ptr<dis::Estimator> dis0;  // its flow to t-1, on the side stream
 };
@@ -160,11 +165,40 @@ static int join_side(const ss_session *s)
     return SS_OK;
 }
 
+// Scratch reused by consecutive stateless calls: a call on another stream
+// than the previous user of the same scratch first waits for that user's work
+struct StreamOrder {
+    cudaEvent_t done = nullptr;
+    cudaStream_t last = nullptr;
+    bool used = false;
+    ~StreamOrder()
+    {
+        if (done) cudaEventDestroy(done);
+    }
+    int before(cudaStream_t st)
+    {
+        if (used && st != last) SS_CUDA_TRY(cudaStreamWaitEvent(st, done, 0));
+        return SS_OK;
+    }
+    int after(cudaStream_t st)
+    {
+        if (!done) SS_CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        SS_CUDA_TRY(cudaEventRecord(done, st));
+        last = st;
+        used = true;
+        return SS_OK;
+    }
+};
+
 struct ss_flownet {
     int device;
     int precision;
     fn::Weights wts;
-    std::map<std::pair<int, int>, std::unique_ptr<fn::Run>> runs;  // stateless calls
+    // stateless calls (ss_flownet_flow): one scratch set per frame size,
+    // shared by all callers -- host threads serialise on the mutex, streams
+    // on the StreamOrder event
+    std::mutex mu;
+    std::map<std::pair<int, int>, std::pair<std::unique_ptr<fn::Run>, StreamOrder>> runs;
 };
 
 static int session_alloc(ss_session *s)
@@ -237,6 +271,7 @@ static void session_free(ss_session *s)
     if (s->st_done) cudaEventDestroy(s->st_done);
     cudaFree(s->stI);
     cudaFree(s->stP);
+    if (s->xev) cudaEventDestroy(s->xev);
     s->run.reset();
     s->dis.reset();
     s->dis0.reset();
@@ -255,8 +290,10 @@ static int copy_frame(ss_session *s, float *dst, const void *src, int c, int dty
         set_error("unsupported dtype");
         return SS_VALUE_ERROR;
     }
-    // stage u8 in the tail of dst (4x smaller), then widen in place-safe order
-    // via a separate staging buffer: use O_new as scratch (not live here)
+    // stage the u8 bytes in O_new (scratch between steps; an asynchronous
+    // output copy may still be reading it -- it held the previous output)
+    // and widen them into dst (x / 255, imgio.py:72)
+    if (s->out_pending) SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->out_done, 0));
     uint8_t *stage = reinterpret_cast<uint8_t *>(s->O_new);
     if ((size_t)s->h * s->w * s->cp * sizeof(float) < n) {
         set_error("u8 staging buffer too small");
@@ -447,16 +484,23 @@ int ss_dis_flow(const float *frame_a, const float *frame_b, int h, int w, int c,
 {
     if (int rc = check_hw(h, w)) return rc;
     if (int rc = check_c(c)) return rc;
+    // per host thread; consecutive calls on different streams are ordered
     static thread_local std::unique_ptr<dis::Estimator> est;
+    static thread_local StreamOrder order;
     const dis::Options o = dis_options(levels, patch, iters, downscale);
+    cudaStream_t st = (cudaStream_t)stream;
     if (!est || est->h != h || est->w != w || !same_opts(est->opts, o)) {
+        if (est && order.used) SS_CUDA_TRY(cudaEventSynchronize(order.done));  // freed below
         est.reset(new dis::Estimator());
+        order.used = false;
         if (int rc = est->init(h, w, o)) {
             est.reset();
             return rc;
         }
     }
-    return est->run(frame_a, frame_b, c, uv, valid, (cudaStream_t)stream);
+    if (int rc = order.before(st)) return rc;
+    if (int rc = est->run(frame_a, frame_b, c, uv, valid, st)) return rc;
+    return order.after(st);
 }
 
 // ---- metrics -------------------------------------------------------------------
@@ -581,6 +625,34 @@ int ss_session_reset(ss_session *s)
 }
 
 void *ss_session_stream(const ss_session *s) { return (void *)s->stream; }
+
+// cross-stream ordering with the caller's stream (e.g. torch's current
+// stream, which may be the legacy default stream 0): device sources produced
+// there are complete before the session reads them, and temporaries the
+// caller frees afterwards are not reused before the session's copy ran
+static int xev(ss_session *s)
+{
+    if (!s->xev) SS_CUDA_TRY(cudaEventCreateWithFlags(&s->xev, cudaEventDisableTiming));
+    return SS_OK;
+}
+
+int ss_session_wait_stream(ss_session *s, void *stream)
+{
+    if ((cudaStream_t)stream == s->stream) return SS_OK;
+    if (int rc = xev(s)) return rc;
+    SS_CUDA_TRY(cudaEventRecord(s->xev, (cudaStream_t)stream));
+    SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->xev, 0));
+    return SS_OK;
+}
+
+int ss_session_signal_stream(ss_session *s, void *stream)
+{
+    if ((cudaStream_t)stream == s->stream) return SS_OK;
+    if (int rc = xev(s)) return rc;
+    SS_CUDA_TRY(cudaEventRecord(s->xev, s->stream));
+    SS_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, s->xev, 0));
+    return SS_OK;
+}
 
 int ss_session_join(ss_session *s)
 {
@@ -1022,7 +1094,9 @@ int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b,
 {
     if (int rc = check_hw(h, w)) return rc;
     if (int rc = check_c(c)) return rc;
-    auto &run = net->runs[{h, w}];
+    std::lock_guard<std::mutex> lock(net->mu);
+    auto &entry = net->runs[{h, w}];
+    auto &run = entry.first;
     if (!run) {
         run.reset(new fn::Run());
         if (int rc = run->init(&net->wts, h, w)) {
@@ -1031,10 +1105,12 @@ int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b,
         }
     }
     cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = entry.second.before(st)) return rc;
     run->conv_mode = conv_mode_for(net->precision);
     if (int rc = run->pyramid(0, -1, frame_a, c, st)) return rc;
     if (int rc = run->pyramid(1, -1, frame_b, c, st)) return rc;
-    return run->flow(0, 1, uv, valid, st);
+    if (int rc = run->flow(0, 1, uv, valid, st)) return rc;
+    return entry.second.after(st);
 }
 
 int ss_session_attach_flownet(ss_session *s, ss_flownet *net)

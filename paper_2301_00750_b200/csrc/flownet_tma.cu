@@ -742,7 +742,11 @@ static int launch_parts(const ConvParams &p, const CUtensorMap &tmA, int prec, i
     a.splits = splits;
     a.ws = splits > 1 ? p.ws : nullptr;
     a.units = tiles_all * splits;
-    const int grid = std::min(a.units, p.grid_cap > 0 ? std::min(p.grid_cap, n_sm_tma) : n_sm_tma);
+    // SS_CONV_GRID_MAX (tests): fewer persistent CTAs, so small layers also
+    // walk several units per CTA (TMEM accumulator alternation, ring wrap)
+    static const int grid_max = getenv("SS_CONV_GRID_MAX") ? std::max(1, atoi(getenv("SS_CONV_GRID_MAX"))) : 0;
+    int grid = std::min(a.units, p.grid_cap > 0 ? std::min(p.grid_cap, n_sm_tma) : n_sm_tma);
+    if (grid_max) grid = std::min(grid, grid_max);
     const size_t smem = (size_t)2 * a.na * a.a_slot + (size_t)a.stages * a.b_stage + bar_bytes + a.stages * 16;
     const CUtensorMap &tmB = *static_cast<const CUtensorMap *>(p.tmB);
     const int rc = launch_pdl("k_conv_tc3", conv_kernel(prec, amode, a.b_res != 0), dim3(grid), dim3(TM_THREADS),

@@ -517,6 +517,365 @@ __global__ void __launch_bounds__(blk::THREADS, 1)
     push_maxbits(bits_all, a.maxbits);
 }
 
+// ---------------------------------------------------------------------------
+// v2: the TMA-fed persistent pass with 4 x 4 blocks per thread (round 2).
+//
+// Same region (128 x 64, K = 8 iterations per pass, 8-pixel apron), tile walk
+// and TMA double staging as k_sgd_tma, but the neighbour exchange is rebuilt
+// around the shared-memory port, which bounded the 2 x 8 layout (every
+// element had an external W or E neighbour, read back with 2-way bank
+// conflicts: ~52 wavefronts per warp-iteration, as many cycles as the FP32
+// pipe needed for the math):
+//   * warp w owns region rows 4w..4w+3 over the full 128-column width, lane l
+//     columns 4l..4l+3; the 16 elements live in registers as vertical packed
+//     pairs (rows 0,2) and (rows 1,3) of each column, so every N / S / W / E
+//     operand of the packed update is an existing register pair except the
+//     block's own edge rows / columns;
+//   * W / E edge columns come from the neighbouring lanes by warp shuffle (no
+//     shared memory, no barrier);
+//   * N / S edge rows go through a double-buffered row exchange laid out
+//     [slot][col j][lane] -- conflict-free 1-wavefront accesses, 16 per
+//     warp-iteration -- with one barrier per iteration;
+//   * the replicate (Neumann) boundary: at an image top / bottom edge the
+//     edge warp also writes its own edge row into the slot its neighbour
+//     outside the image would write (that warp skips it), so the exchange
+//     itself serves the boundary; left / right edges select the lane's own
+//     column instead of the shuffled one.
+// Requires w % 4 == 0 and h % 4 == 0 (every image edge on a block boundary);
+// per element the reference op sequence is unchanged, so iterates stay
+// bit-identical (tests/test_gpu_parity.py).
+namespace v2 {
+constexpr int K = 8;
+constexpr int RW = 128, RH = 64;
+constexpr int OW = RW - 2 * K, OH = RH - 2 * K;
+constexpr int STAGE = RW * RH;
+constexpr int SLOT = 2 * 4 * 32;  // [top row | bottom row][col j][lane]
+// RB rows per thread block (4 or 8): RH / RB warps, one RB-row strip each.
+// Row-exchange slots per parity: 0 and NW + 1 are virtual warps outside the
+// region, NW + 2 is a sink for writes a replicate ghost replaces.
+template <int RB>
+struct Cfg {
+    static constexpr int NW = RH / RB;
+    static constexpr int NP = RB / 2;  // packed pairs per column: rows (r, r + NP)
+    static constexpr int THREADS = 32 * NW;
+    static constexpr int PAR = (NW + 3) * SLOT;
+    static constexpr size_t SMEM = (5ull * STAGE + 2ull * PAR) * sizeof(float) + 16;
+};
+}  // namespace v2
+
+// Packed pairs live in 64-bit registers (PTX .b64): ptxas then keeps each
+// pair in an aligned register pair instead of rebuilding it from two scalars
+// before every FADD2 / FFMA2 (which cost more MOVs than the math).
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float lo, float hi)
+{
+    u64 d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+    return d;
+}
+__device__ __forceinline__ float lo32(u64 x)
+{
+    float l, h;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(x));
+    return l;
+}
+__device__ __forceinline__ float hi32(u64 x)
+{
+    float l, h;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(x));
+    return h;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b)
+{
+    u64 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b)
+{
+    u64 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c)
+{
+    u64 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+// round(a * b) exactly: see fmul2 (the -0 addend is a run-time value)
+__device__ __forceinline__ u64 mul2(u64 a, u64 b, u64 z) { return fma2(a, b, z); }
+
+// A pair built once and kept in an aligned register pair: x + (-0) == x
+// exactly for every float (zeros keep their sign), and with the -0 a run-time
+// value ptxas can neither drop the add nor fold it into a consumer (it folded
+// a multiply by one into the next subtraction as an FMA and then re-packed the
+// scalars in every iteration).
+__device__ __forceinline__ u64 pk_reg(float lo, float hi, u64 negzero2)
+{
+    return add2(pk(lo, hi), negzero2);
+}
+
+// sgd_update2 on .b64 pairs (consistency.py:282-291, one rounding per op)
+__device__ __forceinline__ u64 sgd_u64(u64 o, u64 op, u64 N, u64 S, u64 W, u64 E, u64 lp, u64 a,
+                                       u64 wcv, u64 eta, u64 kappa, u64 m4, u64 z)
+{
+    u64 g = fma2(o, m4, N);
+    g = add2(g, S);
+    g = add2(g, W);
+    g = add2(g, E);
+    g = sub2(g, lp);
+    u64 d = sub2(o, a);
+    d = mul2(d, wcv, z);
+    g = sub2(d, g);
+    g = mul2(g, eta, z);
+    u64 m = sub2(o, op);
+    m = mul2(m, kappa, z);
+    return add2(sub2(o, g), m);
+}
+
+struct V2Consts {
+    u64 eta, kap, m4, z;
+};
+
+// one iteration of a thread's 4 x RB block: X = current iterate (pairs
+// [col j][r] = rows (r, r + NP)), Y = previous iterate, overwritten with the
+// new one, whose edge rows go to parity buffer `wr` at the per-tile
+// destinations top_dst / bot_dst (own slot, replicate ghost or sink)
+template <int RB>
+__device__ __forceinline__ void v2_iter(const u64 (&X)[4][RB / 2], u64 (&Y)[4][RB / 2],
+                                        const u64 (&Av)[4][RB / 2], const u64 (&Lv)[4][RB / 2],
+                                        const u64 (&Wv)[4][RB / 2], const float *rd, float *wr,
+                                        int n_off, int s_off, int t_off, int b_off, bool lft,
+                                        bool rgt, const V2Consts &k, bool track, float &mx)
+{
+    constexpr int NP = RB / 2;
+    // W / E edge columns from the neighbouring lanes (lane 0 / 31 get their
+    // own values: region columns -1 / 128 are apron garbage, never committed)
+    u64 wv[NP], ev[NP];
+#pragma unroll
+    for (int r = 0; r < NP; ++r) {
+        wv[r] = pk(__shfl_up_sync(0xffffffffu, lo32(X[3][r]), 1),
+                   __shfl_up_sync(0xffffffffu, hi32(X[3][r]), 1));
+        ev[r] = pk(__shfl_down_sync(0xffffffffu, lo32(X[0][r]), 1),
+                   __shfl_down_sync(0xffffffffu, hi32(X[0][r]), 1));
+        wv[r] = lft ? X[0][r] : wv[r];  // replicate boundary: the neighbour is the cell itself
+        ev[r] = rgt ? X[3][r] : ev[r];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        // N / S edge rows: bottom row of the strip above, top row of the strip below
+        const float nr = rd[n_off + j * 32];
+        const float sr = rd[s_off + j * 32];
+#pragma unroll
+        for (int r = 0; r < NP; ++r) {
+            const u64 Nn = r == 0 ? pk(nr, lo32(X[j][NP - 1])) : X[j][r - 1];
+            const u64 Sn = r == NP - 1 ? pk(hi32(X[j][0]), sr) : X[j][r + 1];
+            const u64 Wn = j == 0 ? wv[r] : X[j - 1][r];
+            const u64 En = j == 3 ? ev[r] : X[j + 1][r];
+            const u64 u = sgd_u64(X[j][r], Y[j][r], Nn, Sn, Wn, En, Lv[j][r], Av[j][r], Wv[j][r],
+                                  k.eta, k.kap, k.m4, k.z);
+            Y[j][r] = u;
+            if (track) mx = fmaxf(mx, fmaxf(fabsf(lo32(u)), fabsf(hi32(u))));
+        }
+    }
+    // publish the new edge rows (row 0, row RB - 1)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        wr[t_off + j * 32] = lo32(Y[j][0]);
+        wr[b_off + j * 32] = hi32(Y[j][NP - 1]);
+    }
+}
+
+template <int RB>
+__global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
+    k_sgd_v2(const __grid_constant__ TmaMaps maps, BlockedArgs a)
+{
+    using namespace v2;
+    constexpr int NW = Cfg<RB>::NW, NP = Cfg<RB>::NP, THREADS = Cfg<RB>::THREADS, PAR = Cfg<RB>::PAR;
+    extern __shared__ __align__(1024) float smem_v2[];
+    float *stage = smem_v2;              // 5 x (RH x RW)
+    float *rows = stage + 5 * STAGE;     // 2 parities x PAR
+    uint64_t *bar = reinterpret_cast<uint64_t *>(rows + 2 * PAR);
+    const int lane = threadIdx.x, wp = threadIdx.y;
+    const int tid = wp * 32 + lane;
+    const int ntx = (a.w + OW - 1) / OW, nty = (a.h + OH - 1) / OH;
+    const int ntiles = ntx * nty * a.c;
+    constexpr uint32_t TX_BYTES = 5u * STAGE * sizeof(float);
+
+    auto coords = [&](int t, int &ch, int &x, int &y) {
+        ch = t / (ntx * nty);
+        const int rem = t - ch * ntx * nty;
+        const int ty = rem / ntx, tx = rem - ty * ntx;
+        x = tx * OW - K;
+        y = ty * OH - K;
+    };
+    auto issue = [&](int t) {
+        int ch, x, y;
+        coords(t, ch, x, y);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(smem_u32(bar)), "r"(TX_BYTES) : "memory");
+        tma_load_3d(stage + 0 * STAGE, &maps.O, x, y, ch, bar);
+        tma_load_3d(stage + 1 * STAGE, &maps.Op, x, y, ch, bar);
+        tma_load_3d(stage + 2 * STAGE, &maps.A, x, y, ch, bar);
+        tma_load_3d(stage + 3 * STAGE, &maps.L, x, y, ch, bar);
+        tma_load_2d(stage + 4 * STAGE, &maps.W, x, y, bar);
+    };
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // row buffers start finite (the virtual slots are read, never written
+    // except as replicate ghosts)
+    for (int i = tid; i < 2 * PAR; i += THREADS) rows[i] = 0.0f;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // the first tile's constant inputs load while the previous pass drains
+    if (tid == 0 && (int)blockIdx.x < ntiles) {
+        int ch, x, y;
+        coords(blockIdx.x, ch, x, y);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(smem_u32(bar)), "r"(TX_BYTES) : "memory");
+        tma_load_3d(stage + 2 * STAGE, &maps.A, x, y, ch, bar);
+        tma_load_3d(stage + 3 * STAGE, &maps.L, x, y, ch, bar);
+        tma_load_2d(stage + 4 * STAGE, &maps.W, x, y, bar);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        tma_load_3d(stage + 0 * STAGE, &maps.O, x, y, ch, bar);
+        tma_load_3d(stage + 1 * STAGE, &maps.Op, x, y, ch, bar);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __syncthreads();
+
+    V2Consts kc;
+    kc.eta = pk(a.eta, a.eta);
+    kc.kap = pk(a.kappa, a.kappa);
+    kc.m4 = pk(-4.0f, -4.0f);
+    kc.z = pk(a.negzero, a.negzero);
+    const bool interior = lane >= K / 4 && lane < 32 - K / 4 && wp >= K / RB && wp < NW - K / RB;
+    uint32_t phase = 0;
+    unsigned bits_all = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int ch, rx0, ry0;
+        coords(t, ch, rx0, ry0);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        u64 X[4][NP], Y[4][NP], Av[4][NP], Lv[4][NP], Wv[4][NP];
+        {
+            // pairs (row r, row r + NP) of the thread's RB x 4 block, each
+            // materialised once per tile in an aligned register pair (see
+            // pk_reg); built from scalars at every use instead, ptxas re-packs
+            // them in every iteration
+            auto ld = [&](int arr, u64 (&D)[4][NP]) {
+#pragma unroll
+                for (int r = 0; r < NP; ++r) {
+                    const float *plo = stage + arr * STAGE + (RB * wp + r) * RW + 4 * lane;
+                    const float4 lo = *reinterpret_cast<const float4 *>(plo);
+                    const float4 hi = *reinterpret_cast<const float4 *>(plo + NP * RW);
+                    D[0][r] = pk_reg(lo.x, hi.x, kc.z);
+                    D[1][r] = pk_reg(lo.y, hi.y, kc.z);
+                    D[2][r] = pk_reg(lo.z, hi.z, kc.z);
+                    D[3][r] = pk_reg(lo.w, hi.w, kc.z);
+                }
+            };
+            ld(0, X);
+            ld(1, Y);
+            ld(2, Av);
+            ld(3, Lv);
+            ld(4, Wv);
+        }
+        const int gx0 = rx0 + 4 * lane, gy0 = ry0 + RB * wp;
+        const bool lft = gx0 == 0, rgt = gx0 + 4 == a.w;
+        const bool inside = gx0 >= 0 && gx0 < a.w && gy0 >= 0 && gy0 < a.h;
+        const bool track = interior && inside;
+        // row-exchange offsets (per lane): N row = bottom row of slot wp, S
+        // row = top row of slot wp + 2; own rows go to slot wp + 1 -- except
+        // at an image edge, where the edge strip writes its edge row into the
+        // outside neighbour's slot instead (replicate boundary: that is the
+        // value the inside strip must read), and the outside strip's own
+        // write there is sent to the sink slot
+        const int sink = (NW + 2) * SLOT + lane;
+        const int n_off = wp * SLOT + 128 + lane, s_off = (wp + 2) * SLOT + lane;
+        const int t_off = gy0 == 0 ? wp * SLOT + 128 + lane : gy0 == a.h ? sink : (wp + 1) * SLOT + lane;
+        const int b_off = gy0 + RB == a.h ? (wp + 2) * SLOT + lane
+                          : gy0 + RB == 0  ? sink : (wp + 1) * SLOT + 128 + lane;
+        float *rb0 = rows, *rb1 = rows + PAR;
+        // publish the initial edge rows (parity 0)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            rb0[t_off + j * 32] = lo32(X[j][0]);
+            rb0[b_off + j * 32] = hi32(X[j][NP - 1]);
+        }
+        __syncthreads();  // stage consumed, rows published
+        if (tid == 0 && t + (int)gridDim.x < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(t + gridDim.x);
+        }
+        float mx = 0.0f;
+        for (int it = 0; it < a.iters; it += 2) {
+            v2_iter<RB>(X, Y, Av, Lv, Wv, rb0, rb1, n_off, s_off, t_off, b_off, lft, rgt, kc,
+                        track, mx);
+            __syncthreads();
+            if (it + 1 < a.iters) {
+                v2_iter<RB>(Y, X, Av, Lv, Wv, rb1, rb0, n_off, s_off, t_off, b_off, lft, rgt, kc,
+                            track, mx);
+                __syncthreads();
+            }
+        }
+        // write the interior back (the current iterate is in Y after an odd count)
+        const bool odd = a.iters & 1;
+        bool nan_seen = false;
+        if (interior && inside) {
+            const long plane = (long)ch * a.h * a.w;
+#pragma unroll
+            for (int rr = 0; rr < RB; ++rr) {
+                const int q = rr % NP;
+                float o[4], op[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const u64 cur = odd ? Y[j][q] : X[j][q];
+                    const u64 prv = odd ? X[j][q] : Y[j][q];
+                    o[j] = rr < NP ? lo32(cur) : hi32(cur);
+                    op[j] = rr < NP ? lo32(prv) : hi32(prv);
+                    nan_seen |= o[j] != o[j];
+                }
+                const long qi = (long)(gy0 + rr) * a.w + gx0;
+                if (a.hwc_out) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        a.hwc_out[(qi + j) * a.c + ch] = fminf(fmaxf(o[j], 0.0f), 1.0f);
+                } else {
+                    *reinterpret_cast<float4 *>(a.Oout + plane + qi) = make_float4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<float4 *>(a.Oprev_out + plane + qi) =
+                        make_float4(op[0], op[1], op[2], op[3]);
+                }
+            }
+        }
+        bits_all = max(bits_all, nan_seen ? 0x7fffffffu : __float_as_uint(mx));
+    }
+    push_maxbits(bits_all, a.maxbits);
+}
+
+template <int RB>
+static int launch_v2(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
+{
+    using C = v2::Cfg<RB>;
+    static bool attr = false;
+    if (!attr) {
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_v2<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM));
+        attr = true;
+    }
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        SS_CUDA_TRY(cudaGetDevice(&dev));
+        SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int ntiles = ((a.w + v2::OW - 1) / v2::OW) * ((a.h + v2::OH - 1) / v2::OH) * a.c;
+    const int grid = std::min(ntiles, n_sm);
+    return fn::launch_pdl("k_sgd_v2", k_sgd_v2<RB>, dim3(grid), dim3(32, C::NW), C::SMEM, st, maps, a);
+}
+
 template <int K>
 static int launch_tma(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
 {
@@ -783,12 +1142,15 @@ int SolverWork::ensure(int h_, int w_, int c_, int iterations)
 
 int solver_variant()
 {
-    // 0 = streaming (one iteration per launch), 1 = blocked LDG, 2 = blocked TMA
+    // 0 = streaming (one iteration per launch), 1 = blocked LDG, 2 = blocked
+    // TMA (2 x 8 blocks), 3 = v2 (4 x 4 blocks; w % 4 == h % 4 == 0, else 2)
     static int v = [] {
         const char *e = getenv("SS_SOLVER");
         if (e && !strcmp(e, "stream")) return 0;
         if (e && !strcmp(e, "ldg")) return 1;
-        return 2;
+        if (e && !strcmp(e, "tma")) return 2;
+        if (e && !strcmp(e, "v2r4")) return 4;
+        return 3;
     }();
     return v;
 }
@@ -866,14 +1228,16 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
     const long hw = (long)wk.h * wk.w;
     const long n = hw * wk.c;
     int variant = solver_variant();
-    if (variant == 2 && (wk.w % 4 != 0 || !encode_fn())) variant = 1;
-    const int K = variant == 2 ? tma_k() : K_LDG;
+    if (variant == 3 && wk.h % 8 != 0) variant = 4;  // RB = 8 needs h % 8 == 0
+    if (variant >= 3 && (wk.w % 4 != 0 || wk.h % 4 != 0)) variant = 2;
+    if (variant >= 2 && (wk.w % 4 != 0 || !encode_fn())) variant = 1;
+    const int K = variant >= 3 ? v2::K : variant == 2 ? tma_k() : K_LDG;
     const int n_pass = variant ? (iters + K - 1) / K : 0;
 
     if (variant) {
         SS_CUDA_TRY(cudaMemsetAsync(wk.maxbits, 0, (size_t)n_pass * sizeof(unsigned), st));
         TmaMaps m_init, m_set[2];
-        if (variant == 2) {
+        if (variant >= 2) {
             TmaMaps base;
             if ((rc = make_map(&base.A, A, wk.w, wk.h, wk.c, true))) return rc;
             if ((rc = make_map(&base.L, lapP, wk.w, wk.h, wk.c, true))) return rc;
@@ -918,7 +1282,11 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
             a.maxbits = wk.maxbits + ps;
             a.aligned = (variant == 2 ? K : K_LDG) == 8 && wk.h % 8 == 0 && wk.w % 2 == 0 &&
                         getenv("SS_SOLVER_ALIGNED") == nullptr;
-            if (variant == 2) {
+            if (variant >= 3) {
+                const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];
+                rc = variant == 3 ? launch_v2<8>(mp, a, st) : launch_v2<4>(mp, a, st);
+                if (rc) return rc;
+            } else if (variant == 2) {
                 const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];
                 if (K == 4) rc = launch_tma<4>(mp, a, st);
                 else rc = launch_tma<8>(mp, a, st);

@@ -282,8 +282,106 @@ def make_dis(flow, synthetic):
     _save("dis.npz", **out)
 
 
+def _sha(a) -> np.ndarray:
+    import hashlib
+
+    return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8)
+
+
+def make_dis_large(flow, synthetic):
+    """Reference DIS flow at 960x540 (parity at >= 540p).  The
+    frames are regenerated on the test side by the package's synthetic module
+    (same recipe, same seed); their hashes pin that they are the same frames.
+    The flow is pinned bit for bit by its sha256, plus a strided sample for
+    diagnostics."""
+    out = {}
+    seq = synthetic.translating_sequence(frames=2, height=540, width=960, step=(2, 1), seed=31)
+    for tag, opts in (("d1", flow.FlowOptions()), ("d2", flow.FlowOptions(downscale=2))):
+        f = flow.estimate_flow(seq.inputs[1], seq.inputs[0], opts)
+        out[f"{tag}_uv_sha"] = _sha(f.uv)
+        out[f"{tag}_valid_sha"] = _sha(f.valid)
+        out[f"{tag}_uv_sample"] = np.ascontiguousarray(f.uv[::7, ::7])
+        out[f"{tag}_opts"] = np.array([opts.levels, opts.patch_size, opts.iterations_per_level,
+                                       opts.downscale])
+    out["a_sha"] = _sha(np.asarray(seq.inputs[1], np.float32))
+    out["b_sha"] = _sha(np.asarray(seq.inputs[0], np.float32))
+    out["shape"] = np.array([540, 960, 3])
+    out["seed"] = np.array(31)
+    _save("dis_large.npz", **out)
+
+
+def make_imgio(consistency, flow, imgio, synthetic):
+    """8-bit I/O of the live path: load = uint8 / 255 in float32
+    (imgio.py:72 via a real PNG round trip), quantize = rint(clip(x)*255)
+    (imgio.py:132, service.py:101-102), and a Session.solve_next-shaped u8
+    stream (service.py:154-226): u8 frames loaded, stabilized with an integer
+    ConstantFlow, outputs quantized."""
+    import io
+    import tempfile
+
+    from PIL import Image
+
+    from streamstab import service
+
+    out = {}
+    rng = np.random.default_rng(707)
+    u8 = rng.integers(0, 256, (16, 24, 3), dtype=np.uint8)
+    u8.reshape(-1)[:256] = np.arange(256, dtype=np.uint8)  # every code value
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "f.png")
+        Image.fromarray(u8, mode="RGB").save(path)
+        out["load_u8"] = u8
+        out["load_f32"] = imgio.load_frame(path)
+    # quantization: ties (k + 0.5) / 255, values just around them, outside [0, 1]
+    k = np.arange(256, dtype=np.float64)
+    vals = np.concatenate([(k + 0.5) / 255.0, k / 255.0,
+                           np.nextafter(((k + 0.5) / 255.0).astype(np.float32), np.float32(0)),
+                           np.nextafter(((k + 0.5) / 255.0).astype(np.float32), np.float32(1)),
+                           [-1.0, -1e-7, 1.0 + 1e-7, 2.0, 0.5]]).astype(np.float32)
+    vals = np.concatenate([vals, rng.random(4 * 256 * 3 - vals.size).astype(np.float32)])
+    q = vals[: 16 * 64 * 3].reshape(16, 64, 3)
+    png = service.encode_png(q)
+    out["quant_f32"] = q
+    out["quant_u8"] = np.asarray(Image.open(io.BytesIO(png)).convert("RGB"), np.uint8)
+    # u8 stream through the solve_next loop shape
+    seq = synthetic.translating_sequence(frames=5, height=40, width=64, step=(2, 1), seed=41)
+    ins = [np.rint(np.asarray(f) * 255).astype(np.uint8) for f in seq.inputs]
+    prs = [np.rint(np.asarray(f) * 255).astype(np.uint8) for f in seq.processed]
+    load = lambda a: imgio.as_frame(a.astype(np.float32) / 255.0)  # noqa: E731 (imgio.py:72)
+    state = consistency.SessionState(params=consistency.preset("default"))
+    prov = flow.ConstantFlow(2, 1)
+    n = len(ins)
+    state.push_pair(1, load(ins[0]), load(prs[0]))
+    state.push_pair(2, load(ins[1]), load(prs[1]))
+    loaded = 2
+    outs = {1: np.rint(np.clip(state.prev_output, 0, 1) * 255.0).astype(np.uint8)}
+    while state.solved_through < n:
+        target = state.solved_through + 1
+        if target < n:
+            if loaded < target + 1:
+                loaded += 1
+                state.push_pair(loaded, load(ins[loaded - 1]), load(prs[loaded - 1]))
+            o = consistency.stabilize_step(state, prov)
+        else:
+            o = consistency.stream_end_step(state, prov)
+        outs[target] = np.rint(np.clip(o, 0.0, 1.0) * 255.0).astype(np.uint8)
+    for i in range(n):
+        out[f"stream_I{i + 1}"] = ins[i]
+        out[f"stream_P{i + 1}"] = prs[i]
+        out[f"stream_O{i + 1}"] = outs[i + 1]
+    out["stream_n"] = np.array(n)
+    _save("imgio.npz", **out)
+
+
 def main():
     consistency, flow, imgio, synthetic = _import_ref()
+    if len(sys.argv) > 1:  # regenerate only the named fixtures
+        for name in sys.argv[1:]:
+            {"dis_large": lambda: make_dis_large(flow, synthetic),
+             "imgio": lambda: make_imgio(consistency, flow, imgio, synthetic)}[name]()
+        return
+    make_dis_large(flow, synthetic)
+    make_imgio(consistency, flow, imgio, synthetic)
     make_dis(flow, synthetic)
     make_warp(flow, imgio)
     make_occlusion(flow, imgio)

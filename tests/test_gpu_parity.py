@@ -279,6 +279,25 @@ def test_solver_matches_oracle_bitwise_odd_shapes(ss, shape):
         assert np.array_equal(got, want), (shape, iters)
 
 
+# v2 serves shapes with w % 4 == 0 and h % 8 == 0 (4x8 blocks) or h % 4 == 0
+# (4x4 blocks; the others fall back to the 2x8 TMA kernel): image edges land on
+# every lane / warp position of a 128x64 region (the region origin moves by
+# 112 / 48 per tile), one-tile images, images narrower than a region
+@pytest.mark.parametrize("shape", [(4, 4, 3), (8, 12, 1), (44, 116, 3), (52, 124, 3), (56, 128, 1),
+                                   (60, 132, 3), (96, 228, 3), (100, 236, 1), (148, 340, 3),
+                                   (208, 452, 1), (4, 452, 3), (452, 4, 3)])
+def test_solver_v2_aligned_shapes_bitwise(ss, shape):
+    rng = np.random.default_rng(7 * sum(shape))
+    p = rng.random(shape).astype(np.float32)
+    a = rng.random(shape).astype(np.float32)
+    wc = rng.uniform(0, 2, shape[:2]).astype(np.float32)
+    for iters in (1, 2, 7, 8, 9, 16, 150):
+        prm = ss.ConsistencyParams(iterations=iters)
+        got = ss.solve_screened_poisson(p, a, wc, prm, p)
+        want = orc.solve_screened_poisson(p, a, wc, orc.Params(iterations=iters), p)
+        assert np.array_equal(got, want), (shape, iters)
+
+
 def test_step_720p_matches_oracle(ss):
     from paper_2301_00750_b200 import synthetic
 
@@ -313,7 +332,7 @@ VARIANT_SCRIPT = r"""
 import sys, numpy as np
 sys.path[:0] = [sys.argv[1], sys.argv[1] + '/oracle']
 import oracle as orc, paper_2301_00750_b200 as ss
-for shape in [(61, 200, 3), (130, 124, 1), (47, 301, 3)]:
+for shape in [(61, 200, 3), (130, 124, 1), (47, 301, 3), (64, 200, 3), (132, 124, 1), (100, 340, 3)]:
     r = np.random.default_rng(sum(shape))
     p = r.random(shape).astype(np.float32); a = r.random(shape).astype(np.float32)
     wc = r.uniform(0, 2, shape[:2]).astype(np.float32)
@@ -326,10 +345,12 @@ print("ok")
 
 
 @pytest.mark.parametrize("env", [{"SS_SOLVER": "stream"}, {"SS_SOLVER": "ldg"},
-                                 {"SS_SOLVER_K": "4"}, {"SS_SOLVER_K": "8"}])
+                                 {"SS_SOLVER": "tma", "SS_SOLVER_K": "4"},
+                                 {"SS_SOLVER": "tma", "SS_SOLVER_K": "8"}, {"SS_SOLVER": "v2"},
+                                 {"SS_SOLVER": "v2r4"}])
 def test_solver_variants_bitwise(ss, env):
-    """Every solver schedule (streaming, blocked LDG, blocked TMA at K = 4/6/8)
-    produces the reference's bits."""
+    """Every solver schedule (streaming, blocked LDG, blocked TMA at K = 4/8,
+    v2 with 4x8 (default) and 4x4 blocks) produces the reference's bits."""
     import os
     import subprocess
     import sys

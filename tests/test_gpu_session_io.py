@@ -274,3 +274,177 @@ def test_pipelined_dis_session_matches_stateless_flows(lib):
     assert len(a) == len(b) == 5
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def _slow_chain(torch, n=40):
+    """A long default-stream kernel chain (several ms on a B200)."""
+    x = torch.randn(4096, 4096, device="cuda")
+    for _ in range(n):
+        x = x @ x
+        x = x / (x.abs().max() + 1)
+    return x
+
+
+def test_device_push_waits_for_producing_stream(lib):
+    """frames written by a long default-stream chain are
+    pushed only once complete (the session stream is a private non-blocking
+    stream when torch's current stream is the legacy default)."""
+    import torch
+
+    import paper_2301_00750_b200 as ss
+    from paper_2301_00750_b200 import synthetic
+
+    seq = synthetic.translating_sequence(frames=4, height=64, width=96, seed=21)
+    want = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"),
+                                    ss.ConstantFlow(2, 1)))
+    assert torch.cuda.current_stream().cuda_stream == 0
+
+    def frames():
+        for i, p in zip(seq.inputs, seq.processed):
+            di = torch.empty((64, 96, 3), device="cuda")
+            dp = torch.empty((64, 96, 3), device="cuda")
+            di.fill_(float("nan"))
+            dp.fill_(float("nan"))
+            _slow_chain(torch)
+            # the real content lands at the end of the chain
+            di.copy_(torch.from_numpy(i).cuda(non_blocking=True))
+            dp.copy_(torch.from_numpy(p).cuda(non_blocking=True))
+            yield di, dp
+
+    got = dict(ss.stabilize_stream(frames(), ss.preset("default"), ss.ConstantFlow(2, 1)))
+    assert sorted(got) == sorted(want)
+    for t in want:
+        g = got[t].cpu().numpy() if hasattr(got[t], "cpu") else got[t]
+        assert np.array_equal(g, want[t]), t
+
+
+def test_device_flow_waits_for_producing_stream(lib):
+    """an on-device FlowField produced late on torch's stream
+    is copied into the session slot only when complete."""
+    import torch
+
+    import paper_2301_00750_b200 as ss
+    from paper_2301_00750_b200 import synthetic
+    from paper_2301_00750_b200.imgio import FlowField
+
+    seq = synthetic.translating_sequence(frames=4, height=48, width=80, seed=22)
+    ref = ss.ConstantFlow(2.37, 1.13)
+
+    class LateDeviceFlow:
+        def flow_between(self, a, fa, b, fb):
+            f = ref.flow_between(a, fa, b, fb)
+            uv = torch.full((48, 80, 2), float("nan"), device="cuda")
+            _slow_chain(torch, 20)
+            uv.copy_(torch.from_numpy(np.ascontiguousarray(f.uv)).cuda(non_blocking=True))
+            return FlowField(uv)
+
+    want = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"), ref))
+    got = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"),
+                                   LateDeviceFlow()))
+    for t in want:
+        assert np.array_equal(got[t], want[t]), t
+
+
+@pytest.mark.parametrize("u,v", [(float("nan"), 1.0), (2e9, 0.0), (0.0, -1.5e9), (1e9, -1e9)])
+def test_constant_flow_validity_like_flowfield(lib, u, v):
+    """ConstantFlow's FlowField marks NaN / |uv| > 1e9 invalid
+    (imgio.py:172-174); the device fill does the same."""
+    _lib, L = lib
+    h, w = 8, 12
+    sess = ctypes.c_void_p()
+    assert L.ss_session_create(h, w, 3, 3, None, ctypes.byref(sess)) == 0
+    try:
+        f = np.zeros((h, w, 3), np.float32)
+        assert L.ss_push_pair(sess, 1, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+        assert L.ss_push_pair(sess, 2, f.ctypes.data, f.ctypes.data, _lib.SS_F32, _lib.SS_HOST) == 0
+        assert L.ss_set_constant_flow(sess, 0, u, v, 1) == 0
+        valid = np.full((h, w), 7, np.uint8)
+        assert L.ss_flows(sess, 0, None, valid.ctypes.data, _lib.SS_HOST) == 0
+        uv = np.empty((h, w, 2), np.float32)
+        uv[:, :, 0], uv[:, :, 1] = u, v
+        want = np.abs(uv).max(axis=2) <= 1e9
+        assert np.array_equal(valid.astype(bool), want)
+    finally:
+        L.ss_session_destroy(sess)
+
+
+def test_stateless_flows_on_two_streams(lib):
+    """stateless CNN / DIS flows issued alternately on two
+    streams (shared scratch) equal the single-stream results."""
+    import torch
+
+    import paper_2301_00750_b200 as ss
+    from paper_2301_00750_b200 import synthetic
+    from paper_2301_00750_b200.flow import estimate_flow
+
+    seq = synthetic.translating_sequence(frames=4, height=64, width=96, seed=23)
+    net = ss.LiteFlowNet(seed=0)
+    pairs = [(seq.inputs[k + 1], seq.inputs[k]) for k in range(3)]
+    want_cnn = [net.flow_between(2, a, 1, b).uv for a, b in pairs]
+    want_dis = [estimate_flow(a, b).uv for a, b in pairs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    got_cnn, got_dis = [], []
+    for k, (a, b) in enumerate(pairs):
+        with torch.cuda.stream(streams[k % 2]):
+            got_cnn.append(net.flow_between(2, a, 1, b).uv)
+            got_dis.append(estimate_flow(a, b).uv)
+    for k in range(3):
+        assert np.array_equal(np.asarray(got_cnn[k]), np.asarray(want_cnn[k])), k
+        assert np.array_equal(np.asarray(got_dis[k]), np.asarray(want_dis[k])), k
+
+
+def test_u8_ingest_matches_reference_load(lib, golden):
+    """uint8 frames pushed to the session are widened exactly as
+    imgio.load_frame does (uint8 / 255 in float32; reference fixture made by a
+    real PNG round trip through the reference loader)."""
+    import paper_2301_00750_b200 as ss
+
+    g = golden("imgio.npz")
+    state = ss.SessionState(params=ss.preset("default"))
+    state.push_pair(1, g["load_u8"], g["load_u8"])
+    got = state.prev_output
+    assert got.dtype == np.float32
+    assert np.array_equal(got, g["load_f32"])
+
+
+def test_u8_quantization_matches_reference_encode(lib, golden):
+    """Device quantization = service.encode_png / imgio.save_frame:
+    rint(clip(x, 0, 1) * 255), ties to even, out-of-range values clipped."""
+    import paper_2301_00750_b200 as ss
+
+    g = golden("imgio.npz")
+    q = g["quant_f32"]
+    state = ss.SessionState(params=ss.preset("default"))
+    state.push_pair(1, q, q)
+    assert np.array_equal(state.output_u8(), g["quant_u8"])
+
+
+def test_solve_next_loop_u8_in_u8_out(lib, golden):
+    """A Session.solve_next-shaped loop (service.py:154-226) on the GPU:
+    8-bit frames in (SS_U8 push), stabilize_step / stream_end_step, 8-bit
+    frames out (device quantization) -- bitwise the reference's loop
+    (integer ConstantFlow; reference fixture)."""
+    import paper_2301_00750_b200 as ss
+
+    g = golden("imgio.npz")
+    n = int(g["stream_n"])
+    ins = [g[f"stream_I{i}"] for i in range(1, n + 1)]
+    prs = [g[f"stream_P{i}"] for i in range(1, n + 1)]
+    state = ss.SessionState(params=ss.preset("default"))
+    prov = ss.ConstantFlow(2, 1)
+    state.push_pair(1, ins[0], prs[0])
+    state.push_pair(2, ins[1], prs[1])
+    loaded = 2
+    got = {1: state.output_u8()}
+    while state.solved_through < n:
+        target = state.solved_through + 1
+        if target < n:
+            if loaded < target + 1:
+                loaded += 1
+                state.push_pair(loaded, ins[loaded - 1], prs[loaded - 1])
+            ss.stabilize_step(state, prov)
+        else:
+            ss.stream_end_step(state, prov)
+        got[target] = state.output_u8()
+    for t in range(1, n + 1):
+        assert np.array_equal(got[t], g[f"stream_O{t}"]), t
