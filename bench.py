@@ -3,27 +3,38 @@
 (flow + warp + blend + solve), BASELINE.json's metric.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--flow fp32|bf16|constant] [--height H --width W]
+                    [--flow fp32|bf16|dis|constant] [--no-configs] [--no-e2e]
 
 One process per GPU (torchrun for N > 1).  Streams are independent (SURVEY
-§8(e)): every rank runs its own 1080p stream; torch.distributed is used only
-for the timing barrier and the max over ranks, never on the data path ->
-"scaling": "weak".
+§8(e)): they are sharded over ranks (paper_2301_00750_b200/sharding.py) and
+torch.distributed carries only the timing barrier and the max over ranks,
+never data -> "scaling": "weak" for the headline (one 1080p stream per GPU).
 
-A step = one stabilize_step of a 1920x1080 RGB stream with the lite flow CNN
-(BASELINE config 2: fp32 flow, interactive local/global blend): push the next
-(input, processed) pair; the network computes the new frame's feature pyramid
-and the two flows t->t-1, t->t+1 into the session's flow slots; the fused
-warp/weights/blend pass (K1); the 150-iteration screened-Poisson solve (K2);
-commit.  The consistency params alternate per frame (k1/k2 0.3/0.5 <-> 0.5/0.3,
-lambda 2.0 <-> 0.5).
+Headline (BASELINE configs[1]): one 1920x1080 RGB stream per GPU, lite flow
+CNN (fp32-class path), default preset with a per-frame interactive schedule
+(k1/k2 0.3/0.5 <-> 0.5/0.3, lambda 2.0 <-> 0.5), 150 solver iterations.  A
+step = push the next (input, processed) pair; new frame's pyramid and the two
+flows t->t-1, t->t+1; fused warp / weights / blends (K1); the 150-iteration
+screened-Poisson solve (K2); commit.
 
-`value` is device-timed (one CUDA event pair on the session stream around the
-K steps; no L2 flush -- each step touches several times the L2) with the
-frames already in HBM; `e2e` is the same step
-through the C ABI from pinned host buffers (H2D of the pair and D2H of O_t in
-the timed region).  `--impl reference` times the CPU restatement of the
-reference step (oracle/, all host threads) on a bounded sample.
+* ``value``: device time, one CUDA event pair on the session stream around
+  the K steps (the session's internal streams joined at the end), frames in
+  HBM.  No L2 flush: every step touches > 0.5 GB (>> 126 MB L2).
+* ``e2e``: the same step through the C ABI from pinned host f32 buffers,
+  H2D of the pair and D2H of O_t in the timed region; ``e2e_python_api``: the
+  drop-in numpy API (SessionState.push_pair + stabilize_step, numpy in and
+  out), i.e. what the reference's callers (service.py:206-226) would run.
+* ``roofline``: the dominant kernel by live share, K2 (k_sgd_v2), against the
+  FP32 issue rate; K1 against measured HBM and the flow network (whole stage
+  and its heaviest conv, est3_1) as secondaries.
+* ``configs``: every other BASELINE config, each device-timed with e2e and a
+  roofline: [0] 640x360, [2] 1080p bf16 flow, [3] 3840x2160, [4] 64 streams
+  sharded over the ranks (aggregate and per-stream), plus the reference's own
+  DIS flow on the GPU (like for like with the reference arm).
+* ``--impl reference``: the reference itself (baseline/_ref, installed from
+  /root/reference; stabilize_step with BuiltinFlow, its default provider) on
+  the host cores, one stream per process; falls back to the oracle port when
+  baseline/_ref is absent.
 """
 
 from __future__ import annotations
@@ -43,24 +54,27 @@ sys.path.insert(0, ROOT)
 
 H, W = 1080, 1920
 METRIC = "1080p frames/s (flow+warp+blend), per stream and box aggregate at 1/2/4/8 GPU"
-SOLVER_K = 8  # iterations per temporally-blocked solver pass (csrc/solver.cu)
+SOLVER_ITERS = 150
+SOLVER_OPS_PER_ELEM = 14  # FP32 ops / pixel / channel / iteration
+K1_BYTES_PER_PX = 130     # K1 algorithmic bytes / pixel
+FLOW_GFLOP_1080 = 131.0   # lite CNN, one pyramid + two flows at 1080p
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--flow", default="fp32", choices=["fp32", "bf16", "dis", "constant"])
     ap.add_argument("--height", type=int, default=H)
     ap.add_argument("--width", type=int, default=W)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=1,
-                    help="concurrent independent video streams per GPU (BASELINE configs[4]); "
-                         "each has its own session on its own CUDA stream, driven by its own "
-                         "host thread")
+    ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--streams-total", type=int, default=64,
+                    help="configs[4]: concurrent streams over all ranks")
     return ap.parse_args()
 
 
@@ -75,6 +89,21 @@ def params_for(t):
     if t % 2 == 0:
         return ConsistencyParams(k1=0.3, k2=0.5, lam=2.0)
     return ConsistencyParams(k1=0.5, k2=0.3, lam=0.5)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "of measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "of fallback"
+
+
+# FP32 non-FMA op rate: MEASURED_PEAKS.json has none; tools/fp32_rate_probe.cu
+# measured 126.5 FP32 results / clk / SM (FADD2 stream, 16 warps / SM) on this
+# pool's B200 -> x 148 SMs x 1965 MHz (profiles/r02_fp32_rate_probe.txt)
+FP32_PEAK_TOPS = 126.5 * 148 * 1.965e9 / 1e12
 
 
 class ClockSampler:
@@ -98,6 +127,7 @@ class ClockSampler:
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
+        return self
 
     def _read(self):
         for line in self.proc.stdout:
@@ -131,18 +161,139 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---------------------------------------------------------------------------
-# CPU restatement (oracle/): the reference arm and the cpu_baseline leg
-def _cpu_step_seconds(h, w, flow_kind, budget_s):
-    """Seconds per full step of the CPU restatement on all host threads:
-    consistency step (C, OpenMP) timed in full; the flow CNN (numpy restatement)
-    timed on a 1/16-area crop and scaled by pixel count (one new pyramid + two
-    estimator passes per step, like the GPU step)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
+def _check(rc, L):
+    if rc != 0:
+        raise RuntimeError(f"streamstab_b200 error {rc}: {L.ss_last_error().decode()}")
 
+
+def _med(xs):
+    xs = sorted(xs)
+    return xs[len(xs) // 2] if xs else 0.0
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference package itself (baseline/_ref) on host cores
+_REF_WORKER = r"""
+import json, os, sys, time
+sys.path.insert(0, sys.argv[1])
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+import numpy as np
+from streamstab import consistency, flow, synthetic
+h, w, seed, steps = (int(x) for x in sys.argv[2:6])
+seq = synthetic.translating_sequence(frames=2 + steps, height=h, width=w, step=(2, 1), seed=seed)
+prov = flow.BuiltinFlow(flow.FlowOptions())
+state = consistency.SessionState(params=consistency.preset("default"))
+state.push_pair(1, seq.inputs[0], seq.processed[0])
+state.push_pair(2, seq.inputs[1], seq.processed[1])
+times = []
+for k in range(steps):
+    state.push_pair(3 + k, seq.inputs[2 + k], seq.processed[2 + k])
+    p = state.params
+    state.params = consistency.ConsistencyParams(k1=0.3 if k % 2 == 0 else 0.5,
+                                                 k2=0.5 if k % 2 == 0 else 0.3,
+                                                 lam=2.0 if k % 2 == 0 else 0.5)
+    t0 = time.perf_counter()
+    consistency.stabilize_step(state, prov)
+    times.append(time.perf_counter() - t0)
+print(json.dumps({"times": times}))
+"""
+
+
+def _ref_available():
+    return os.path.isdir(os.path.join(REF_DIR, "streamstab"))
+
+
+def _host_info():
+    info = {"nproc": os.cpu_count() or 1}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    info["mem_available_gb"] = round(int(line.split()[1]) / 2**20, 1)
+    except OSError:
+        pass
+    return info
+
+
+def run_reference_processes(h, w, procs, steps):
+    """``procs`` independent streams, one reference process each (one core
+    each: OMP/BLAS threads 1), ``steps`` timed stabilize_step calls each.
+    Returns (per-stream step seconds list, wall seconds of the parallel run)."""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               PYTHONPATH=REF_DIR)
+    t0 = time.perf_counter()
+    ps = [subprocess.Popen([sys.executable, "-c", _REF_WORKER, REF_DIR, str(h), str(w), str(s),
+                            str(steps)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                           text=True, env=env) for s in range(procs)]
+    outs = [p.communicate() for p in ps]
+    wall = time.perf_counter() - t0
+    times = []
+    for (o, e), p in zip(outs, ps):
+        if p.returncode != 0:
+            raise RuntimeError(f"reference worker failed: {e[-500:]}")
+        times.append(json.loads(o.strip().splitlines()[-1])["times"])
+    return times, wall
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    h, w = args.height, args.width
+    info = _host_info()
+    if _ref_available():
+        # one process per host core (memory permitting: ~2.5 GB per 1080p
+        # stream), one timed 1080p step each (~25 s of CPU work): a bounded
+        # sample; a per-process untimed warm-up would double the run
+        mem = info.get("mem_available_gb", 64.0)
+        per = 2.5 * (h * w) / (1080 * 1920)
+        procs = max(1, min(info["nproc"], int(mem / max(per, 0.1)), 64))
+        times, wall = run_reference_processes(h, w, procs, 1)
+        step_s = [t for ts in times for t in ts]
+        per_stream = 1.0 / _med(step_s)
+        aggregate = procs / max(max(step_s), 1e-9)
+        kind, sample = "reference", (
+            f"reference streamstab (baseline/_ref, installed from /root/reference) "
+            f"stabilize_step with BuiltinFlow(FlowOptions()) -- its default provider, DIS -- "
+            f"default preset + the interactive schedule, 150 iterations, {w}x{h}: {procs} "
+            f"independent streams, one process per core (BLAS threads 1), 1 timed step each")
+        value = aggregate
+        extra = {"per_stream_fps": round(per_stream, 5), "processes": procs,
+                 "step_s_median": round(_med(step_s), 3), "wall_s": round(wall, 1)}
+    else:
+        sec, cores, sample = _port_step_seconds(h, w, "fp32", 10.0)
+        kind, value, procs = "port", 1.0 / sec, cores
+        extra = {"note": "baseline/_ref absent: oracle port timed instead"}
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "frames/s",
+        "n_gpus": world, "steps": 1, "warmup": 0,
+        "ms_per_step": round(1e3 / value, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": dict({"workload": f"{w}x{h}, the reference's own step and default flow "
+                                    "provider on the host cores (aggregate over streams)"},
+                       **extra, host=info),
+        "cpu_baseline": {"value": round(value, 5), "unit": "frames/s", "cores": procs,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def _port_step_seconds(h, w, flow_kind, budget_s):
+    """The oracle port (oracle/, C + numpy CNN restatement) on all host
+    threads: consistency step in full; CNN flow on a 1/16-area crop scaled by
+    area.  Used only when the reference itself is not installed."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import flownet_oracle as fo
+    import numpy as np
     import oracle as orc
+
     from paper_2301_00750_b200 import liteflownet as lf
     from paper_2301_00750_b200 import synthetic
 
@@ -158,11 +309,8 @@ def _cpu_step_seconds(h, w, flow_kind, budget_s):
         orc.run_step(seq.inputs[0], seq.processed[0], seq.inputs[1], seq.processed[1],
                      seq.inputs[2], seq.processed[2], seq.processed[0], fp, fn, orc.Params())
         cons.append(time.perf_counter() - t0)
-    t_cons = sum(cons) / len(cons)
     t_flow = 0.0
-    sample = f"{len(cons)} full {w}x{h} consistency steps (oracle/streamstab_oracle.c, {cores} threads)"
-    if flow_kind == "dis":
-        sample += " (DIS flow not included: no CPU restatement of it on the box)"
+    sample = f"{len(cons)} {w}x{h} consistency steps (oracle/streamstab_oracle.c, {cores} threads)"
     if flow_kind in ("fp32", "bf16"):
         ch, cw = max(64, h // 4), max(64, w // 4)
         scale = (math.ceil(h / 64) * math.ceil(w / 64)) / (math.ceil(ch / 64) * math.ceil(cw / 64))
@@ -175,42 +323,462 @@ def _cpu_step_seconds(h, w, flow_kind, budget_s):
         pb = fo.pyramid(wts, b)
         t0 = time.perf_counter()
         fo.flow(wts, a, b, pyr1=pa, pyr2=pb)
-        t_est = time.perf_counter() - t0
-        t_flow = scale * (t_pyr + 2 * t_est)
-        sample += (f" + flow CNN restatement (oracle/flownet_oracle.py, numpy) timed on a "
-                   f"{cw}x{ch} crop and scaled x{scale:.1f} by area")
-    return t_cons + t_flow, cores, sample
-
-
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
-    h, w = args.height, args.width
-    steps = max(1, min(args.steps, 3))
-    warm = 1 if args.warmup > 0 else 0  # one untimed sample (each is ~4 s of CPU work)
-    for _ in range(warm):
-        _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
-    secs, cores, sample = [], 0, ""
-    for _ in range(steps):
-        s, cores, sample = _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
-        secs.append(s)
-    sec = sum(secs) / len(secs)
-    fps = 1.0 / sec
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": round(fps, 5), "unit": "frames/s",
-        "n_gpus": world, "steps": len(secs), "warmup": warm, "ms_per_step": round(sec * 1e3, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": f"{w}x{h} single stream, default preset, 150 iterations, "
-                               f"flow={args.flow}"},
-        "cpu_baseline": {"value": round(fps, 5), "unit": "frames/s", "cores": cores,
-                         "kind": "port", "sample": sample},
-        "e2e": {"value": round(fps, 5), "unit": "frames/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }), flush=True)
+        t_flow = scale * (t_pyr + 2 * (time.perf_counter() - t0))
+        sample += f" + CNN restatement on a {cw}x{ch} crop scaled x{scale:.1f} by area"
+    return sum(cons) / len(cons) + t_flow, cores, sample
 
 
 # ---------------------------------------------------------------------------
+# GPU arm
+class Env:
+    def __init__(self, torch, dist, rank, world, local):
+        import paper_2301_00750_b200 as ss
+        from paper_2301_00750_b200 import _lib
+
+        self.torch, self.dist, self.rank, self.world, self.local = torch, dist, rank, world, local
+        self.ss, self.lib_mod, self.L = ss, _lib, _lib.lib()
+        self.peaks, self.peaks_src = load_peaks()
+        self._flows = {}
+
+    def flow(self, kind):
+        if kind not in self._flows:
+            ss = self.ss
+            if kind == "constant":
+                self._flows[kind] = ss.ConstantFlow(2, 1)
+            elif kind == "dis":
+                from paper_2301_00750_b200.flow import BuiltinFlow
+
+                self._flows[kind] = BuiltinFlow()  # the reference's default provider
+            else:
+                self._flows[kind] = ss.LiteFlowNet(seed=0, precision=kind)
+        return self._flows[kind]
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max_ms(self, ms):
+        from paper_2301_00750_b200.sharding import max_over_ranks
+
+        return max_over_ranks(ms, self.dist, device="cuda")
+
+
+FLOW_DESC = {"fp32": "lite flow CNN, fp32-class (3xTF32 tcgen05 convs, fp32 activations), "
+                     "random-init seeded weights",
+             "bf16": "lite flow CNN, bf16 tcgen05 convs, random-init seeded weights",
+             "dis": "reference built-in DIS flow (BuiltinFlow, FlowOptions()) on GPU, "
+                    "bit-identical to flow.py (tests/test_gpu_fullsize.py)",
+             "constant": "ConstantFlow(2,1) on device"}
+
+
+def run_stream(env, h, w, flow_kind, steps, warmup, e2e=True, e2e_python=False, seed=0):
+    """One stream on this rank's GPU: device-timed K steps (+ e2e)."""
+    torch, ss, L, lib = env.torch, env.ss, env.L, env.lib_mod
+    from paper_2301_00750_b200.consistency import _run_step, _start_flow_to_prev
+    from paper_2301_00750_b200.synthetic import DeviceSequence
+
+    flow = env.flow(flow_kind)
+    seq = DeviceSequence(h, w, step=(2, 1), seed=seed + env.rank)
+    pool_n = 8
+    pool = [seq.frame(k + 1) for k in range(pool_n)]
+    torch.cuda.synchronize()
+    state = ss.SessionState(params=params_for(0))
+    stream = torch.cuda.current_stream()
+    pos = [0]
+
+    def push():
+        pos[0] += 1
+        i, p = pool[(pos[0] - 1) % pool_n]
+        state.push_pair(pos[0], i, p)
+
+    push()
+    push()
+
+    def step():
+        _start_flow_to_prev(state, flow)  # stabilize_stream's order
+        push()
+        # stage the next pair (device -> device on the session's upload
+        # stream): ss_step then computes its pyramid behind the solver too
+        i2, p2 = pool[pos[0] % pool_n]
+        _check(L.ss_stage_pair(state.handle, pos[0] + 1, i2.data_ptr(), p2.data_ptr(),
+                               lib.SS_F32, lib.SS_DEVICE), L)
+        state.params = params_for(pos[0])
+        _run_step(state, flow, with_next=True, return_host=False)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    fl, bl, so = [], [], []
+    env.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(env.local).start()
+    n0 = int(L.ss_kernel_launches())
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+        tm = state.last_timing
+        fl.append(tm.flow_ms)
+        bl.append(tm.warp_blend_ms)
+        so.append(tm.solve_ms)
+    _check(L.ss_session_join(state.handle), L)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = int(L.ss_kernel_launches()) - n0
+    clocks = sampler.stop()
+    total_ms = env.max_ms(ev0.elapsed_time(ev1))
+    res = {"ms_per_step": total_ms / steps, "fps": env.world * steps * 1e3 / total_ms,
+           "launches": launches, "clocks": clocks,
+           "stage_ms": {"flow": _med(fl), "warp_blend": _med(bl), "solve": _med(so)}}
+    if e2e:
+        res["e2e"] = run_e2e_abi(env, state, pool, flow_kind, h, w, steps, warmup)
+    if e2e_python:
+        res["e2e_python"] = run_e2e_python(env, flow, h, w, steps, warmup)
+    if flow_kind in ("fp32", "bf16") and h * w >= 1920 * 1080:
+        res["est3_1"] = time_conv(env, state)
+    del state
+    torch.cuda.synchronize()
+    return res
+
+
+def time_conv(env, state):
+    """est3_1 (1/8-res 3x3 conv, the flow network's heaviest) timed live on
+    the session's buffers (CUDA events, 20 launches)."""
+    L = env.L
+    cms, cfl = ctypes.c_float(0.0), ctypes.c_double(0.0)
+    _check(L.ss_session_time_conv(state.handle, 3, 20, ctypes.byref(cms), ctypes.byref(cfl)), L)
+    return {"ms": cms.value, "gflop": cfl.value / 1e9}
+
+
+def run_e2e_abi(env, state, pool, flow_kind, h, w, steps, warmup):
+    """The same step through the C ABI from pinned host memory: the pair's
+    H2D and O_t's D2H inside the timed region, every step."""
+    torch, L, lib = env.torch, env.L, env.lib_mod
+    from paper_2301_00750_b200._dev import params_struct
+
+    n_host = 4
+    host_i = [pool[k][0].cpu().pin_memory() for k in range(n_host)]
+    host_p = [pool[k][1].cpu().pin_memory() for k in range(n_host)]
+    outs = [torch.empty((h, w, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+    sess = state.handle
+    pos = [int(L.ss_solved_through(sess)) + 1]
+    use_cnn = flow_kind in ("fp32", "bf16")
+    if use_cnn:
+        _check(L.ss_session_attach_flownet(sess, env.flow(flow_kind).handle()), L)
+
+    def step(k):
+        pos[0] += 1
+        if use_cnn:
+            # flow t -> t-1 needs only buffered frames: start it on the side
+            # stream first so the upload of frame t+1 overlaps it
+            _check(L.ss_session_compute_flow(sess, 0), L)
+        _check(L.ss_push_pair(sess, pos[0], host_i[k % n_host].data_ptr(),
+                              host_p[k % n_host].data_ptr(), lib.SS_F32, lib.SS_HOST), L)
+        t = int(L.ss_solved_through(sess)) + 1
+        if use_cnn:
+            _check(L.ss_session_compute_flow(sess, 1), L)
+        elif flow_kind == "dis":
+            for which in (0, 1):
+                _check(L.ss_session_compute_dis_flow(sess, which, 5, 9, 4, 1), L)
+        else:
+            _check(L.ss_set_constant_flow(sess, 0, 2.0, 1.0, -1), L)
+            _check(L.ss_set_constant_flow(sess, 1, 2.0, 1.0, 1), L)
+        # the next pair's upload overlaps this step (ss_push_pair swaps it in)
+        _check(L.ss_stage_pair(sess, pos[0] + 1, host_i[(k + 1) % n_host].data_ptr(),
+                               host_p[(k + 1) % n_host].data_ptr(), lib.SS_F32, lib.SS_HOST), L)
+        prm = params_struct(params_for(t))
+        it = ctypes.c_int(0)
+        _check(L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)), L)
+        _check(L.ss_output_async(sess, outs[k % 2].data_ptr(), lib.SS_F32, lib.SS_HOST), L)
+
+    for k in range(warmup):
+        step(k)
+    torch.cuda.synchronize()
+    env.barrier()
+    # three back-to-back windows of K steps (host wall clock, device
+    # synchronised at both ends of each); the median window is reported
+    dts, k0 = [], warmup
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for k in range(k0, k0 + steps):
+            step(k)
+        _check(L.ss_output_wait(sess), L)
+        torch.cuda.synchronize()
+        dts.append(time.perf_counter() - t0)
+        k0 += steps
+    dt = env.max_ms(sorted(dts)[1] * 1e3) / 1e3
+    return {"value": round(env.world * steps / dt, 3), "unit": "frames/s",
+            "windows_fps": [round(env.world * steps / x, 2) for x in dts],
+            "h2d_bytes_per_step": 2 * h * w * 3 * 4, "d2h_bytes_per_step": h * w * 3 * 4,
+            "path": "C ABI per step: ss_session_compute_flow(0) + ss_push_pair (pair staged from "
+                    "pinned host f32 by the previous step's ss_stage_pair) + "
+                    "ss_session_compute_flow(1) + ss_stage_pair(next pair) + ss_step + "
+                    "ss_output_async (pinned, double-buffered)",
+            "timer": "host wall clock around K steps, device synchronised at both ends; median "
+                     "of 3 consecutive windows"}
+
+
+def run_e2e_python(env, flow, h, w, steps, warmup):
+    """The drop-in numpy API, as the reference's service loop calls it
+    (service.py:206-226): SessionState.push_pair(numpy) + stabilize_step ->
+    numpy O_t, with the interactive params set between frames."""
+    import numpy as np
+
+    ss, torch = env.ss, env.torch
+    from paper_2301_00750_b200.consistency import _start_flow_to_prev
+    from paper_2301_00750_b200.synthetic import DeviceSequence
+
+    seq = DeviceSequence(h, w, step=(2, 1), seed=7 + env.rank)
+    frames = [tuple(np.ascontiguousarray(x.cpu().numpy()) for x in seq.frame(k + 1))
+              for k in range(4)]
+    state = ss.SessionState(params=params_for(0))
+    pos = [0]
+
+    def push():
+        pos[0] += 1
+        i, p = frames[(pos[0] - 1) % len(frames)]
+        state.push_pair(pos[0], i, p)
+
+    push()
+    push()
+
+    def step():
+        _start_flow_to_prev(state, flow)  # stabilize_stream's order
+        push()
+        state.params = params_for(pos[0])
+        out = ss.stabilize_step(state, flow)
+        assert out.dtype == np.float32 and out.shape == (h, w, 3)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    env.barrier()
+    dts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            step()
+        dts.append(time.perf_counter() - t0)
+    dt = env.max_ms(sorted(dts)[1] * 1e3) / 1e3
+    return {"value": round(env.world * steps / dt, 3), "unit": "frames/s",
+            "windows_fps": [round(env.world * steps / x, 2) for x in dts],
+            "h2d_bytes_per_step": 2 * h * w * 3 * 4, "d2h_bytes_per_step": h * w * 3 * 4,
+            "path": "numpy in / numpy out: SessionState.push_pair(pageable numpy f32) + "
+                    "stabilize_step (returns O_t as numpy)"}
+
+
+def rooflines(env, h, w, res, flow_kind):
+    """Dominant kernel by live share = K2 (solver); K1 and the flow network
+    as secondaries.  Algorithmic work per launch: DESIGN.md §4."""
+    peaks, src = env.peaks, env.peaks_src
+    st = res["stage_ms"]
+    n = h * w
+    solve_ops = SOLVER_OPS_PER_ELEM * 3 * n * SOLVER_ITERS
+    achieved = solve_ops / (st["solve"] * 1e-3) / 1e12
+    traffic = _traffic_table()
+    n_pass = math.ceil(SOLVER_ITERS / 8)
+    line = {
+        "kernel": "k_sgd_v2<8> (K2: 150 SGD-momentum iterations as 19 temporally blocked passes)",
+        "bound": "fp32", "achieved": round(achieved, 3), "peak": round(FP32_PEAK_TOPS, 2),
+        "unit": "TFLOP/s", "frac": round(achieved / FP32_PEAK_TOPS, 4),
+        "traffic": traffic.get("k_sgd_v2 solver pass") if (h, w) == (1080, 1920) else None,
+        "algorithmic": f"{SOLVER_OPS_PER_ELEM} FP32 ops/px/channel/iteration x 3 x {n} px x "
+                       f"{SOLVER_ITERS} = {solve_ops / 1e9:.2f} G ops per solve",
+        "peak_source": "measured FP32 result rate (tools/fp32_rate_probe.cu: 126.5/clk/SM) x 148 "
+                       "SMs x 1965 MHz; MEASURED_PEAKS.json has no FP32 entry",
+        "launch_ms": round(st["solve"] / n_pass, 5), "stage_ms": round(st["solve"], 4),
+        "share_of_step": round(st["solve"] / res["ms_per_step"], 3),
+    }
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    k1 = K1_BYTES_PER_PX * n / (st["warp_blend"] * 1e-3) / 1e9
+    sec = [{"kernel": "k_presolve (K1: fused warps, weights, blends, w_c, dP)", "bound": "hbm",
+            "achieved": round(k1, 1), "peak": hbm, "unit": "GB/s", "frac": round(k1 / hbm, 4),
+            "traffic": traffic.get("k_presolve K1") if (h, w) == (1080, 1920) else None,
+            "launch_ms": round(st["warp_blend"], 5), "peak_source": f"hbm_gbs {src}"}]
+    if flow_kind in ("fp32", "bf16"):
+        bf = float(peaks.get("bf16_tflops_sustained", 1400.0))
+        peak = bf if flow_kind == "bf16" else bf / 6.0
+        psrc = (f"bf16_tflops_sustained {src}" if flow_kind == "bf16" else
+                f"bf16_tflops_sustained {src} / 2 (tf32 rate) / 3 (3xTF32 MMAs per product)")
+        gflop = FLOW_GFLOP_1080 * n / (1920 * 1080)
+        sec.append({"kernel": "lite flow CNN stage (1 pyramid + 2 flows, concurrent streams)",
+                    "bound": "tensor", "achieved": round(gflop / st["flow"], 2), "peak": round(peak, 1),
+                    "unit": "TFLOP/s", "frac": round(gflop / st["flow"] / peak, 4),
+                    "stage_ms": round(st["flow"], 4), "peak_source": psrc})
+        if "est3_1" in res:
+            c = res["est3_1"]
+            tf = c["gflop"] / c["ms"]
+            sec.append({"kernel": "k_conv_tc3 est3_1 (1/8-res 3x3 conv, 147 live -> 128 ch)",
+                        "bound": "tensor", "achieved": round(tf, 2), "peak": round(peak, 1),
+                        "unit": "TFLOP/s", "frac": round(tf / peak, 4), "launch_ms": round(c["ms"], 5),
+                        "traffic": traffic.get("k_conv_tc3 est3_1 " + flow_kind),
+                        "peak_source": psrc})
+    line["secondary"] = sec
+    return line
+
+
+def _traffic_table():
+    """DRAM bytes per launch of the roofline kernels, from the committed ncu
+    --set full captures (profiles/r02_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
+            tab = json.load(f)["kernels"]
+    except (OSError, KeyError, ValueError):
+        return {}
+    return {k: v["traffic_bytes"] for k, v in tab.items()}
+
+
+def config_entry(env, name, h, w, flow_kind, res, workload, rl=True):
+    e = {"workload": workload, "value": round(res["fps"], 3), "unit": "frames/s",
+         "ms_per_step": round(res["ms_per_step"], 4), "flow": FLOW_DESC[flow_kind],
+         "stage_ms_median": {k: round(v, 4) for k, v in res["stage_ms"].items()},
+         "gpu_launches": res["launches"], "clocks": res["clocks"]}
+    if "e2e" in res:
+        e["e2e"] = res["e2e"]
+    if rl:
+        e["roofline"] = rooflines(env, h, w, res, flow_kind)
+    return e
+
+
+def run_configs(env, args):
+    """BASELINE configs other than the headline, each device-timed with e2e
+    and a roofline (N = 1; configs[4] runs at every N)."""
+    steps = max(5, min(args.steps, 10))
+    warm = max(3, min(args.warmup, 5))
+    out = {}
+    if env.world == 1:
+        r = run_stream(env, 360, 640, "fp32", steps * 2, warm, e2e=True)
+        out["configs[0]"] = config_entry(
+            env, "0", 360, 640, "fp32", r,
+            "640x360 stream, random-init lite flow net (fp32 path), default preset + interactive "
+            "schedule (BASELINE configs[0], the reference's CPU-runnable case)")
+        r = run_stream(env, H, W, "bf16", steps, warm, e2e=True)
+        out["configs[2]"] = config_entry(
+            env, "2", H, W, "bf16", r,
+            "1920x1080 single stream, bf16 tensor-core flow path (stated tolerance vs the fp32 "
+            "oracle: EPE mean <= 0.05 px, max <= 0.3 px, step PSNR >= 45 dB)")
+        r = run_stream(env, 2160, 3840, "fp32", steps, warm, e2e=True)
+        out["configs[3]"] = config_entry(
+            env, "3", 2160, 3840, "fp32", r, "3840x2160 single stream, lite flow CNN fp32 path")
+        r = run_stream(env, H, W, "dis", steps, warm, e2e=True)
+        out["dis_1080p"] = config_entry(
+            env, "dis", H, W, "dis", r,
+            "1920x1080 single stream with the reference's own flow provider (BuiltinFlow, DIS) on "
+            "the GPU: like for like with the reference arm")
+    out["configs[4]"] = run_multi(env, args.streams_total, H, W, "fp32", steps, warm)
+    return out
+
+
+class ThreadedSessions:
+    """configs[4] backend for sharding.run_sharded: one session per owned
+    stream, each on its own CUDA stream and driven by its own host thread (the
+    C ABI releases the GIL), so the streams' kernels overlap on the GPU.
+    Device time = earliest start event to latest end event (CUDA events)."""
+
+    def __init__(self, env, h, w, flow_kind):
+        self.env, self.h, self.w, self.flow_kind = env, h, w, flow_kind
+        self.launches, self.clocks = 0, None
+
+    def open(self, stream_ids):
+        env, torch = self.env, self.env.torch
+        from paper_2301_00750_b200.synthetic import DeviceSequence
+
+        self.ids = stream_ids
+        self.flow = env.flow(self.flow_kind)
+        seq = DeviceSequence(self.h, self.w, step=(2, 1), seed=env.rank)
+        self.pool = [seq.frame(k + 1) for k in range(8)]
+        self.streams = [torch.cuda.Stream() for _ in stream_ids]
+        self.states, self.pos = [], [0] * len(stream_ids)
+        for s_ in range(len(stream_ids)):
+            with torch.cuda.stream(self.streams[s_]):
+                self.states.append(env.ss.SessionState(params=params_for(0)))
+                for _ in range(2):
+                    self._push(s_)
+
+    def _push(self, s_):
+        self.pos[s_] += 1
+        i, p = self.pool[(self.pos[s_] + 3 * self.ids[s_] - 1) % len(self.pool)]
+        self.states[s_].push_pair(self.pos[s_], i, p)
+
+    def _step(self, s_):
+        from paper_2301_00750_b200.consistency import _run_step, _start_flow_to_prev
+
+        st = self.states[s_]
+        _start_flow_to_prev(st, self.flow)
+        self._push(s_)
+        st.params = params_for(self.pos[s_])
+        _run_step(st, self.flow, with_next=True, return_host=False)
+
+    def warm(self, steps):
+        torch = self.env.torch
+        for s_ in range(len(self.ids)):  # serially (one-time setup, graph capture)
+            with torch.cuda.stream(self.streams[s_]):
+                for _ in range(steps):
+                    self._step(s_)
+        torch.cuda.synchronize()
+
+    def run_timed(self, steps):
+        env, torch, L = self.env, self.env.torch, self.env.L
+        S = len(self.ids)
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(S)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(S)]
+        gate = threading.Barrier(S)
+        errors = []
+
+        def worker(s_):
+            try:
+                with torch.cuda.stream(self.streams[s_]):
+                    gate.wait()
+                    ev0[s_].record(self.streams[s_])
+                    for _ in range(steps):
+                        self._step(s_)
+                    _check(L.ss_session_join(self.states[s_].handle), L)
+                    ev1[s_].record(self.streams[s_])
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+
+        ref = torch.cuda.Event(enable_timing=True)
+        ref.record()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(env.local).start()
+        n0 = int(L.ss_kernel_launches())
+        threads = [threading.Thread(target=worker, args=(s_,)) for s_ in range(S)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        torch.cuda.synchronize()
+        self.launches = int(L.ss_kernel_launches()) - n0
+        self.clocks = sampler.stop()
+        if errors:
+            raise errors[0]
+        return max(ref.elapsed_time(e) for e in ev1) - min(ref.elapsed_time(e) for e in ev0)
+
+    def close(self):
+        self.states = []
+        self.env.torch.cuda.synchronize()
+
+
+def run_multi(env, n_total, h, w, flow_kind, steps, warmup):
+    """configs[4]: ``n_total`` concurrent streams sharded over the ranks
+    (sharding.run_sharded: stream i -> rank i mod N, max-over-ranks time)."""
+    from paper_2301_00750_b200.sharding import run_sharded
+
+    be = ThreadedSessions(env, h, w, flow_kind)
+    r = run_sharded(n_total, env.world, env.rank, be, steps, warmup, env.dist, device="cuda")
+    S = len(r["streams"])
+    return {"workload": f"{n_total} concurrent {w}x{h} streams sharded over {env.world} GPU(s) "
+                        f"({S} per GPU, stream i -> rank i mod N), flow={flow_kind}, default "
+                        "preset + interactive schedule (BASELINE configs[4])",
+            "value": round(r["fps"], 3), "unit": "frames/s", "streams_per_gpu": S,
+            "per_stream_fps": round(r["per_stream_fps"], 3),
+            "ms_per_step": round(r["ms"] / steps, 4),
+            "scaling": "strong (fixed total of streams)", "gpu_launches": be.launches,
+            "clocks": be.clocks,
+            "timer": "CUDA events per stream: earliest start to latest end, max over ranks"}
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -225,380 +793,53 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    import paper_2301_00750_b200 as ss
-    from paper_2301_00750_b200 import _lib
-    from paper_2301_00750_b200.consistency import _run_step, _start_flow_to_prev
-    from paper_2301_00750_b200.synthetic import DeviceSequence
-
+    env = Env(torch, dist, rank, world, local)
     h, w = args.height, args.width
-    L = _lib.lib()
-    seq = DeviceSequence(h, w, step=(2, 1), seed=rank)
-    if args.flow == "constant":
-        flow = ss.ConstantFlow(2, 1)
-    elif args.flow == "dis":
-        from paper_2301_00750_b200.flow import BuiltinFlow
 
-        flow = BuiltinFlow()  # the reference's default provider (flow.py:361-369)
-    else:
-        flow = ss.LiteFlowNet(seed=0, precision=args.flow)
-    # frames are generated in HBM before any timed region (a pool cycled by
-    # position; the consistency step never sees the generator)
-    pool_n = 16
-    pool = [seq.frame(k + 1) for k in range(pool_n)]
-    torch.cuda.synchronize()
-    if args.streams > 1:
-        run_multi(args, torch, dist, rank, world, local, L, ss, flow, pool)
-        return
-    state = ss.SessionState(params=params_for(0))
-    stream = torch.cuda.current_stream()
-    pos = 0
+    res = run_stream(env, h, w, args.flow, args.steps, args.warmup, e2e=not args.no_e2e,
+                     e2e_python=not args.no_e2e)
+    roofline = rooflines(env, h, w, res, args.flow)
+    configs = None if args.no_configs else run_configs(env, args)
 
-    def push():
-        nonlocal pos
-        pos += 1
-        i, p = pool[(pos - 1) % pool_n]
-        state.push_pair(pos, i, p)
-
-    push()
-    push()
-
-    def step():
-        _start_flow_to_prev(state, flow)  # stabilize_stream's order
-        push()
-        # stage the next pair (device -> device on the session's upload
-        # stream, overlapping this step): ss_step then also computes its
-        # pyramid behind the solver, and the next push swaps it in
-        i2, p2 = pool[pos % pool_n]
-        _check(L.ss_stage_pair(state.handle, pos + 1, i2.data_ptr(), p2.data_ptr(), _lib.SS_F32,
-                               _lib.SS_DEVICE), L)
-        state.params = params_for(pos)
-        _run_step(state, flow, with_next=True, return_host=False)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    # ---- device-timed region -------------------------------------------------
-    sampler = ClockSampler(local)
-    # one event pair around all K steps: ss_step pre-launches the next step's
-    # pyramid and flow t+1 -> t behind its solver, so per-step intervals would
-    # miss the work between one step's end and the next one's start.  The
-    # region ends with the session's internal streams joined, so it holds
-    # exactly K pre-launched pyramids and flows (the first ones ran during
-    # warm-up).  No L2 flush: each step touches > 0.5 GB (ring frames, both
-    # flows' activations, solver iterates), several times the 126 MB L2.
-    ev_start = torch.cuda.Event(enable_timing=True)
-    ev_end = torch.cuda.Event(enable_timing=True)
-    flow_ms, blend_ms, solve_ms = [], [], []
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    sampler.start()
-    launches0 = int(L.ss_kernel_launches())
-    ev_start.record(stream)
-    for k in range(args.steps):
-        step()
-        tm = state.last_timing
-        flow_ms.append(tm.flow_ms)
-        blend_ms.append(tm.warp_blend_ms)
-        solve_ms.append(tm.solve_ms)
-    _check(L.ss_session_join(state.handle), L)
-    ev_end.record(stream)
-    torch.cuda.synchronize()
-    launches = int(L.ss_kernel_launches()) - launches0  # this library's kernels, timed steps
-    clocks = sampler.stop()
-    total_ms = ev_start.elapsed_time(ev_end)
-    if dist:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = world * 1e3 / ms_per_step  # frames/s over all ranks (one stream each)
-
-    e2e = None if args.no_e2e else run_e2e(args, L, state, pool, flow, torch, dist)
-
-    # ---- roofline: stage times are CUDA events on the session stream ----------
-    med = lambda xs: sorted(xs)[len(xs) // 2]  # noqa: E731
-    med_flow, med_blend, med_solve = med(flow_ms), med(blend_ms), med(solve_ms)
-    n_pass = math.ceil(150 / SOLVER_K)
-    per_pass_ms = med_solve / n_pass
-    flops_per_pass = 14.0 * h * w * 3 * SOLVER_K  # algorithmic FP32 ops, SURVEY 8(d)
-    fp32_peak = 148 * 128 * 1.965e9 / 1e12
-    achieved = flops_per_pass / (per_pass_ms * 1e-3) / 1e12
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except OSError:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    bf16_peak = float(peaks.get("bf16_tflops_sustained", 1412.7))
-    k1_gbs = 130.0 * h * w / (med_blend * 1e-3) / 1e9
-    traffic = _traffic_table()
-    solver_line = {
-        "kernel": f"k_sgd_tma<{SOLVER_K}> (solver pass = {SOLVER_K} SGD-momentum iterations)",
-        "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 2),
-        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4),
-        "traffic": traffic.get("k_sgd_tma<8> solver pass") if SOLVER_K == 8 else None,
-        "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1965 MHz non-FMA op rate "
-                       "(MEASURED_PEAKS.json has no FP32 entry)",
-        "launch_ms": round(per_pass_ms, 5), "stage_ms": round(med_solve, 4)}
-    k1_line = {
-        "kernel": "k_presolve (K1 fused warp+weights+blend)", "bound": "hbm",
-        "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-        "frac": round(k1_gbs / hbm_peak, 4), "traffic": traffic.get("k_presolve K1"),
-        "launch_ms": round(med_blend, 5),
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
-    if args.flow in ("constant", "dis"):
-        roofline = dict(solver_line, secondary=[k1_line])
-    else:
-        # the flow network is the largest stage; its heaviest kernel is the
-        # 1/8-resolution first estimator conv, timed live on the session's
-        # buffers (CUDA events, 20 launches)
-        cms, cfl = ctypes.c_float(0.0), ctypes.c_double(0.0)
-        _check(L.ss_session_time_conv(state.handle, 3, 20, ctypes.byref(cms), ctypes.byref(cfl)), L)
-        conv_tf = cfl.value / (cms.value * 1e-3) / 1e12
-        # 3xTF32: tf32 runs at half the bf16 rate and each fp32 product is 3 MMAs
-        conv_peak = bf16_peak if args.flow == "bf16" else bf16_peak / 6.0
-        roofline = {
-            "kernel": "k_conv_tc3<%d,1,0> est3_1 (1/8-res 3x3 conv, 147 live -> 128 ch; TMA halo tiles, "
-                      "tcgen05/TMEM, %s)" % ((0, "bf16 operands") if args.flow == "bf16" else (1, "3xTF32")),
-            "bound": "tensor", "achieved": round(conv_tf, 2), "peak": round(conv_peak, 1),
-            "unit": "TFLOP/s", "frac": round(conv_tf / conv_peak, 4),
-            "traffic": traffic.get("k_conv_tc3 est3_1 " + ("bf16" if args.flow == "bf16" else "fp32")),
-            "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained" if args.flow == "bf16"
-                            else "derived: MEASURED_PEAKS bf16 sustained / 2 (tf32 rate) / 3 "
-                                 "(3xTF32 MMAs per fp32 product)"),
-            "launch_ms": round(cms.value, 5),
-            "flow_stage": {"ms": round(med_flow, 4), "gflop": 131.0,
-                           "achieved_tflops": round(131.0 / med_flow, 2)},
-            "secondary": [solver_line, k1_line],
-        }
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sec, cores, sample = _cpu_step_seconds(h, w, args.flow, budget_s=10.0)
-        cpu = {"value": round(1.0 / sec, 5), "unit": "frames/s", "cores": cores, "kind": "port",
-               "sample": sample}
+        if _ref_available():
+            # a bounded sample: one 1080p step of the reference (~25 s of CPU
+            # work, one core); the --impl reference arm runs it on every core
+            times, _ = run_reference_processes(h, w, 1, 1)
+            sec = times[0][0]
+            cpu = {"value": round(1.0 / sec, 5), "unit": "frames/s", "cores": 1,
+                   "kind": "reference",
+                   "sample": f"1 timed {w}x{h} stabilize_step of the reference (baseline/_ref, "
+                             "BuiltinFlow = its default DIS provider, 150 iterations), one core"}
+        else:
+            sec, cores, sample = _port_step_seconds(h, w, args.flow, 10.0)
+            cpu = {"value": round(1.0 / sec, 5), "unit": "frames/s", "cores": cores,
+                   "kind": "port", "sample": sample}
     line = {
-        "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": f"{w}x{h} single stream per GPU, flow={args.flow} + "
-                               "default preset with per-frame interactive k1/k2/lambda schedule, "
-                               "150 solver iterations",
-                   "flow": {"fp32": "lite flow CNN, fp32-class (3xTF32 tcgen05 convs, fp32 "
-                                    "activations), random-init seeded weights",
-                            "bf16": "lite flow CNN, bf16 tcgen05 convs, random-init seeded "
-                                    "weights",
-                            "dis": "reference built-in DIS flow (BuiltinFlow, FlowOptions()) on "
-                                   "GPU, bit-identical to flow.py on the golden cases",
-                            "constant": "ConstantFlow(2,1) on device"}[args.flow],
-                   "streams_per_gpu": 1,
-                   "l2": "not flushed: each step touches > 0.5 GB (frames, two flows' activations, solver iterates) >> 126 MB L2",
-                   "stage_ms_median": {"flow": round(med_flow, 4), "warp_blend": round(med_blend, 4),
-                                       "solve": round(med_solve, 4)}},
+        "metric": METRIC, "value": round(res["fps"], 3), "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if args.flow == "bf16" else "f32", "data": "synthetic",
+        "config": {"workload": f"{w}x{h} single stream per GPU (BASELINE configs[1]), "
+                               f"flow={args.flow}, default preset with a per-frame interactive "
+                               "k1/k2/lambda schedule, 150 solver iterations",
+                   "flow": FLOW_DESC[args.flow], "streams_per_gpu": 1,
+                   "l2": "not flushed: each step touches > 0.5 GB (frames, two flows' "
+                         "activations, solver iterates) >> 126 MB L2",
+                   "stage_ms_median": {k: round(v, 4) for k, v in res["stage_ms"].items()}},
         "roofline": roofline,
         "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "clocks": clocks,
+        "e2e": res.get("e2e"),
+        "e2e_python_api": res.get("e2e_python"),
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+        "configs": configs,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
-
-
-def run_multi(args, torch, dist, rank, world, local, L, ss, flow, pool):
-    """S independent streams per GPU (BASELINE configs[4]): one session per
-    stream, each on its own CUDA stream and driven by its own host thread
-    (the C ABI releases the GIL), so their kernels overlap on the GPU.  Device
-    time = earliest start event to latest end event over the streams (CUDA
-    events), max over ranks; the streams' working set (S x 0.6 GB) is far
-    larger than L2, so no flush is needed between steps."""
-    from paper_2301_00750_b200.consistency import _run_step, _start_flow_to_prev
-
-    S = args.streams
-    pool_n = len(pool)
-    streams = [torch.cuda.Stream() for _ in range(S)]
-    states, pos = [], [0] * S
-    for s_ in range(S):
-        with torch.cuda.stream(streams[s_]):
-            states.append(ss.SessionState(params=params_for(0)))
-
-    def step(s_):
-        st = states[s_]
-        _start_flow_to_prev(st, flow)
-        pos[s_] += 1
-        i, p = pool[(pos[s_] + 3 * s_ - 1) % pool_n]
-        st.push_pair(pos[s_], i, p)
-        st.params = params_for(pos[s_])
-        _run_step(st, flow, with_next=True, return_host=False)
-
-    for s_ in range(S):  # prime + warm up serially (one-time setup, graph capture)
-        with torch.cuda.stream(streams[s_]):
-            for _ in range(2):
-                pos[s_] += 1
-                i, p = pool[(pos[s_] + 3 * s_ - 1) % pool_n]
-                states[s_].push_pair(pos[s_], i, p)
-            for _ in range(args.warmup):
-                step(s_)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(S)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(S)]
-    gate = threading.Barrier(S)
-    errors = []
-
-    def worker(s_):
-        try:
-            with torch.cuda.stream(streams[s_]):
-                gate.wait()
-                ev0[s_].record(streams[s_])
-                for _ in range(args.steps):
-                    step(s_)
-                _check(L.ss_session_join(states[s_].handle), L)
-                ev1[s_].record(streams[s_])
-        except Exception as e:  # noqa: BLE001
-            errors.append(e)
-
-    ref = torch.cuda.Event(enable_timing=True)
-    ref.record()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
-    launches0 = int(L.ss_kernel_launches())
-    threads = [threading.Thread(target=worker, args=(s_,)) for s_ in range(S)]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    torch.cuda.synchronize()
-    launches = int(L.ss_kernel_launches()) - launches0
-    clocks = sampler.stop()
-    if errors:
-        raise errors[0]
-    total_ms = (max(ref.elapsed_time(e) for e in ev1) - min(ref.elapsed_time(e) for e in ev0))
-    if dist:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    frames = world * S * args.steps
-    value = frames / (total_ms * 1e-3)
-    line = {
-        "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if args.flow != "bf16" else "bf16", "data": "synthetic",
-        "config": {"workload": f"{args.width}x{args.height}, {S} concurrent streams per GPU "
-                               f"(configs[4]), flow={args.flow}, default preset with per-frame "
-                               "interactive schedule, 150 solver iterations",
-                   "streams_per_gpu": S, "per_stream_fps": round(value / (world * S), 3),
-                   "l2": "not flushed: working set of the concurrent streams >> L2"},
-        "e2e": None, "gpu_launches": launches, "clocks": clocks,
-        "roofline": None, "cpu_baseline": None,
-    }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
-
-
-def run_e2e(args, L, state, pool, flow, torch, dist):
-    """The same step through the C ABI from pinned host memory."""
-    from paper_2301_00750_b200 import _lib
-    from paper_2301_00750_b200._dev import params_struct
-
-    h, w = args.height, args.width
-    n_host = 4
-    host_i = [pool[k][0].cpu().pin_memory() for k in range(n_host)]
-    host_p = [pool[k][1].cpu().pin_memory() for k in range(n_host)]
-    # two pinned result buffers: each step's result is read back with
-    # ss_output_async, overlapping the next step (one copy in flight)
-    outs = [torch.empty((h, w, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
-    sess = state.handle
-    pos = [int(L.ss_solved_through(sess)) + 1]  # last pushed position
-    use_cnn = args.flow in ("fp32", "bf16")
-    if use_cnn:
-        _check(L.ss_session_attach_flownet(sess, flow.handle()), L)
-
-    def step(k):
-        pos[0] += 1
-        if use_cnn:
-            # flow t -> t-1 needs only buffered frames: start it on the side
-            # stream first so the host->device copy of frame t+1 overlaps it
-            # (the order consistency.stabilize_stream uses)
-            _check(L.ss_session_compute_flow(sess, 0), L)
-        _check(L.ss_push_pair(sess, pos[0], host_i[k % n_host].data_ptr(),
-                              host_p[k % n_host].data_ptr(), _lib.SS_F32, _lib.SS_HOST), L)
-        t = int(L.ss_solved_through(sess)) + 1
-        if use_cnn:
-            _check(L.ss_session_compute_flow(sess, 1), L)
-        elif args.flow == "dis":
-            for which in (0, 1):
-                _check(L.ss_session_compute_dis_flow(sess, which, 5, 9, 4, 1), L)
-        else:
-            _check(L.ss_set_constant_flow(sess, 0, 2.0, 1.0, -1), L)
-            _check(L.ss_set_constant_flow(sess, 1, 2.0, 1.0, 1), L)
-        # the next pair's upload overlaps this step (ss_push_pair swaps it in)
-        _check(L.ss_stage_pair(sess, pos[0] + 1, host_i[(k + 1) % n_host].data_ptr(),
-                               host_p[(k + 1) % n_host].data_ptr(), _lib.SS_F32, _lib.SS_HOST), L)
-        prm = params_struct(params_for(t))
-        it = ctypes.c_int(0)
-        _check(L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)), L)
-        _check(L.ss_output_async(sess, outs[k % 2].data_ptr(), _lib.SS_F32, _lib.SS_HOST), L)
-
-    for k in range(args.warmup):
-        step(k)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    # three back-to-back windows of K steps (host wall clock, device
-    # synchronised at both ends of each); the median window is reported --
-    # a single window of a host-driven loop is sensitive to host jitter
-    dts, k0 = [], args.warmup
-    for _ in range(3):
-        t0 = time.perf_counter()
-        for k in range(k0, k0 + args.steps):
-            step(k)
-        _check(L.ss_output_wait(sess), L)
-        torch.cuda.synchronize()
-        dts.append(time.perf_counter() - t0)
-        k0 += args.steps
-    dt = sorted(dts)[1]
-    if dist:
-        t = torch.tensor([dt], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    world = dist.get_world_size() if dist else 1
-    return {"value": round(world * args.steps / dt, 3), "unit": "frames/s",
-            "windows_fps": [round(world * args.steps / x, 2) for x in dts],
-            "h2d_bytes_per_step": 2 * h * w * 3 * 4, "d2h_bytes_per_step": h * w * 3 * 4,
-            "path": "C ABI per step: ss_session_compute_flow(0) + ss_push_pair (pair staged from "
-                    "pinned host f32 by the previous step's ss_stage_pair: its upload overlaps that "
-                    "step) + ss_session_compute_flow(1) + ss_stage_pair(next pair) + ss_step + "
-                    "ss_output_async (pinned, double-buffered: the result copy overlaps the next step)",
-            "timer": "host wall clock around K steps, device synchronised at both ends; median of "
-                     "3 consecutive windows"}
-
-
-def _traffic_table():
-    """DRAM bytes per launch of the roofline kernels, from the committed ncu
-    --set full captures (profiles/r01_traffic.json; tools/profile_round.sh)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            tab = json.load(f)["kernels"]
-    except (OSError, KeyError, ValueError):
-        return {}
-    return {k: v["traffic_bytes"] for k, v in tab.items()}
-
-
-def _check(rc, L):
-    if rc != 0:
-        raise RuntimeError(f"streamstab_b200 error {rc}: {L.ss_last_error().decode()}")
 
 
 if __name__ == "__main__":
