@@ -3,6 +3,7 @@
 // (consistency.py:306-413).  The index logic (3-pair ring, consecutive
 // positions, one-frame latency, error texts) follows consistency.py:321-353
 // exactly; the per-frame math is K1 (k_presolve) + K2 (solve_planar).
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <map>
@@ -82,6 +83,112 @@ __global__ void k_fill_flow(float *__restrict__ uv, uint8_t *__restrict__ valid,
     }
 }
 
+
+// Host <-> device copies from / to PAGEABLE host memory (numpy arrays: the
+// drop-in API) go through a small pinned bounce ring: the host-side memcpy of
+// chunk i+1 (several threads) overlaps the DMA of chunk i, instead of the
+// driver's single-threaded staging.  Pinned sources / destinations (cudaHostAlloc,
+// torch pin_memory) are copied directly.
+struct Bounce {
+    static constexpr size_t CHUNK = 8u << 20;
+    uint8_t *buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~Bounce()
+    {
+        for (int k = 0; k < 2; ++k) {
+            if (ev[k]) {
+                cudaEventSynchronize(ev[k]);
+                cudaEventDestroy(ev[k]);
+            }
+            if (buf[k]) cudaFreeHost(buf[k]);
+        }
+    }
+    int ensure()
+    {
+        for (int k = 0; k < 2; ++k) {
+            if (!buf[k]) SS_CUDA_TRY(cudaHostAlloc(&buf[k], CHUNK, cudaHostAllocDefault));
+            if (!ev[k]) SS_CUDA_TRY(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+        }
+        return SS_OK;
+    }
+};
+
+static bool host_pinned(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+static void par_memcpy(void *dst, const void *src, size_t n)
+{
+    constexpr size_t PIECE = 512u << 10;
+    const long pieces = (long)((n + PIECE - 1) / PIECE);
+#pragma omp parallel for schedule(static) num_threads(8) if (pieces > 1)
+    for (long i = 0; i < pieces; ++i) {
+        const size_t off = (size_t)i * PIECE;
+        std::memcpy(static_cast<uint8_t *>(dst) + off, static_cast<const uint8_t *>(src) + off,
+                    std::min(PIECE, n - off));
+    }
+}
+
+// host -> device (returns once the host source may be reused; the DMA of the
+// last chunks may still be in flight on `st`)
+static int h2d(Bounce &b, void *dst, const void *src, size_t n, cudaStream_t st)
+{
+    if (n < (256u << 10) || host_pinned(src)) {
+        SS_CUDA_TRY(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+        return SS_OK;
+    }
+    if (int rc = b.ensure()) return rc;
+    for (size_t off = 0, i = 0; off < n; off += Bounce::CHUNK, ++i) {
+        const int k = (int)(i & 1);
+        const size_t c = std::min(Bounce::CHUNK, n - off);
+        SS_CUDA_TRY(cudaEventSynchronize(b.ev[k]));  // the slot's previous DMA is done
+        par_memcpy(b.buf[k], static_cast<const uint8_t *>(src) + off, c);
+        SS_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t *>(dst) + off, b.buf[k], c,
+                                    cudaMemcpyHostToDevice, st));
+        SS_CUDA_TRY(cudaEventRecord(b.ev[k], st));
+    }
+    return SS_OK;
+}
+
+// device -> host, synchronous (the data is in dst on return)
+static int d2h(Bounce &b, void *dst, const void *src, size_t n, cudaStream_t st)
+{
+    if (n < (256u << 10) || host_pinned(dst)) {
+        SS_CUDA_TRY(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
+        SS_CUDA_TRY(cudaStreamSynchronize(st));
+        return SS_OK;
+    }
+    if (int rc = b.ensure()) return rc;
+    size_t pend_off = 0, pend_n = 0;
+    int pend_k = -1;
+    for (size_t off = 0, i = 0; off < n; off += Bounce::CHUNK, ++i) {
+        const int k = (int)(i & 1);
+        const size_t c = std::min(Bounce::CHUNK, n - off);
+        SS_CUDA_TRY(cudaEventSynchronize(b.ev[k]));
+        SS_CUDA_TRY(cudaMemcpyAsync(b.buf[k], static_cast<const uint8_t *>(src) + off, c,
+                                    cudaMemcpyDeviceToHost, st));
+        SS_CUDA_TRY(cudaEventRecord(b.ev[k], st));
+        if (pend_k >= 0) {  // drain the previous chunk while this one copies
+            SS_CUDA_TRY(cudaEventSynchronize(b.ev[pend_k]));
+            par_memcpy(static_cast<uint8_t *>(dst) + pend_off, b.buf[pend_k], pend_n);
+        }
+        pend_k = k;
+        pend_off = off;
+        pend_n = c;
+    }
+    if (pend_k >= 0) {
+        SS_CUDA_TRY(cudaEventSynchronize(b.ev[pend_k]));
+        par_memcpy(static_cast<uint8_t *>(dst) + pend_off, b.buf[pend_k], pend_n);
+    }
+    return SS_OK;
+}
+
 }  // namespace ss
 
 using namespace ss;
@@ -153,6 +260,7 @@ struct ss_session {
     // completed): an upload into them needs no ordering after the session
     bool stage_idle = true;
     cudaEvent_t xev = nullptr;  // ss_session_wait_stream / ss_session_signal_stream
+    mutable Bounce bounce;      // pageable host <-> device copies
     std::unique_ptr<dis::Estimator> dis;   // built-in flow (BuiltinFlow)
     std::unique_ptr<dis::Estimator> dis0;  // its flow to t-1, on the side stream
 };
@@ -283,6 +391,7 @@ static int copy_frame(ss_session *s, float *dst, const void *src, int c, int dty
     const size_t n = (size_t)s->h * s->w * c;
     const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (dtype == SS_F32) {
+        if (where == SS_HOST) return h2d(s->bounce, dst, src, n * sizeof(float), s->stream);
         SS_CUDA_TRY(cudaMemcpyAsync(dst, src, n * sizeof(float), kind, s->stream));
         return SS_OK;
     }
@@ -299,7 +408,11 @@ static int copy_frame(ss_session *s, float *dst, const void *src, int c, int dty
         set_error("u8 staging buffer too small");
         return SS_VALUE_ERROR;
     }
-    SS_CUDA_TRY(cudaMemcpyAsync(stage, src, n, kind, s->stream));
+    if (where == SS_HOST) {
+        if (int rc = h2d(s->bounce, stage, src, n, s->stream)) return rc;
+    } else {
+        SS_CUDA_TRY(cudaMemcpyAsync(stage, src, n, kind, s->stream));
+    }
     k_u8_to_f32<<<blocks_for((long)n, 256), 256, 0, s->stream>>>(stage, (long)n, dst);
     SS_LAUNCH_CHECK("k_u8_to_f32");
     return SS_OK;
@@ -794,11 +907,15 @@ int ss_set_flow(ss_session *s, int which, const float *uv, const uint8_t *valid,
     if (which == 0) s->dis_used = false;
     const size_t px = (size_t)s->h * s->w;
     const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    SS_CUDA_TRY(cudaMemcpyAsync(s->uv[which], uv, px * 2 * sizeof(float), kind, s->stream));
-    if (valid)
-        SS_CUDA_TRY(cudaMemcpyAsync(s->valid[which], valid, px, kind, s->stream));
-    else
-        SS_CUDA_TRY(cudaMemsetAsync(s->valid[which], 1, px, s->stream));
+    if (where == SS_HOST) {
+        if (int rc = h2d(s->bounce, s->uv[which], uv, px * 2 * sizeof(float), s->stream)) return rc;
+        if (valid)
+            if (int rc = h2d(s->bounce, s->valid[which], valid, px, s->stream)) return rc;
+    } else {
+        SS_CUDA_TRY(cudaMemcpyAsync(s->uv[which], uv, px * 2 * sizeof(float), kind, s->stream));
+        if (valid) SS_CUDA_TRY(cudaMemcpyAsync(s->valid[which], valid, px, kind, s->stream));
+    }
+    if (!valid) SS_CUDA_TRY(cudaMemsetAsync(s->valid[which], 1, px, s->stream));
     s->flow_for[which] = s->solved_through + 1;
     return SS_OK;
 }
@@ -976,17 +1093,23 @@ int ss_output(const ss_session *s, void *dst, int dtype, int where)
     }
     const size_t n = (size_t)s->h * s->w * s->cp;
     const cudaMemcpyKind kind = where == SS_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    if (dtype == SS_F32) {
-        SS_CUDA_TRY(cudaMemcpyAsync(dst, s->O, n * sizeof(float), kind, s->stream));
-    } else if (dtype == SS_U8) {
-        uint8_t *tmp = reinterpret_cast<uint8_t *>(s->O_new);  // scratch between steps
+    const void *src = s->O;
+    size_t bytes = n * sizeof(float);
+    if (dtype == SS_U8) {
+        // O_new is scratch between steps, but an asynchronous output copy
+        // may still be reading it (it held the previous output)
+        if (s->out_pending) SS_CUDA_TRY(cudaStreamWaitEvent(s->stream, s->out_done, 0));
+        uint8_t *tmp = reinterpret_cast<uint8_t *>(s->O_new);
         k_f32_to_u8<<<blocks_for((long)n, 256), 256, 0, s->stream>>>(s->O, (long)n, tmp);
         SS_LAUNCH_CHECK("k_f32_to_u8");
-        SS_CUDA_TRY(cudaMemcpyAsync(dst, tmp, n, kind, s->stream));
-    } else {
+        src = tmp;
+        bytes = n;
+    } else if (dtype != SS_F32) {
         set_error("unsupported dtype");
         return SS_VALUE_ERROR;
     }
+    if (where == SS_HOST) return d2h(s->bounce, dst, src, bytes, s->stream);
+    SS_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, kind, s->stream));
     SS_CUDA_TRY(cudaStreamSynchronize(s->stream));
     return SS_OK;
 }
