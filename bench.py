@@ -75,6 +75,11 @@ def parse():
     ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--streams-total", type=int, default=64,
                     help="configs[4]: concurrent streams over all ranks")
+    ap.add_argument("--stream-workers", type=int, default=4,
+                    help="configs[4]: host threads per rank, each stepping its share of the "
+                         "rank's sessions in turn")
+    ap.add_argument("--only-config", default=None,
+                    help="diagnostics: run just this configs entry (e.g. 4) and print it")
     return ap.parse_args()
 
 
@@ -666,18 +671,21 @@ def run_configs(env, args):
             env, "dis", H, W, "dis", r,
             "1920x1080 single stream with the reference's own flow provider (BuiltinFlow, DIS) on "
             "the GPU: like for like with the reference arm")
-    out["configs[4]"] = run_multi(env, args.streams_total, H, W, "fp32", steps, warm)
+    out["configs[4]"] = run_multi(env, args.streams_total, H, W, "fp32", steps, warm,
+                                  args.stream_workers)
     return out
 
 
 class ThreadedSessions:
     """configs[4] backend for sharding.run_sharded: one session per owned
-    stream, each on its own CUDA stream and driven by its own host thread (the
-    C ABI releases the GIL), so the streams' kernels overlap on the GPU.
-    Device time = earliest start event to latest end event (CUDA events)."""
+    stream, each on its own CUDA stream; ``workers`` host threads (the C ABI
+    releases the GIL) each step their share of the sessions in turn, so a few
+    streams' kernels overlap on the GPU at any time.  Device time = earliest
+    start event to latest end event (CUDA events)."""
 
-    def __init__(self, env, h, w, flow_kind):
+    def __init__(self, env, h, w, flow_kind, workers=4):
         self.env, self.h, self.w, self.flow_kind = env, h, w, flow_kind
+        self.workers = workers
         self.launches, self.clocks = 0, None
 
     def open(self, stream_ids):
@@ -721,18 +729,24 @@ class ThreadedSessions:
     def run_timed(self, steps):
         env, torch, L = self.env, self.env.torch, self.env.L
         S = len(self.ids)
+        T = max(1, min(self.workers, S))
         ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(S)]
         ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(S)]
-        gate = threading.Barrier(S)
+        gate = threading.Barrier(T)
         errors = []
 
-        def worker(s_):
+        def worker(t_):
+            # worker t_ owns sessions t_, t_ + T, ... and steps them in turn
+            mine = list(range(t_, S, T))
             try:
-                with torch.cuda.stream(self.streams[s_]):
-                    gate.wait()
+                gate.wait()
+                for s_ in mine:
                     ev0[s_].record(self.streams[s_])
-                    for _ in range(steps):
-                        self._step(s_)
+                for _ in range(steps):
+                    for s_ in mine:
+                        with torch.cuda.stream(self.streams[s_]):
+                            self._step(s_)
+                for s_ in mine:
                     _check(L.ss_session_join(self.states[s_].handle), L)
                     ev1[s_].record(self.streams[s_])
             except Exception as e:  # noqa: BLE001
@@ -743,7 +757,7 @@ class ThreadedSessions:
         torch.cuda.synchronize()
         sampler = ClockSampler(env.local).start()
         n0 = int(L.ss_kernel_launches())
-        threads = [threading.Thread(target=worker, args=(s_,)) for s_ in range(S)]
+        threads = [threading.Thread(target=worker, args=(t_,)) for t_ in range(T)]
         for t in threads:
             t.start()
         for t in threads:
@@ -760,12 +774,12 @@ class ThreadedSessions:
         self.env.torch.cuda.synchronize()
 
 
-def run_multi(env, n_total, h, w, flow_kind, steps, warmup):
+def run_multi(env, n_total, h, w, flow_kind, steps, warmup, workers=4):
     """configs[4]: ``n_total`` concurrent streams sharded over the ranks
     (sharding.run_sharded: stream i -> rank i mod N, max-over-ranks time)."""
     from paper_2301_00750_b200.sharding import run_sharded
 
-    be = ThreadedSessions(env, h, w, flow_kind)
+    be = ThreadedSessions(env, h, w, flow_kind, workers)
     r = run_sharded(n_total, env.world, env.rank, be, steps, warmup, env.dist, device="cuda")
     S = len(r["streams"])
     return {"workload": f"{n_total} concurrent {w}x{h} streams sharded over {env.world} GPU(s) "
@@ -774,6 +788,7 @@ def run_multi(env, n_total, h, w, flow_kind, steps, warmup):
             "value": round(r["fps"], 3), "unit": "frames/s", "streams_per_gpu": S,
             "per_stream_fps": round(r["per_stream_fps"], 3),
             "ms_per_step": round(r["ms"] / steps, 4),
+            "host_workers_per_gpu": min(workers, S),
             "scaling": "strong (fixed total of streams)", "gpu_launches": be.launches,
             "clocks": be.clocks,
             "timer": "CUDA events per stream: earliest start to latest end, max over ranks"}
@@ -795,6 +810,14 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     env = Env(torch, dist, rank, world, local)
     h, w = args.height, args.width
+    if args.only_config == "4":
+        r = run_multi(env, args.streams_total, h, w, args.flow, max(5, min(args.steps, 10)),
+                      max(3, min(args.warmup, 5)), args.stream_workers)
+        if rank == 0:
+            print(json.dumps(r), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        return
 
     res = run_stream(env, h, w, args.flow, args.steps, args.warmup, e2e=not args.no_e2e,
                      e2e_python=not args.no_e2e)
