@@ -114,7 +114,9 @@ SS_API int ss_solve_screened_poisson(const float *processed, const float *target
 /* ---- built-in DIS flow (estimate_flow, flow.py:168-325) --- */
 /* FlowOptions (flow.py:27-42): levels >= 1, odd patch >= 3, iterations per
  * level, downscale in {1, 2, 4}.  Flow from frame_a toward frame_b ((h, w, c)
- * float32 device pointers) into uv (h, w, 2) / valid (h, w) (may be NULL). */
+ * float32 device pointers) into uv (h, w, 2) / valid (h, w) (may be NULL).
+ * Scratch is per host thread; consecutive calls of one thread on different
+ * streams are ordered (the later call waits for the earlier one's work). */
 SS_API int ss_dis_flow(const float *frame_a, const float *frame_b, int h, int w, int c,
                        int levels, int patch, int iters, int downscale, float *uv,
                        uint8_t *valid, void *stream);
@@ -193,13 +195,16 @@ typedef struct ss_flownet ss_flownet;
 /* Number of float32 parameters the network expects (liteflownet.n_params). */
 SS_API int64_t ss_flownet_num_params(void);
 /* Upload weights (host float32, liteflownet.flatten_weights layout) to the
- * current device.  precision: SS_FLOW_FP32 (CUDA-core FFMA) or SS_FLOW_BF16
- * (tcgen05 tensor cores, bf16 operands, fp32 accumulation). */
+ * current device.  precision: SS_FLOW_FP32 (3xTF32 on tcgen05 tensor cores:
+ * fp32-class accuracy) or SS_FLOW_BF16 (tcgen05, bf16 operands, fp32
+ * accumulation). */
 enum ss_flow_precision { SS_FLOW_FP32 = 0, SS_FLOW_BF16 = 1 };
 SS_API int ss_flownet_create(const float *weights, int64_t n, int precision, ss_flownet **out);
 SS_API int ss_flownet_destroy(ss_flownet *net);
 /* Stateless: flow from frame_a toward frame_b ((h, w, c) HWC float32 device
- * pointers) into uv (h, w, 2) and valid (h, w) (may be NULL); stream-ordered. */
+ * pointers) into uv (h, w, 2) and valid (h, w) (may be NULL); stream-ordered.
+ * Thread-safe: calls share one scratch set per frame size, serialised by a
+ * mutex; a call on another stream waits for the previous user's work. */
 SS_API int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b, int h,
                            int w, int c, float *uv, uint8_t *valid, void *stream);
 /* Attach the network to a session: it computes the step's flows itself,

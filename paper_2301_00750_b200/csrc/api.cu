@@ -1177,12 +1177,9 @@ int ss_flows(const ss_session *s, int which, float *uv_dst, uint8_t *valid_dst, 
 }
 
 // ---- lite flow network ----------------------------------------------------------
-// fp32 -> 3xTF32 on tcgen05 (fp32-class accuracy); bf16 -> bf16 tcgen05;
-// SS_FLOW_CONV=ffma forces the CUDA-core FFMA implicit GEMM (cross-check)
+// fp32 -> 3xTF32 on tcgen05 (fp32-class accuracy); bf16 -> bf16 tcgen05
 static int conv_mode_for(int precision)
 {
-    const char *e = getenv("SS_FLOW_CONV");
-    if (e && !strcmp(e, "ffma")) return fn::CONV_FFMA;
     return precision == SS_FLOW_BF16 ? fn::CONV_TC_BF16 : fn::CONV_TC_TF32X3;
 }
 
@@ -1271,8 +1268,7 @@ int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
             SS_CUDA_TRY(cudaEventCreateWithFlags(&s->hjoin, cudaEventDisableTiming));
         }
     }
-    if (int rc = fn::prepare_conv_tma()) return rc;
-    return fn::prepare_conv_tc();
+    return fn::prepare_conv_tma();
 }
 
 int ss_session_compute_dis_flow(ss_session *s, int which, int levels, int patch, int iters,

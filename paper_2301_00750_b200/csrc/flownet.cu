@@ -63,7 +63,6 @@ static std::vector<LayerDev> table()
 Weights::~Weights()
 {
     cudaFree(block);
-    cudaFree(tc_block);
     cudaFree(tma_block);
     cudaFree(bf_block);
 }
@@ -122,59 +121,6 @@ int Weights::upload(const float *host, int64_t n)
     for (size_t i = 0; i < layers.size(); ++i) {
         layers[i].w = block + woff[i];
         layers[i].b = block + boff[i];
-    }
-
-    // tensor-core weight stages (flownet_tc.cu): per K stage, N = cout_pad rows
-    // of 128 bytes of K in the core-matrix layout
-    //   byte(n, kb) = (n / 8) * 1024 + (kb / 16) * 128 + (n % 8) * 16 + kb % 16
-    // bf16: 64 K per stage; 3xTF32: 32 K per stage, (hi, lo) blocks
-    auto core_off = [](int n, int kb) {
-        return (size_t)(n / 8) * 1024 + (size_t)(kb / 16) * 128 + (size_t)(n % 8) * 16 + kb % 16;
-    };
-    std::vector<size_t> obf(layers.size(), 0), otf(layers.size(), 0);
-    size_t tc_total = 0;
-    for (size_t i = 0; i < layers.size(); ++i) {
-        auto &l = layers[i];
-        if (l.dw) continue;
-        const int K = l.k * l.k * l.cin, N = l.cout_pad;
-        obf[i] = tc_total;
-        tc_total += (size_t)((K + 63) / 64) * N * 128;
-        otf[i] = tc_total;
-        tc_total += (size_t)((K + 31) / 32) * 2 * N * 128;
-    }
-    std::vector<uint8_t> tch(tc_total, 0);
-    for (size_t i = 0; i < layers.size(); ++i) {
-        auto &l = layers[i];
-        if (l.dw) continue;
-        const int K = l.k * l.k * l.cin, N = l.cout_pad;
-        const float *wl = dev.data() + woff[i];  // [K][cout_pad]
-        for (int k = 0; k < K; ++k) {
-            for (int n = 0; n < l.cout; ++n) {
-                const float f = wl[(size_t)k * N + n];
-                uint32_t u;
-                std::memcpy(&u, &f, 4);
-                // bf16, round to nearest even
-                const uint16_t bf = (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
-                std::memcpy(&tch[obf[i] + (size_t)(k / 64) * N * 128 + core_off(n, (k % 64) * 2)], &bf, 2);
-                // tf32 hi (truncated) / lo (exact remainder)
-                const uint32_t hu = u & 0xffffe000u;
-                float hi, lo;
-                std::memcpy(&hi, &hu, 4);
-                lo = f - hi;
-                const size_t st = otf[i] + (size_t)(k / 32) * 2 * N * 128;
-                std::memcpy(&tch[st + core_off(n, (k % 32) * 4)], &hi, 4);
-                std::memcpy(&tch[st + (size_t)N * 128 + core_off(n, (k % 32) * 4)], &lo, 4);
-            }
-        }
-    }
-    cudaFree(tc_block);
-    tc_block = nullptr;
-    SS_CUDA_TRY(cudaMalloc(&tc_block, tc_total));
-    SS_CUDA_TRY(cudaMemcpy(tc_block, tch.data(), tc_total, cudaMemcpyHostToDevice));
-    for (size_t i = 0; i < layers.size(); ++i) {
-        if (layers[i].dw) continue;
-        layers[i].tc_bf16 = static_cast<uint8_t *>(tc_block) + obf[i];
-        layers[i].tc_tf32 = static_cast<uint8_t *>(tc_block) + otf[i];
     }
 
     // TMA path (flownet_tma.cu): per layer [kblocks][parts][2 np][32] fp32 --
@@ -364,9 +310,6 @@ static int side_grid_cap()
 }
 static thread_local float *ws_ = nullptr;
 static thread_local size_t ws_floats_ = 0;
-// SS_CONV_TMA=0: the fp32 path uses the register-gather tcgen05 kernel
-// (flownet_tc.cu) instead of the TMA-fed one (A/B comparison)
-static const bool use_tma_ = getenv("SS_CONV_TMA") == nullptr || strcmp(getenv("SS_CONV_TMA"), "0");
 
 // SS_FLOW_PROFILE=1: per-launch device times of the network (CUDA events),
 // printed to stderr after every pyramid / flow call (diagnostics only)
@@ -416,7 +359,6 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
                 int out_ld, cudaStream_t st)
 {
     ConvParams p;
-    p.wtc = conv_mode_ == CONV_TC_BF16 ? L.tc_bf16 : L.tc_tf32;
     p.ws = ws_;
     p.ws_floats = ws_floats_;
     p.in = in;
@@ -441,9 +383,7 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
     p.tmB = bf ? &L.tmB_bf : &L.tmB;
     p.grid_cap = grid_cap_;
     p.tma_T = bf ? L.tma_T_bf : L.tma_T;
-    if (conv_mode_ == CONV_FFMA) return launch_conv_ffma(p, st);
-    if (use_tma_) return launch_conv_tma(p, bf ? 0 : 1, st);
-    return launch_conv_tc(p, conv_mode_ == CONV_TC_BF16 ? 0 : 1, st);
+    return launch_conv_tma(p, bf ? 0 : 1, st);
 }
 
 // capture fn(st) into a graph (thread-local capture mode) and instantiate it

@@ -53,7 +53,6 @@ struct ConvParams {
     float *out;
     int out_ld, Ho, Wo;
     int k, stride, dil, pad, act;
-    const void *wtc;            // tensor-core weight stages (flownet_tc.cu layout)
     float *ws = nullptr;        // split-K workspace (tensor-core path), may be null
     size_t ws_floats = 0;
     int k_per_split = 0;        // set by the launcher
@@ -63,12 +62,9 @@ struct ConvParams {
     int tma_T = 1;              // taps per weight stage of that map
 };
 
-enum ConvMode { CONV_FFMA = 0, CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
+enum ConvMode { CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
 
-int launch_conv_ffma(const ConvParams &p, cudaStream_t st);
 // kind 0: bf16 operands (kind::f16); kind 1: 3xTF32 (kind::tf32)
-int launch_conv_tc(const ConvParams &p, int kind, cudaStream_t st);
-int prepare_conv_tc();  // one-time kernel attributes (call outside stream capture)
 // TMA-fed warp-specialised 3xTF32 conv (flownet_tma.cu)
 int launch_conv_tma(const ConvParams &p, int prec, cudaStream_t st);  // prec: 1 3xTF32, 0 bf16
 int prepare_conv_tma();
@@ -94,7 +90,6 @@ struct LayerDev {
     int cin, cout, cout_pad, k, stride, dil, act;
     bool dw;
     float *w = nullptr, *b = nullptr;
-    const void *tc_bf16 = nullptr, *tc_tf32 = nullptr;  // tensor-core stage layouts
     // TMA path (flownet_tma.cu): [kblock = cb * k*k + tap][part][hi np rows;
     // lo np rows][32 channels] fp32, its tensor map, taps per stage
     const float *wt_tma = nullptr;
@@ -110,7 +105,6 @@ struct LayerDev {
 struct Weights {
     std::vector<LayerDev> layers;
     float *block = nullptr;
-    void *tc_block = nullptr;
     float *tma_block = nullptr;
     void *bf_block = nullptr;
     ~Weights();

@@ -42,149 +42,6 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // ---------------------------------------------------------------------------
-// Implicit-GEMM convolution on CUDA cores (FFMA), fp32.
-//   M = Ho*Wo output pixels (tile BM = 128), N = Cout (tile BN), K = k*k*Cin
-//   (tile BK = 16, float4 groups never straddle a tap because Cin % 4 == 0).
-// Thread tile 8 pixels x 4 output channels; A staged [m][k] so one LDS.128
-// yields 4 k-values of a pixel, B staged [k][n].  cp.async double buffering
-// with zero-fill for padding / tails.
-constexpr int BM = 128, BK = 16, AS = BK + 4;
-
-template <int BN>
-__global__ void __launch_bounds__(16 * (BN / 4)) k_conv_ffma(ConvParams p)
-{
-    pdl_wait();
-    constexpr int NT = BN / 4;       // channel groups
-    constexpr int THREADS = 16 * NT; // 16 pixel groups
-    __shared__ __align__(16) float As[2][BM][AS];
-    __shared__ __align__(16) float Bs[2][BK][BN];
-    const int tid = threadIdx.x;
-    const int tm = tid % 16, tn = tid / 16;
-    const int M = p.Ho * p.Wo;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-    const int Ktot = p.k * p.k * p.Cin;
-    const int nk = (Ktot + BK - 1) / BK;
-
-    // A slots of this thread: BM*BK/4 float4 = 512 per stage
-    constexpr int A_SLOTS = (BM * BK / 4) / THREADS;
-    int a_m[A_SLOTS], a_oy[A_SLOTS], a_ox[A_SLOTS], a_kq[A_SLOTS];
-#pragma unroll
-    for (int s = 0; s < A_SLOTS; ++s) {
-        const int f = tid + s * THREADS;
-        a_m[s] = f >> 2;
-        a_kq[s] = f & 3;
-        const int pix = m0 + a_m[s];
-        a_oy[s] = pix < M ? pix / p.Wo : -100000;
-        a_ox[s] = pix < M ? pix - (pix / p.Wo) * p.Wo : 0;
-    }
-    // B slots: BK*BN/4 float4
-    constexpr int B_SLOTS = (BK * BN / 4 + THREADS - 1) / THREADS;
-
-    auto load_stage = [&](int st, int kt) {
-        const int k0 = kt * BK;
-#pragma unroll
-        for (int s = 0; s < A_SLOTS; ++s) {
-            const int k = k0 + a_kq[s] * 4;
-            const int tap = k / p.Cin, ci = k - tap * p.Cin;
-            const int ky = tap / p.k, kx = tap - ky * p.k;
-            const int iy = a_oy[s] * p.stride + ky * p.dil - p.pad;
-            const int ix = a_ox[s] * p.stride + kx * p.dil - p.pad;
-            const bool ok = k < Ktot && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W;
-            const float *src = ok ? p.in + ((long)iy * p.W + ix) * p.in_ld + ci : p.in;
-            cp_async16(&As[st][a_m[s]][a_kq[s] * 4], src, ok);
-        }
-#pragma unroll
-        for (int s = 0; s < B_SLOTS; ++s) {
-            const int f = tid + s * THREADS;
-            if (f < BK * BN / 4) {
-                const int kr = f / (BN / 4), nc = (f - kr * (BN / 4)) * 4;
-                const int k = k0 + kr, n = n0 + nc;
-                const bool ok = k < Ktot && n < p.Cout_pad;
-                const float *src = ok ? p.wgt + (long)k * p.Cout_pad + n : p.wgt;
-                cp_async16(&Bs[st][kr][nc], src, ok);
-            }
-        }
-        cp_async_commit();
-    };
-
-    float acc[8][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-
-    load_stage(0, 0);
-    for (int kt = 0; kt < nk; ++kt) {
-        const int st = kt & 1;
-        if (kt + 1 < nk) {
-            load_stage(st ^ 1, kt + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            float4 a[8], b[4];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(&As[st][i * 16 + tm][kk]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const float4 *>(&Bs[st][kk + j][tn * 4]);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float av[4] = {a[i].x, a[i].y, a[i].z, a[i].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    acc[i][0] = fmaf(av[j], b[j].x, acc[i][0]);
-                    acc[i][1] = fmaf(av[j], b[j].y, acc[i][1]);
-                    acc[i][2] = fmaf(av[j], b[j].z, acc[i][2]);
-                    acc[i][3] = fmaf(av[j], b[j].w, acc[i][3]);
-                }
-            }
-        }
-        __syncthreads();
-    }
-
-    const int n = n0 + tn * 4;
-    if (n >= p.Cout) return;
-    float bias[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) bias[j] = n + j < p.Cout ? p.bias[n + j] : 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int pix = m0 + i * 16 + tm;
-        if (pix >= M) continue;
-        float v[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            v[j] = acc[i][j] + bias[j];
-            if (p.act) v[j] = leaky(v[j]);
-        }
-        float *dst = p.out + (long)pix * p.out_ld + n;
-        if (n + 4 <= p.Cout) {
-            *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-        } else {
-            for (int j = 0; j < p.Cout - n; ++j) dst[j] = v[j];
-        }
-    }
-}
-
-int launch_conv_ffma(const ConvParams &p, cudaStream_t st)
-{
-    const int M = p.Ho * p.Wo;
-    const int gx = (M + BM - 1) / BM;
-    if (p.Cout > 32) {
-        k_conv_ffma<64><<<dim3(gx, (p.Cout + 63) / 64), 256, 0, st>>>(p);
-    } else if (p.Cout > 16) {
-        k_conv_ffma<32><<<dim3(gx, 1), 128, 0, st>>>(p);
-    } else {
-        k_conv_ffma<16><<<dim3(gx, 1), 64, 0, st>>>(p);
-    }
-    SS_LAUNCH_CHECK("k_conv_ffma");
-    return SS_OK;
-}
-
-// ---------------------------------------------------------------------------
 // depthwise 3x3 (dilated), NHWC, zero padding, no bias / activation.
 // A thread owns 4 channels x DW_PX horizontally adjacent pixels: its 9 weight
 // float4 stay in registers, and all 9 x DW_PX input loads of a row are issued
@@ -661,6 +518,69 @@ int launch_flow_final(const float *f3, int ld3, const float *r, int ldr, int Hc,
 {
     return launch_pdl("k_flow_final", k_flow_final, dim3(blocks_for((long)h * w, 256)), dim3(256), 0, st, f3, ld3,
                       r, ldr, Hc, Wc, h, w, uv, valid);
+}
+
+// ---------------------------------------------------------------------------
+// split-K reduction of the conv kernels' partial sums (flownet_tma.cu)
+
+// out[m, n] = act(sum_s ws[s, m, n] + bias[n])
+// ws: [part][split][M][N]; output channel c of part c / N (N % 4 == 0, so a
+// float4 group never straddles parts)
+__global__ void k_splitk_reduce(const float *__restrict__ ws, int splits, int M, int N, int Cout,
+                                const float *__restrict__ bias, int act, float *__restrict__ out,
+                                int out_ld)
+{
+    pdl_wait();
+    const int n4 = (Cout + 3) / 4;
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)M * n4) return;
+    const int m = (int)(i / n4), n = (int)(i - (long)m * n4) * 4;
+    const int part = n / N, nn = n - part * N;
+    // partials are added in split order; their loads are issued eight at a
+    // time (a serial load -> add chain would pay one L2 round trip per split)
+    const float *src = ws + ((size_t)part * splits * M + m) * N + nn;
+    const size_t stride = (size_t)M * N;
+    float4 acc = *reinterpret_cast<const float4 *>(src);
+    int s = 1;
+    for (; s + 8 <= splits; s += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldcg(reinterpret_cast<const float4 *>(src + (s + j) * stride));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            acc.x += v[j].x;
+            acc.y += v[j].y;
+            acc.z += v[j].z;
+            acc.w += v[j].w;
+        }
+    }
+    for (; s < splits; ++s) {
+        const float4 v = __ldcg(reinterpret_cast<const float4 *>(src + s * stride));
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+    }
+    float r[4] = {acc.x, acc.y, acc.z, acc.w};
+    float *dst = out + (long)m * out_ld + n;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (n + j >= Cout) break;
+        const float x = r[j] + bias[n + j];
+        dst[j] = act ? leaky(x) : x;
+    }
+}
+
+int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,
+                         int act, float *out, int out_ld, cudaStream_t st, int parts)
+{
+    if (parts > 1 && N % 4 != 0) {
+        set_error("split-K reduce: part width must be a multiple of 4");
+        return SS_VALUE_ERROR;
+    }
+    const long n = (long)M * ((Cout + 3) / 4);
+    return launch_pdl("k_splitk_reduce", k_splitk_reduce, dim3(blocks_for(n, 128)), dim3(128), 0, st, ws, splits,
+                      M, N, Cout, bias, act, out, out_ld);
 }
 
 }  // namespace fn

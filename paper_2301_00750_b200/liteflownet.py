@@ -170,7 +170,8 @@ class LiteFlowNet:
     straight into the session's HBM flow slots and caches each ring frame's
     feature pyramid, so a step computes one new pyramid and two estimator
     passes.  ``flow_between`` is the stateless form (FlowField out).
-    precision: "fp32" (CUDA-core FFMA) or "bf16" (tcgen05 tensor cores).
+    precision: "fp32" (3xTF32 on tcgen05: fp32-class accuracy) or "bf16"
+    (bf16 operands on tcgen05, fp32 accumulation).
     """
 
     def __init__(self, weights: dict | None = None, seed: int = 0, precision: str = "fp32"):

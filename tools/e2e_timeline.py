@@ -1,4 +1,4 @@
-"""Host-side timeline of the e2e loop (bench.run_e2e order): wall time spent in
+"""Host-side timeline of the e2e loop (bench.run_e2e_abi order): wall time spent in
 each C-ABI call per step, to locate host blocking.  Usage: e2e_timeline.py fp32"""
 import ctypes, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

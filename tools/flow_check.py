@@ -1,4 +1,4 @@
-"""Diagnostics: lite flow net GPU paths (3xTF32 / bf16 tcgen05, FFMA) vs the CPU
+"""Diagnostics: lite flow net GPU paths (3xTF32 and bf16 tcgen05) vs the CPU
 restatement, and 1080p flow timing.  Usage: python tools/flow_check.py"""
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
