@@ -21,9 +21,11 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -876,6 +878,419 @@ static int launch_v2(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
     return fn::launch_pdl("k_sgd_v2", k_sgd_v2<RB>, dim3(grid), dim3(32, C::NW), C::SMEM, st, maps, a);
 }
 
+// ---------------------------------------------------------------------------
+// v3: v2<8> on CTA pairs (round 2).  A 2-CTA thread-block cluster stacks two
+// 128 x 64 regions into one 128 x 128 region with a single 8-pixel apron, so
+// the apron recompute drops from 128*64 / (112*48) = 1.52x to
+// 128*128 / (112*112) = 1.31x and a 1080p pass is 8 rounds of tiles per SM
+// instead of 9.  The two strips that meet at the seam (rank 0's bottom warp,
+// rank 1's top warp) exchange their edge rows every iteration through
+// distributed shared memory: st.async of the new row straight into the
+// partner's receive slot, completing bytes on the partner's mbarrier -- a
+// point-to-point handshake between two warps, not a cluster barrier.  The
+// edge warp computes the pair that holds its seam row first and sends it
+// before the rest of its block, so the partner's next-iteration wait is
+// normally already satisfied.  Ordering argument (no reverse handshake
+// needed): row n lands in receive slot n & 1 and barrier n & 1; the sender
+// writes row n only after it has received the partner's row n - 1, which
+// the partner sends after reading row n - 2 out of that slot (the seam row is
+// read only by the pair computed before the send).  The receiver re-arms
+// barrier n & 1 for row n + 2 right after its wait for row n completes,
+// before its own send that the partner needs to produce row n + 2.
+//
+// Measured at 1080p (B200, 150 iterations): 1.166 ms against v2's 1.066 ms,
+// bit-identical.  The seam handshake itself is cheap (its waits almost never
+// spin; without the exchange, numerically wrong, 1.09 ms), but per tile the
+// kernel runs ~15% slower than v2 (ncu: more fixed-latency "wait" and CTA
+// barrier stalls at 248 registers, plus the cluster barriers at entry / exit),
+// which eats the 9 -> 8 rounds.  Kept selectable (SS_SOLVER=v3, bitwise
+// tested); v2 stays the default.
+namespace v3 {
+constexpr int K = 8, RB = 8, NP = 4, NW = 8, THREADS = 256;
+constexpr int RW = 128, RH = 64;            // one CTA's region
+constexpr int OW = RW - 2 * K;              // 112 interior columns
+constexpr int OH = 2 * RH - 2 * K;          // 112 interior rows per pair
+constexpr int STAGE = RW * RH;
+constexpr int SLOT = 2 * 4 * 32;
+constexpr int PAR = (NW + 3) * SLOT;
+constexpr uint32_t ROW_BYTES = RW * sizeof(float);
+constexpr size_t SMEM = (5ull * STAGE + 2ull * PAR + 2ull * RW) * sizeof(float) + 32;
+}  // namespace v3
+
+__device__ __forceinline__ uint32_t cl_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_id()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_count()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t saddr, uint32_t rank)
+{
+    uint32_t d;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
+    return d;
+}
+__device__ __forceinline__ void cl_sync()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// CTA barrier reached from different code paths (the two loop copies below):
+// the non-.aligned form, which only counts arriving threads
+__device__ __forceinline__ void bar_sync_na() { asm volatile("barrier.sync 0;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arm_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// wait for a phase whose bytes were written by the partner CTA
+__device__ __forceinline__ void mbar_wait_cl(uint64_t *bar, uint32_t phase)
+{
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void st_async_row(uint32_t raddr, float x, float y, float z, float w, uint32_t rbar)
+{
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(raddr), "f"(x), "f"(y), "f"(z), "f"(w), "r"(rbar)
+                 : "memory");
+}
+
+// one iteration of the seam warp: v2_iter<8> with the seam row exchanged with
+// the partner (the other warps run v2_iter<8> itself).  Rank 0 is the upper
+// CTA (its bottom warp receives S / sends its row 7), rank 1 the lower one (its
+// top warp receives N / sends its row 0).  The two pairs that hold a strip's
+// edge rows (0 and NP - 1) go first, then the seam row is sent, then the middle
+// pairs.  (A per-rank template copy of the whole body overflowed the
+// instruction cache: 76 us per pass against 62.)
+template <bool XEDGE>
+__device__ __forceinline__ void v3_iter(const u64 (&X)[4][v3::NP], u64 (&Y)[4][v3::NP],
+                                        const u64 (&Av)[4][v3::NP], const u64 (&Lv)[4][v3::NP],
+                                        const u64 (&Wv)[4][v3::NP], const float *rd, float *wr, int n_off,
+                                        int s_off, int t_off, int b_off, bool lft, bool rgt, const V2Consts &k,
+                                        bool track, float &mx, bool xremote, bool upper,
+                                        const float *recv, uint64_t *xbar, uint32_t n, uint32_t r_recv,
+                                        uint32_t r_bar, bool send)
+{
+    constexpr int NP = v3::NP;
+    u64 wv[NP], ev[NP];
+#pragma unroll
+    for (int r = 0; r < NP; ++r) {
+        wv[r] = pk(__shfl_up_sync(0xffffffffu, lo32(X[3][r]), 1), __shfl_up_sync(0xffffffffu, hi32(X[3][r]), 1));
+        ev[r] = pk(__shfl_down_sync(0xffffffffu, lo32(X[0][r]), 1),
+                   __shfl_down_sync(0xffffffffu, hi32(X[0][r]), 1));
+        wv[r] = lft ? X[0][r] : wv[r];
+        ev[r] = rgt ? X[3][r] : ev[r];
+    }
+    float nr[4], sr[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        nr[j] = rd[n_off + j * 32];
+        sr[j] = rd[s_off + j * 32];
+    }
+    if (XEDGE) {
+        mbar_wait_cl(&xbar[n & 1], (n >> 1) & 1);
+        if ((threadIdx.x & 31) == 0) mbar_arm_tx(&xbar[n & 1], v3::ROW_BYTES);  // row n + 2
+        if (xremote) {
+            const float4 v = *reinterpret_cast<const float4 *>(recv + (n & 1) * v3::RW + 4 * (threadIdx.x & 31));
+            if (upper) {
+                sr[0] = v.x; sr[1] = v.y; sr[2] = v.z; sr[3] = v.w;
+            } else {
+                nr[0] = v.x; nr[1] = v.y; nr[2] = v.z; nr[3] = v.w;
+            }
+        }
+    }
+    auto upd = [&](int j, int r) {
+        const u64 Nn = r == 0 ? pk(nr[j], lo32(X[j][NP - 1])) : X[j][r - 1];
+        const u64 Sn = r == NP - 1 ? pk(hi32(X[j][0]), sr[j]) : X[j][r + 1];
+        const u64 Wn = j == 0 ? wv[r] : X[j - 1][r];
+        const u64 En = j == 3 ? ev[r] : X[j + 1][r];
+        const u64 u = sgd_u64(X[j][r], Y[j][r], Nn, Sn, Wn, En, Lv[j][r], Av[j][r], Wv[j][r], k.eta, k.kap, k.m4,
+                              k.z);
+        Y[j][r] = u;
+        if (track) mx = fmaxf(mx, fmaxf(fabsf(lo32(u)), fabsf(hi32(u))));
+    };
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        upd(j, 0);
+        upd(j, NP - 1);
+    }
+    if (XEDGE && send) {
+        const uint32_t s = (n + 1) & 1;
+        float e[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) e[j] = upper ? hi32(Y[j][NP - 1]) : lo32(Y[j][0]);
+        st_async_row(r_recv + s * v3::ROW_BYTES + 16 * (threadIdx.x & 31), e[0], e[1], e[2], e[3], r_bar + 8 * s);
+    }
+#pragma unroll
+    for (int r = 1; r < NP - 1; ++r)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) upd(j, r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        wr[t_off + j * 32] = lo32(Y[j][0]);
+        wr[b_off + j * 32] = hi32(Y[j][NP - 1]);
+    }
+}
+
+__device__ __forceinline__ void v3_body(const TmaMaps &maps, const BlockedArgs &a, float *stage, float *rows,
+                                        float *recv, uint64_t *bar, uint64_t *xbar)
+{
+    using namespace v3;
+    const int lane = threadIdx.x, wp = threadIdx.y;
+    const int tid = wp * 32 + lane;
+    const int ntx = (a.w + OW - 1) / OW, nty = (a.h + OH - 1) / OH;
+    const int ntiles = ntx * nty * a.c;
+    const int cid = (int)cl_id(), ncl = (int)cl_count();
+    const int rank = (int)cl_rank();
+    const bool upper = rank == 0;
+    constexpr uint32_t TX_BYTES = 5u * STAGE * sizeof(float);
+    auto coords = [&](int t, int &ch, int &x, int &y) {
+        ch = t / (ntx * nty);
+        const int rem = t - ch * ntx * nty;
+        const int ty = rem / ntx, tx = rem - ty * ntx;
+        x = tx * OW - K;
+        y = ty * OH - K + rank * RH;
+    };
+    auto issue = [&](int t) {
+        int ch, x, y;
+        coords(t, ch, x, y);
+        mbar_arm_tx(bar, TX_BYTES);
+        tma_load_3d(stage + 0 * STAGE, &maps.O, x, y, ch, bar);
+        tma_load_3d(stage + 1 * STAGE, &maps.Op, x, y, ch, bar);
+        tma_load_3d(stage + 2 * STAGE, &maps.A, x, y, ch, bar);
+        tma_load_3d(stage + 3 * STAGE, &maps.L, x, y, ch, bar);
+        tma_load_2d(stage + 4 * STAGE, &maps.W, x, y, bar);
+    };
+    if (tid == 0 && cid < ntiles) {
+        int ch, x, y;
+        coords(cid, ch, x, y);
+        mbar_arm_tx(bar, TX_BYTES);
+        tma_load_3d(stage + 2 * STAGE, &maps.A, x, y, ch, bar);
+        tma_load_3d(stage + 3 * STAGE, &maps.L, x, y, ch, bar);
+        tma_load_2d(stage + 4 * STAGE, &maps.W, x, y, bar);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        tma_load_3d(stage + 0 * STAGE, &maps.O, x, y, ch, bar);
+        tma_load_3d(stage + 1 * STAGE, &maps.Op, x, y, ch, bar);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // barriers initialised and armed in both CTAs before any remote access
+    cl_sync();
+
+    V2Consts kc;
+    kc.eta = pk(a.eta, a.eta);
+    kc.kap = pk(a.kappa, a.kappa);
+    kc.m4 = pk(-4.0f, -4.0f);
+    kc.z = pk(a.negzero, a.negzero);
+    const bool interior = lane >= K / 4 && lane < 32 - K / 4 && (rank ? wp < NW - K / RB : wp >= K / RB);
+    const bool xedge = wp == (rank ? 0 : NW - 1);
+    const uint32_t r_recv = cl_mapa(smem_u32(recv), rank ^ 1), r_bar = cl_mapa(smem_u32(xbar), rank ^ 1);
+    uint32_t phase = 0, xn = 0;
+    unsigned bits_all = 0;
+    for (int t = cid; t < ntiles; t += ncl) {
+        int ch, rx0, ry0;
+        coords(t, ch, rx0, ry0);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        u64 X[4][NP], Y[4][NP], Av[4][NP], Lv[4][NP], Wv[4][NP];
+        {
+            auto ld = [&](int arr, u64 (&D)[4][NP]) {
+#pragma unroll
+                for (int r = 0; r < NP; ++r) {
+                    const float *plo = stage + arr * STAGE + (RB * wp + r) * RW + 4 * lane;
+                    const float4 lo = *reinterpret_cast<const float4 *>(plo);
+                    const float4 hi = *reinterpret_cast<const float4 *>(plo + NP * RW);
+                    D[0][r] = pk_reg(lo.x, hi.x, kc.z);
+                    D[1][r] = pk_reg(lo.y, hi.y, kc.z);
+                    D[2][r] = pk_reg(lo.z, hi.z, kc.z);
+                    D[3][r] = pk_reg(lo.w, hi.w, kc.z);
+                }
+            };
+            ld(0, X);
+            ld(1, Y);
+            ld(2, Av);
+            ld(3, Lv);
+            ld(4, Wv);
+        }
+        const int gx0 = rx0 + 4 * lane, gy0 = ry0 + RB * wp;
+        const bool lft = gx0 == 0, rgt = gx0 + 4 == a.w;
+        const bool inside = gx0 >= 0 && gx0 < a.w && gy0 >= 0 && gy0 < a.h;
+        const bool track = interior && inside;
+        // the seam warp reads the partner's row unless an image edge sits on
+        // the seam (then the replicate ghost written locally is the neighbour)
+        const bool xremote = rank ? gy0 != 0 : gy0 + RB != a.h;
+        const int sink = (NW + 2) * SLOT + lane;
+        const int n_off = wp * SLOT + 128 + lane, s_off = (wp + 2) * SLOT + lane;
+        const int t_off = gy0 == 0 ? wp * SLOT + 128 + lane : gy0 == a.h ? sink : (wp + 1) * SLOT + lane;
+        const int b_off = gy0 + RB == a.h ? (wp + 2) * SLOT + lane
+                          : gy0 + RB == 0  ? sink : (wp + 1) * SLOT + 128 + lane;
+        float *rb0 = rows, *rb1 = rows + PAR;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            rb0[t_off + j * 32] = lo32(X[j][0]);
+            rb0[b_off + j * 32] = hi32(X[j][NP - 1]);
+        }
+        // the seam row of iterate 0 goes to the partner
+        if (xedge) {
+            const uint32_t s = xn & 1;
+            float e[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) e[j] = upper ? hi32(X[j][NP - 1]) : lo32(X[j][0]);
+            st_async_row(r_recv + s * ROW_BYTES + 16 * lane, e[0], e[1], e[2], e[3], r_bar + 8 * s);
+        }
+        __syncthreads();  // stage consumed, rows published
+        if (tid == 0 && t + ncl < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(t + ncl);
+        }
+        float mx = 0.0f;
+        // two copies of the iteration loop: the seam warp's, and the other
+        // warps' with no seam code at all (a warp-uniform branch inside one
+        // loop cost ~25% per iteration: reconvergence barriers and a worse
+        // register schedule)
+        auto run = [&](auto xe) {
+            constexpr bool XE = decltype(xe)::value;
+            for (int it = 0; it < a.iters; it += 2) {
+                if (XE)
+                    v3_iter<true>(X, Y, Av, Lv, Wv, rb0, rb1, n_off, s_off, t_off, b_off, lft, rgt, kc, track, mx,
+                                  xremote, upper, recv, xbar, xn + it, r_recv, r_bar, it + 1 < a.iters);
+                else
+                    v2_iter<8>(X, Y, Av, Lv, Wv, rb0, rb1, n_off, s_off, t_off, b_off, lft, rgt, kc, track, mx);
+                bar_sync_na();
+                if (it + 1 < a.iters) {
+                    if (XE)
+                        v3_iter<true>(Y, X, Av, Lv, Wv, rb1, rb0, n_off, s_off, t_off, b_off, lft, rgt, kc, track,
+                                      mx, xremote, upper, recv, xbar, xn + it + 1, r_recv, r_bar, it + 2 < a.iters);
+                    else
+                        v2_iter<8>(Y, X, Av, Lv, Wv, rb1, rb0, n_off, s_off, t_off, b_off, lft, rgt, kc, track, mx);
+                    bar_sync_na();
+                }
+            }
+        };
+        if (xedge)
+            run(std::true_type{});
+        else
+            run(std::false_type{});
+        xn += (uint32_t)a.iters;
+        const bool odd = a.iters & 1;
+        bool nan_seen = false;
+        if (interior && inside) {
+            const long plane = (long)ch * a.h * a.w;
+#pragma unroll
+            for (int rr = 0; rr < RB; ++rr) {
+                const int q = rr % NP;
+                float o[4], op[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const u64 cur = odd ? Y[j][q] : X[j][q];
+                    const u64 prv = odd ? X[j][q] : Y[j][q];
+                    o[j] = rr < NP ? lo32(cur) : hi32(cur);
+                    op[j] = rr < NP ? lo32(prv) : hi32(prv);
+                    nan_seen |= o[j] != o[j];
+                }
+                const long qi = (long)(gy0 + rr) * a.w + gx0;
+                if (a.hwc_out) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) a.hwc_out[(qi + j) * a.c + ch] = fminf(fmaxf(o[j], 0.0f), 1.0f);
+                } else {
+                    *reinterpret_cast<float4 *>(a.Oout + plane + qi) = make_float4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<float4 *>(a.Oprev_out + plane + qi) = make_float4(op[0], op[1], op[2], op[3]);
+                }
+            }
+        }
+        bits_all = max(bits_all, nan_seen ? 0x7fffffffu : __float_as_uint(mx));
+    }
+    push_maxbits(bits_all, a.maxbits);
+}
+
+__global__ void __launch_bounds__(v3::THREADS, 1) k_sgd_v3(const __grid_constant__ TmaMaps maps, BlockedArgs a)
+{
+    using namespace v3;
+    extern __shared__ __align__(1024) float smem_v3[];
+    float *stage = smem_v3;
+    float *rows = stage + 5 * STAGE;
+    float *recv = rows + 2 * PAR;  // [2][RW]: the partner's seam rows
+    uint64_t *bar = reinterpret_cast<uint64_t *>(recv + 2 * RW);
+    uint64_t *xbar = bar + 1;      // [2]: seam-row arrivals
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int i = tid; i < 2 * PAR + 2 * RW; i += THREADS) rows[i] = 0.0f;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(xbar)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(xbar + 1)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_arm_tx(xbar, ROW_BYTES);      // rows 0 and 1
+        mbar_arm_tx(xbar + 1, ROW_BYTES);
+    }
+    __syncthreads();
+    v3_body(maps, a, stage, rows, recv, bar, xbar);
+    // no CTA leaves while its partner may still address its shared memory
+    cl_sync();
+}
+
+static int launch_v3(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
+{
+    static int max_clusters = 0;
+    if (!max_clusters) {
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3::SMEM));
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_v3, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2);
+        cfg.blockDim = dim3(32, v3::NW);
+        cfg.dynamicSmemBytes = v3::SMEM;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SS_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, k_sgd_v3, &cfg));
+        if (max_clusters < 1) {
+            set_error("k_sgd_v3: no 2-CTA cluster fits");
+            return SS_CUDA_ERROR;
+        }
+        if (getenv("SS_SOLVER_DEBUG")) fprintf(stderr, "[solver] k_sgd_v3: %d co-resident CTA pairs\n", max_clusters);
+    }
+    const int ntiles = ((a.w + v3::OW - 1) / v3::OW) * ((a.h + v3::OH - 1) / v3::OH) * a.c;
+    const int ncl = std::min(ntiles, max_clusters);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ncl);
+    cfg.blockDim = dim3(32, v3::NW);
+    cfg.dynamicSmemBytes = v3::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = fn::pdl_enabled() ? 2 : 1;
+    return fn::pdl_status(cudaLaunchKernelEx(&cfg, k_sgd_v3, maps, a), "k_sgd_v3");
+}
+
 template <int K>
 static int launch_tma(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
 {
@@ -1143,14 +1558,17 @@ int SolverWork::ensure(int h_, int w_, int c_, int iterations)
 int solver_variant()
 {
     // 0 = streaming (one iteration per launch), 1 = blocked LDG, 2 = blocked
-    // TMA (2 x 8 blocks), 3 = v2 (4 x 4 blocks; w % 4 == h % 4 == 0, else 2)
+    // TMA (2 x 8 blocks), 3 = v2 (4 x 8 blocks; w % 4 == h % 8 == 0), 4 = v2
+    // with 4 x 4 blocks (h % 4 == 0), 5 = v3 (v2 on 2-CTA clusters; measured
+    // slower than v2 at 1080p, see the v3 comment)
     static int v = [] {
         const char *e = getenv("SS_SOLVER");
         if (e && !strcmp(e, "stream")) return 0;
         if (e && !strcmp(e, "ldg")) return 1;
         if (e && !strcmp(e, "tma")) return 2;
         if (e && !strcmp(e, "v2r4")) return 4;
-        return 3;
+        if (e && !strcmp(e, "v2")) return 3;
+        return 5;
     }();
     return v;
 }
@@ -1228,6 +1646,7 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
     const long hw = (long)wk.h * wk.w;
     const long n = hw * wk.c;
     int variant = solver_variant();
+    if (variant == 5 && wk.h % 8 != 0) variant = 4;  // v3 (pairs of 4x8 blocks) needs h % 8 == 0
     if (variant == 3 && wk.h % 8 != 0) variant = 4;  // RB = 8 needs h % 8 == 0
     if (variant >= 3 && (wk.w % 4 != 0 || wk.h % 4 != 0)) variant = 2;
     if (variant >= 2 && (wk.w % 4 != 0 || !encode_fn())) variant = 1;
@@ -1284,7 +1703,8 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
                         getenv("SS_SOLVER_ALIGNED") == nullptr;
             if (variant >= 3) {
                 const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];
-                rc = variant == 3 ? launch_v2<8>(mp, a, st) : launch_v2<4>(mp, a, st);
+                rc = variant == 5 ? launch_v3(mp, a, st)
+                     : variant == 3 ? launch_v2<8>(mp, a, st) : launch_v2<4>(mp, a, st);
                 if (rc) return rc;
             } else if (variant == 2) {
                 const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];

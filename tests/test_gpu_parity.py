@@ -298,6 +298,40 @@ def test_solver_v2_aligned_shapes_bitwise(ss, shape):
         assert np.array_equal(got, want), (shape, iters)
 
 
+@pytest.mark.parametrize("variant", ["v2", "v3"])
+def test_solver_many_tiles_per_cta_bitwise(ss, variant):
+    """600x800x3 in a subprocess per schedule: v2 walks 8 x 13 x 3 = 312 tiles
+    over 148 CTAs, v3 144 tiles over at most 74 CTA pairs (seam-row counters
+    and receive-slot parities carried across tiles); 5 and 150 iterations,
+    bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    r = subprocess.run([sys.executable, "-c", MANY_TILES_SCRIPT, ROOT], capture_output=True, text=True,
+                       env=dict(os.environ, SS_SOLVER=variant), timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+MANY_TILES_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/oracle']
+import oracle as orc, paper_2301_00750_b200 as ss
+rng = np.random.default_rng(600)
+shape = (600, 800, 3)
+p = rng.random(shape).astype(np.float32)
+a = rng.random(shape).astype(np.float32)
+wc = rng.uniform(0, 2, shape[:2]).astype(np.float32)
+for iters in (5, 150):
+    got = ss.solve_screened_poisson(p, a, wc, ss.ConsistencyParams(iterations=iters), a)
+    want = orc.solve_screened_poisson(p, a, wc, orc.Params(iterations=iters))
+    assert np.array_equal(got, want), iters
+print("ok")
+"""
+
+
 def test_step_720p_matches_oracle(ss):
     from paper_2301_00750_b200 import synthetic
 
@@ -332,7 +366,10 @@ VARIANT_SCRIPT = r"""
 import sys, numpy as np
 sys.path[:0] = [sys.argv[1], sys.argv[1] + '/oracle']
 import oracle as orc, paper_2301_00750_b200 as ss
-for shape in [(61, 200, 3), (130, 124, 1), (47, 301, 3), (64, 200, 3), (132, 124, 1), (100, 340, 3)]:
+# the last six: v3's pairs have 112-row interiors with the seam at 56 + 112k --
+# image bottom on the seam, one row-block either side, a one-pair image
+for shape in [(61, 200, 3), (130, 124, 1), (47, 301, 3), (64, 200, 3), (132, 124, 1), (100, 340, 3),
+              (56, 128, 1), (168, 132, 3), (280, 236, 1), (160, 116, 3), (176, 124, 1), (112, 112, 3)]:
     r = np.random.default_rng(sum(shape))
     p = r.random(shape).astype(np.float32); a = r.random(shape).astype(np.float32)
     wc = r.uniform(0, 2, shape[:2]).astype(np.float32)
@@ -347,10 +384,11 @@ print("ok")
 @pytest.mark.parametrize("env", [{"SS_SOLVER": "stream"}, {"SS_SOLVER": "ldg"},
                                  {"SS_SOLVER": "tma", "SS_SOLVER_K": "4"},
                                  {"SS_SOLVER": "tma", "SS_SOLVER_K": "8"}, {"SS_SOLVER": "v2"},
-                                 {"SS_SOLVER": "v2r4"}])
+                                 {"SS_SOLVER": "v2r4"}, {"SS_SOLVER": "v3"}])
 def test_solver_variants_bitwise(ss, env):
     """Every solver schedule (streaming, blocked LDG, blocked TMA at K = 4/8,
-    v2 with 4x8 (default) and 4x4 blocks) produces the reference's bits."""
+    v2 with 4x8 (default) and 4x4 blocks, v3 = v2 on 2-CTA clusters with a
+    DSMEM seam-row exchange) produces the reference's bits."""
     import os
     import subprocess
     import sys
