@@ -88,12 +88,15 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def params_for(t):
+def params_for(t, fast=False):
+    """The interactive per-frame schedule (k1/k2, lambda toggled); fast: the
+    same on the reference's "fast" preset (50 iterations, flow_downscale 2)."""
     from paper_2301_00750_b200.consistency import ConsistencyParams
 
+    base = {"iterations": 50, "flow_downscale": 2} if fast else {}
     if t % 2 == 0:
-        return ConsistencyParams(k1=0.3, k2=0.5, lam=2.0)
-    return ConsistencyParams(k1=0.5, k2=0.3, lam=0.5)
+        return ConsistencyParams(k1=0.3, k2=0.5, lam=2.0, **base)
+    return ConsistencyParams(k1=0.5, k2=0.3, lam=0.5, **base)
 
 
 def load_peaks():
@@ -354,6 +357,8 @@ class Env:
                 from paper_2301_00750_b200.flow import BuiltinFlow
 
                 self._flows[kind] = BuiltinFlow()  # the reference's default provider
+            elif kind == "fp32_ds2":  # the fast preset's flow_downscale = 2
+                self._flows[kind] = ss.LiteFlowNet(seed=0, precision="fp32", downscale=2)
             else:
                 self._flows[kind] = ss.LiteFlowNet(seed=0, precision=kind)
         return self._flows[kind]
@@ -373,6 +378,8 @@ FLOW_DESC = {"fp32": "lite flow CNN, fp32-class (3xTF32 tcgen05 convs, fp32 acti
              "bf16": "lite flow CNN, bf16 tcgen05 convs, random-init seeded weights",
              "dis": "reference built-in DIS flow (BuiltinFlow, FlowOptions()) on GPU, "
                     "bit-identical to flow.py (tests/test_gpu_fullsize.py)",
+             "fp32_ds2": "lite flow CNN, fp32 path, on 2x box-downscaled frames (FlowOptions.downscale "
+                         "semantics, the fast preset's flow_downscale), flow resized back x2",
              "constant": "ConstantFlow(2,1) on device"}
 
 
@@ -387,7 +394,8 @@ def run_stream(env, h, w, flow_kind, steps, warmup, e2e=True, e2e_python=False, 
     pool_n = 8
     pool = [seq.frame(k + 1) for k in range(pool_n)]
     torch.cuda.synchronize()
-    state = ss.SessionState(params=params_for(0))
+    fast = flow_kind == "fp32_ds2"
+    state = ss.SessionState(params=params_for(0, fast))
     stream = torch.cuda.current_stream()
     pos = [0]
 
@@ -407,7 +415,7 @@ def run_stream(env, h, w, flow_kind, steps, warmup, e2e=True, e2e_python=False, 
         i2, p2 = pool[pos[0] % pool_n]
         _check(L.ss_stage_pair(state.handle, pos[0] + 1, i2.data_ptr(), p2.data_ptr(),
                                lib.SS_F32, lib.SS_DEVICE), L)
-        state.params = params_for(pos[0])
+        state.params = params_for(pos[0], fast)
         _run_step(state, flow, with_next=True, return_host=False)
 
     for _ in range(warmup):
@@ -468,7 +476,8 @@ def run_e2e_abi(env, state, pool, flow_kind, h, w, steps, warmup):
     outs = [torch.empty((h, w, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
     sess = state.handle
     pos = [int(L.ss_solved_through(sess)) + 1]
-    use_cnn = flow_kind in ("fp32", "bf16")
+    use_cnn = flow_kind in ("fp32", "bf16", "fp32_ds2")
+    fast = flow_kind == "fp32_ds2"
     if use_cnn:
         _check(L.ss_session_attach_flownet(sess, env.flow(flow_kind).handle()), L)
 
@@ -492,7 +501,7 @@ def run_e2e_abi(env, state, pool, flow_kind, h, w, steps, warmup):
         # the next pair's upload overlaps this step (ss_push_pair swaps it in)
         _check(L.ss_stage_pair(sess, pos[0] + 1, host_i[(k + 1) % n_host].data_ptr(),
                                host_p[(k + 1) % n_host].data_ptr(), lib.SS_F32, lib.SS_HOST), L)
-        prm = params_struct(params_for(t))
+        prm = params_struct(params_for(t, fast))
         it = ctypes.c_int(0)
         _check(L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)), L)
         _check(L.ss_output_async(sess, outs[k % 2].data_ptr(), lib.SS_F32, lib.SS_HOST), L)
@@ -579,17 +588,18 @@ def rooflines(env, h, w, res, flow_kind):
     peaks, src = env.peaks, env.peaks_src
     st = res["stage_ms"]
     n = h * w
-    solve_ops = SOLVER_OPS_PER_ELEM * 3 * n * SOLVER_ITERS
+    iters = 50 if flow_kind == "fp32_ds2" else SOLVER_ITERS  # the fast preset
+    solve_ops = SOLVER_OPS_PER_ELEM * 3 * n * iters
     achieved = solve_ops / (st["solve"] * 1e-3) / 1e12
     traffic = _traffic_table()
-    n_pass = math.ceil(SOLVER_ITERS / 8)
+    n_pass = math.ceil(iters / 8)
     line = {
-        "kernel": "k_sgd_v2<8> (K2: 150 SGD-momentum iterations as 19 temporally blocked passes)",
+        "kernel": f"k_sgd_v2<8> (K2: {iters} SGD-momentum iterations as {n_pass} temporally blocked passes)",
         "bound": "fp32", "achieved": round(achieved, 3), "peak": round(FP32_PEAK_TOPS, 2),
         "unit": "TFLOP/s", "frac": round(achieved / FP32_PEAK_TOPS, 4),
         "traffic": traffic.get("k_sgd_v2 solver pass") if (h, w) == (1080, 1920) else None,
         "algorithmic": f"{SOLVER_OPS_PER_ELEM} FP32 ops/px/channel/iteration x 3 x {n} px x "
-                       f"{SOLVER_ITERS} = {solve_ops / 1e9:.2f} G ops per solve",
+                       f"{iters} = {solve_ops / 1e9:.2f} G ops per solve",
         "peak_source": "measured FP32 result rate (tools/fp32_rate_probe.cu: 126.5/clk/SM) x 148 "
                        "SMs x 1965 MHz; MEASURED_PEAKS.json has no FP32 entry",
         "launch_ms": round(st["solve"] / n_pass, 5), "stage_ms": round(st["solve"], 4),
@@ -601,12 +611,12 @@ def rooflines(env, h, w, res, flow_kind):
             "achieved": round(k1, 1), "peak": hbm, "unit": "GB/s", "frac": round(k1 / hbm, 4),
             "traffic": traffic.get("k_presolve K1") if (h, w) == (1080, 1920) else None,
             "launch_ms": round(st["warp_blend"], 5), "peak_source": f"hbm_gbs {src}"}]
-    if flow_kind in ("fp32", "bf16"):
+    if flow_kind in ("fp32", "bf16", "fp32_ds2"):
         bf = float(peaks.get("bf16_tflops_sustained", 1400.0))
         peak = bf if flow_kind == "bf16" else bf / 6.0
         psrc = (f"bf16_tflops_sustained {src}" if flow_kind == "bf16" else
                 f"bf16_tflops_sustained {src} / 2 (tf32 rate) / 3 (3xTF32 MMAs per product)")
-        gflop = FLOW_GFLOP_1080 * n / (1920 * 1080)
+        gflop = FLOW_GFLOP_1080 * n / (1920 * 1080) / (4 if flow_kind == "fp32_ds2" else 1)
         sec.append({"kernel": "lite flow CNN stage (1 pyramid + 2 flows, concurrent streams)",
                     "bound": "tensor", "achieved": round(gflop / st["flow"], 2), "peak": round(peak, 1),
                     "unit": "TFLOP/s", "frac": round(gflop / st["flow"] / peak, 4),
@@ -666,6 +676,11 @@ def run_configs(env, args):
         r = run_stream(env, 2160, 3840, "fp32", steps, warm, e2e=True)
         out["configs[3]"] = config_entry(
             env, "3", 2160, 3840, "fp32", r, "3840x2160 single stream, lite flow CNN fp32 path")
+        r = run_stream(env, H, W, "fp32_ds2", steps, warm, e2e=True)
+        out["fast_1080p"] = config_entry(
+            env, "fast", H, W, "fp32_ds2", r,
+            "1920x1080 single stream, the reference's 'fast' preset (50 iterations, flow_downscale 2: "
+            "the lite CNN on 960x540 box-downscaled frames) + interactive schedule")
         r = run_stream(env, H, W, "dis", steps, warm, e2e=True)
         out["dis_1080p"] = config_entry(
             env, "dis", H, W, "dis", r,

@@ -200,6 +200,12 @@ SS_API int64_t ss_flownet_num_params(void);
  * accumulation). */
 enum ss_flow_precision { SS_FLOW_FP32 = 0, SS_FLOW_BF16 = 1 };
 SS_API int ss_flownet_create(const float *weights, int64_t n, int precision, ss_flownet **out);
+/* Provider downscale (replaces FlowOptions.downscale, flow.py:34, :183-188,
+   for this provider): the network runs on box_downscale(frame, d) and its
+   flow is resize_bilinear'd back to the frame size times d.  d in {1, 2, 4}
+   (else SS_VALUE_ERROR, the reference's message); the fast preset's
+   flow_downscale (consistency.py:101) is what callers pass. */
+SS_API int ss_flownet_set_downscale(ss_flownet *net, int downscale);
 SS_API int ss_flownet_destroy(ss_flownet *net);
 /* Stateless: flow from frame_a toward frame_b ((h, w, c) HWC float32 device
  * pointers) into uv (h, w, 2) and valid (h, w) (may be NULL); stream-ordered.

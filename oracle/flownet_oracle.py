@@ -134,9 +134,48 @@ def pyramid(weights, img):
     return feats  # index l-1 -> level l
 
 
-def flow(weights, img1, img2, pyr1=None, pyr2=None):
+def box_downscale(arr, f):
+    """Restates reference flow.py:69-80: integer box average, remainder cropped."""
+    arr = np.asarray(arr, np.float32)
+    if f == 1:
+        return arr
+    h2, w2 = arr.shape[0] // f * f, arr.shape[1] // f * f
+    c = arr[:h2, :w2]
+    v = c.reshape(h2 // f, f, w2 // f, f, *c.shape[2:])
+    return v.mean(axis=(1, 3), dtype=np.float32)
+
+
+def resize_bilinear(arr, shape):
+    """Restates reference flow.py:54-66 (+ _bilinear_gather :83-99): pixel
+    centres, border clamp, float32."""
+    arr = np.asarray(arr, np.float32)
+    ih, iw = arr.shape[:2]
+    oh, ow = shape
+    if (ih, iw) == (oh, ow):
+        return arr.copy()
+    ys = (np.arange(oh, dtype=np.float32) + 0.5) * (ih / oh) - 0.5
+    xs = (np.arange(ow, dtype=np.float32) + 0.5) * (iw / ow) - 0.5
+    yy, xx = np.meshgrid(ys, xs, indexing="ij")
+    yy = np.clip(yy, 0.0, ih - 1.0)
+    xx = np.clip(xx, 0.0, iw - 1.0)
+    y0, x0 = np.floor(yy).astype(np.intp), np.floor(xx).astype(np.intp)
+    y1, x1 = np.minimum(y0 + 1, ih - 1), np.minimum(x0 + 1, iw - 1)
+    fy = (yy - y0).astype(np.float32)[..., None]
+    fx = (xx - x0).astype(np.float32)[..., None]
+    top = arr[y0, x0] * (1 - fx) + arr[y0, x1] * fx
+    bot = arr[y1, x0] * (1 - fx) + arr[y1, x1] * fx
+    return (top * (1 - fy) + bot * fy).astype(np.float32)
+
+
+def flow(weights, img1, img2, pyr1=None, pyr2=None, downscale=1):
     """Flow from img1 toward img2 (FlowProvider.flow_between(t, I_t, b, I_b)):
-    (H, W, 2) float32, u horizontal, v vertical, in full-resolution pixels."""
+    (H, W, 2) float32, u horizontal, v vertical, in full-resolution pixels.
+    downscale d: the network on box_downscale(frame, d), the flow resized back
+    times d -- the provider-level FlowOptions.downscale of flow.py:183-188."""
+    if downscale != 1:
+        h, w = np.asarray(img1).shape[:2]
+        small = flow(weights, box_downscale(img1, downscale), box_downscale(img2, downscale))
+        return resize_bilinear(small, (h, w)) * np.float32(downscale)
     h, w = np.asarray(img1).shape[:2]
     p1 = pyr1 or pyramid(weights, img1)
     p2 = pyr2 or pyramid(weights, img2)

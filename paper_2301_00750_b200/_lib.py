@@ -34,7 +34,7 @@ EXPORTS = (
     "ss_session_create", "ss_session_destroy", "ss_session_reset", "ss_push_pair", "ss_stage_pair",
     "ss_solved_through", "ss_pending", "ss_set_flow", "ss_set_constant_flow", "ss_check_step",
     "ss_step", "ss_output", "ss_output_async", "ss_output_wait", "ss_output_device", "ss_last_timing", "ss_flows",
-    "ss_session_stream", "ss_session_join", "ss_flownet_num_params", "ss_flownet_create", "ss_flownet_destroy",
+    "ss_session_stream", "ss_session_join", "ss_flownet_num_params", "ss_flownet_create", "ss_flownet_set_downscale", "ss_flownet_destroy",
     "ss_flownet_flow", "ss_session_attach_flownet", "ss_session_compute_flow",
     "ss_warping_error_sums", "ss_ssim", "ss_session_time_conv", "ss_dis_flow",
     "ss_session_compute_dis_flow", "ss_session_wait_stream", "ss_session_signal_stream",
@@ -103,6 +103,7 @@ def _declare(L):
         "ss_session_join": (i32, [vp]),
         "ss_flownet_num_params": (i64, []),
         "ss_flownet_create": (i32, [vp, i64, i32, P(vp)]),
+        "ss_flownet_set_downscale": (i32, [vp, i32]),
         "ss_flownet_destroy": (i32, [vp]),
         "ss_flownet_flow": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
         "ss_session_attach_flownet": (i32, [vp, vp]),

@@ -301,6 +301,7 @@ struct StreamOrder {
 struct ss_flownet {
     int device;
     int precision;
+    int downscale = 1;  // FlowOptions.downscale (flow.py:34): network on box-downscaled frames
     fn::Weights wts;
     // stateless calls (ss_flownet_flow): one scratch set per frame size,
     // shared by all callers -- host threads serialise on the mutex, streams
@@ -1200,6 +1201,21 @@ int ss_flownet_create(const float *weights, int64_t n, int precision, ss_flownet
     return SS_OK;
 }
 
+int ss_flownet_set_downscale(ss_flownet *net, int downscale)
+{
+    if (downscale != 1 && downscale != 2 && downscale != 4) {
+        set_error("downscale must be 1, 2 or 4");
+        return SS_VALUE_ERROR;
+    }
+    std::lock_guard<std::mutex> lock(net->mu);
+    if (downscale != net->downscale) {
+        cudaDeviceSynchronize();
+        net->runs.clear();  // scratch sets are sized for the network's frame
+        net->downscale = downscale;
+    }
+    return SS_OK;
+}
+
 int ss_flownet_destroy(ss_flownet *net)
 {
     if (net) {
@@ -1219,7 +1235,7 @@ int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b,
     auto &run = entry.first;
     if (!run) {
         run.reset(new fn::Run());
-        if (int rc = run->init(&net->wts, h, w)) {
+        if (int rc = run->init(&net->wts, h, w, 1, net->downscale)) {
             run.reset();
             return rc;
         }
@@ -1235,7 +1251,7 @@ int ss_flownet_flow(ss_flownet *net, const float *frame_a, const float *frame_b,
 
 int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
 {
-    if (s->net == net && s->run) return SS_OK;
+    if (s->net == net && s->run && s->run->ds == net->downscale) return SS_OK;
     if (int rc = join_side(s)) return rc;
     SS_CUDA_TRY(cudaStreamSynchronize(s->stream));
     s->side_pending = false;
@@ -1244,7 +1260,7 @@ int ss_session_attach_flownet(ss_session *s, ss_flownet *net)
     const char *cc = getenv("SS_FLOW_CONCURRENT");
     const bool concurrent = cc == nullptr || strcmp(cc, "0");
     s->run.reset(new fn::Run());
-    if (int rc = s->run->init(&net->wts, s->h, s->w, concurrent ? 2 : 1)) {
+    if (int rc = s->run->init(&net->wts, s->h, s->w, concurrent ? 2 : 1, net->downscale)) {
         s->run.reset();
         s->net = nullptr;
         return rc;

@@ -243,12 +243,23 @@ void Run::select_set(int set)
     ws = s.ws;
 }
 
-int Run::init(const Weights *wt, int h_, int w_, int nsets_)
+int Run::init(const Weights *wt, int h_, int w_, int nsets_, int downscale)
 {
     nsets = nsets_ < 1 ? 1 : (nsets_ > 2 ? 2 : nsets_);
     wts = wt;
-    h = h_;
-    w = w_;
+    if (downscale != 1 && downscale != 2 && downscale != 4) {
+        set_error("downscale must be 1, 2 or 4");
+        return SS_VALUE_ERROR;
+    }
+    fh = h_;
+    fw = w_;
+    ds = downscale;
+    h = fh / ds;  // box_downscale crops the remainder (flow.py:74-75)
+    w = fw / ds;
+    if (h < 1 || w < 1) {
+        set_error("frame smaller than the flow downscale factor");
+        return SS_VALUE_ERROR;
+    }
     H[0] = (h + 63) / 64 * 64;
     W[0] = (w + 63) / 64 * 64;
     for (int l = 1; l <= 6; ++l) {
@@ -264,6 +275,10 @@ int Run::init(const Weights *wt, int h_, int w_, int nsets_)
     const size_t px1 = (size_t)H[1] * W[1];
     int rc;
     if ((rc = alloc(&prep, (size_t)H[0] * W[0] * 8))) return rc;
+    if (ds > 1) {
+        if ((rc = alloc(&small, (size_t)h * w * 3))) return rc;
+        if ((rc = alloc(&uv_small, (size_t)h * w * 2))) return rc;
+    }
     if ((rc = alloc(&s0, px1 * 16))) return rc;
     if ((rc = alloc(&s1, px1 * 16))) return rc;
     for (auto &sl : slots)
@@ -495,6 +510,11 @@ int Run::pyramid_impl(int slot, const float *img, int c, cudaStream_t st)
     ws_floats_ = ws_floats;
     int rc;
     prof.mark("start", st);
+    if (ds > 1) {  // the network sees the box-downscaled frame
+        if ((rc = launch_box_down_hwc(img, fw, c, ds, h, w, small, st))) return rc;
+        img = small;
+        prof.mark("downscale", st);
+    }
     // the frame -> level-1 "a" layer in one FFMA pass (SS_PYR1A_FUSED=0: the
     // 8-channel padded copy + tensor-core conv)
     static const bool fused = getenv("SS_PYR1A_FUSED") == nullptr || strcmp(getenv("SS_PYR1A_FUSED"), "0");
@@ -573,7 +593,13 @@ int Run::flow_impl(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
         in_ld = 128;
     }
     if ((rc = convp("ref7", wts->L(REF7), rb, 128, hh, ww, rr, 4, st))) return rc;
-    rc = launch_flow_final(E[3], E_LD, rr, 4, hh, ww, h, w, uv, valid, st);
+    if (ds > 1) {
+        // resize_bilinear(flow, frame shape) * downscale (flow.py:187)
+        if ((rc = launch_flow_final(E[3], E_LD, rr, 4, hh, ww, h, w, uv_small, nullptr, st))) return rc;
+        rc = launch_upscale_flow(uv_small, h, w, fh, fw, (float)ds, uv, valid, st);
+    } else {
+        rc = launch_flow_final(E[3], E_LD, rr, 4, hh, ww, h, w, uv, valid, st);
+    }
     prof.mark("final", st);
     prof.dump("flow");
     return rc;

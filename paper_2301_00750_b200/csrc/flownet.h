@@ -85,6 +85,11 @@ int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x,
                 bool copy_f1, cudaStream_t st);
 int launch_flow_final(const float *f3, int ld3, const float *r, int ldr, int Hc, int Wc, int h,
                       int w, float *uv, uint8_t *valid, cudaStream_t st);
+// provider downscale: box_downscale of an HWC frame by f; resize of the
+// network's flow back to the frame size, times s (FlowOptions.downscale)
+int launch_box_down_hwc(const float *in, int w, int c, int f, int ho, int wo, float *out, cudaStream_t st);
+int launch_upscale_flow(const float *in, int hi, int wi, int ho, int wo, float s, float *uv, uint8_t *valid,
+                        cudaStream_t st);
 
 struct LayerDev {
     int cin, cout, cout_pad, k, stride, dil, act;
@@ -119,7 +124,11 @@ struct Weights {
 struct Run {
     const Weights *wts = nullptr;
     int conv_mode = CONV_TC_TF32X3;
+    // h, w: the network's frame; fh, fw: the caller's frame (fh / ds, fw / ds
+    // = h, w with downscale ds: FlowOptions.downscale semantics)
     int h = 0, w = 0, H[7] = {0}, W[7] = {0};
+    int fh = 0, fw = 0, ds = 1;
+    float *small = nullptr, *uv_small = nullptr;
     float *prep = nullptr, *s0 = nullptr, *s1 = nullptr;
     struct Slot {
         int64_t key = -1;
@@ -145,7 +154,7 @@ struct Run {
     std::map<std::tuple<int, const void *, int>, std::pair<cudaGraphExec_t, long>> pyr_graphs;
     std::map<std::tuple<int, int, void *, void *, int>, std::pair<cudaGraphExec_t, long>> flow_graphs;
     ~Run();
-    int init(const Weights *w, int h, int w_, int nsets = 1);
+    int init(const Weights *w, int h, int w_, int nsets = 1, int downscale = 1);
     // pyramid of img (h, w, c) into slot (skipped if key matches)
     int pyramid(int slot, int64_t key, const float *img, int c, cudaStream_t st);
     // flow from the frame in slot a toward the frame in slot b (both computed),

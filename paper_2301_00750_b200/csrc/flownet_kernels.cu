@@ -521,6 +521,69 @@ int launch_flow_final(const float *f3, int ld3, const float *r, int ldr, int Hc,
 }
 
 // ---------------------------------------------------------------------------
+// provider-level downscale (FlowOptions.downscale, flow.py:34, :183-188): the
+// network runs on box-downscaled frames and its flow is resized back
+
+// box_downscale (flow.py:69-80) of an HWC frame by f (remainder cropped): per
+// channel the f x f block, each row summed left to right, the row sums in
+// order, then / f^2
+__global__ void k_box_down_hwc(const float *__restrict__ in, int w, int c, int f, int ho, int wo,
+                               float *__restrict__ out)
+{
+    pdl_wait();
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)ho * wo * c) return;
+    const int ch = (int)(i % c);
+    const long p = i / c;
+    const int y = (int)(p / wo), x = (int)(p - (long)y * wo);
+    float tot = 0.f;
+    for (int dy = 0; dy < f; ++dy) {
+        const float *row = in + ((long)(y * f + dy) * w + (long)x * f) * c + ch;
+        float r = row[0];
+        for (int dx = 1; dx < f; ++dx) r = __fadd_rn(r, row[dx * c]);
+        tot = dy == 0 ? r : __fadd_rn(tot, r);
+    }
+    out[i] = __fdiv_rn(tot, (float)(f * f));
+}
+
+int launch_box_down_hwc(const float *in, int w, int c, int f, int ho, int wo, float *out, cudaStream_t st)
+{
+    return launch_pdl("k_box_down_hwc", k_box_down_hwc, dim3(blocks_for((long)ho * wo * c, 256)), dim3(256), 0, st,
+                      in, w, c, f, ho, wo, out);
+}
+
+// resize_bilinear (flow.py:54-66: pixel centres, border clamp) of the
+// network's (hi, wi, 2) flow to the frame's (ho, wo), times s; valid as a
+// FlowField marks it (imgio.py: finite and |u|, |v| <= 1e9)
+__global__ void k_upscale_flow(const float *__restrict__ in, int hi, int wi, int ho, int wo, float ry, float rx,
+                               float s, float *__restrict__ uv, uint8_t *__restrict__ valid)
+{
+    pdl_wait();
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)ho * wo) return;
+    const int y = (int)(i / wo), x = (int)(i - (long)y * wo);
+    const float ys = fminf(fmaxf(((float)y + 0.5f) * ry - 0.5f, 0.f), (float)(hi - 1));
+    const float xs = fminf(fmaxf(((float)x + 0.5f) * rx - 0.5f, 0.f), (float)(wi - 1));
+    const int y0 = (int)floorf(ys), x0 = (int)floorf(xs);
+    const int y1 = min(y0 + 1, hi - 1), x1 = min(x0 + 1, wi - 1);
+    const float fy = ys - (float)y0, fx = xs - (float)x0;
+    const float2 *f2 = reinterpret_cast<const float2 *>(in);
+    const float2 a = f2[(long)y0 * wi + x0], b = f2[(long)y0 * wi + x1];
+    const float2 c = f2[(long)y1 * wi + x0], d = f2[(long)y1 * wi + x1];
+    const float u = ((a.x * (1.f - fx) + b.x * fx) * (1.f - fy) + (c.x * (1.f - fx) + d.x * fx) * fy) * s;
+    const float v = ((a.y * (1.f - fx) + b.y * fx) * (1.f - fy) + (c.y * (1.f - fx) + d.y * fx) * fy) * s;
+    reinterpret_cast<float2 *>(uv)[i] = make_float2(u, v);
+    if (valid) valid[i] = fabsf(u) <= 1e9f && fabsf(v) <= 1e9f;
+}
+
+int launch_upscale_flow(const float *in, int hi, int wi, int ho, int wo, float s, float *uv, uint8_t *valid,
+                        cudaStream_t st)
+{
+    return launch_pdl("k_upscale_flow", k_upscale_flow, dim3(blocks_for((long)ho * wo, 256)), dim3(256), 0, st, in,
+                      hi, wi, ho, wo, (float)hi / (float)ho, (float)wi / (float)wo, s, uv, valid);
+}
+
+// ---------------------------------------------------------------------------
 // split-K reduction of the conv kernels' partial sums (flownet_tma.cu)
 
 // out[m, n] = act(sum_s ws[s, m, n] + bias[n])

@@ -1567,8 +1567,8 @@ int solver_variant()
         if (e && !strcmp(e, "ldg")) return 1;
         if (e && !strcmp(e, "tma")) return 2;
         if (e && !strcmp(e, "v2r4")) return 4;
-        if (e && !strcmp(e, "v2")) return 3;
-        return 5;
+        if (e && !strcmp(e, "v3")) return 5;
+        return 3;
     }();
     return v;
 }

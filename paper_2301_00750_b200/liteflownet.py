@@ -172,16 +172,25 @@ class LiteFlowNet:
     passes.  ``flow_between`` is the stateless form (FlowField out).
     precision: "fp32" (3xTF32 on tcgen05: fp32-class accuracy) or "bf16"
     (bf16 operands on tcgen05, fp32 accumulation).
+    downscale: FlowOptions.downscale semantics (flow.py:34, :183-188) -- the
+    network runs on ``box_downscale(frame, d)`` and the flow is
+    ``resize_bilinear``'d back times d; callers pass the preset's
+    ``flow_downscale`` (the fast preset: 2), as ``service.py:188`` does for
+    the built-in provider.
     """
 
-    def __init__(self, weights: dict | None = None, seed: int = 0, precision: str = "fp32"):
+    def __init__(self, weights: dict | None = None, seed: int = 0, precision: str = "fp32",
+                 downscale: int = 1):
         if precision not in ("fp32", "bf16"):
             raise ValueError("precision must be 'fp32' or 'bf16'")
+        if downscale not in (1, 2, 4):
+            raise ValueError("downscale must be 1, 2 or 4")
         self.weights = weights if weights is not None else make_weights(seed)
         self.precision = precision
+        self.downscale = downscale
         self._flat = flatten_weights(self.weights)
         self._nets = {}
-        self.backend_id = f"liteflownet(4light-sepref,{precision})"
+        self.backend_id = f"liteflownet(4light-sepref,{precision},downscale={downscale})"
 
     def handle(self):
         import ctypes
@@ -198,6 +207,7 @@ class LiteFlowNet:
             _dev.check(L.ss_flownet_create(self._flat.ctypes.data, self._flat.size, prec,
                                            ctypes.byref(h)))
             self._nets[dev.index] = h
+            _dev.check(L.ss_flownet_set_downscale(h, self.downscale))
         return self._nets[dev.index]
 
     def __del__(self):

@@ -160,3 +160,52 @@ def test_concurrent_sessions_threads_bitwise(ss, net):
         assert sorted(got[k]) == sorted(want[k])
         for t in want[k]:
             assert np.array_equal(got[k][t], want[k][t]), (k, t)
+
+
+# ------------------------------------------- provider downscale (fast preset)
+@pytest.mark.parametrize("shape,d", [((130, 200, 3), 2), ((257, 321, 3), 2), ((260, 392, 1), 4)])
+def test_flow_downscale_matches_cpu(ss, net, shape, d):
+    """FlowOptions.downscale semantics for the CNN (flow.py:183-188): the
+    network on box_downscale(frame, d), the flow resize_bilinear'd back times
+    d -- odd sizes crop the remainder.  Same fp32 bar as the full-resolution
+    path, scaled by d (the flow is d times the network's)."""
+    from paper_2301_00750_b200 import synthetic
+
+    nd = ss.LiteFlowNet(weights=net.weights, downscale=d)
+    seq = synthetic.translating_sequence(frames=2, height=shape[0], width=shape[1], seed=6)
+    a, b = seq.inputs[1], seq.inputs[0]
+    if shape[2] == 1:
+        a, b = a.mean(axis=2, keepdims=True), b.mean(axis=2, keepdims=True)
+    got = nd.flow_between(2, a, 1, b)
+    want = fo.flow(net.weights, a, b, downscale=d)
+    assert got.uv.shape == want.shape == shape[:2] + (2,) and got.valid.all()
+    e = _epe(got.uv, want)
+    assert float(e.max()) <= 2e-3 * d and float(e.mean()) <= 5e-4 * d, (float(e.max()), float(e.mean()))
+
+
+def test_fast_preset_stream_with_downscaled_cnn(ss, net):
+    """The fast preset end to end (50 iterations, flow_downscale 2 handed to the
+    provider as service.py:188 does): GPU session vs the C oracle fed the CPU
+    network's downscaled flows, O_t within 1e-3."""
+    from paper_2301_00750_b200 import synthetic
+
+    p = ss.preset("fast")
+    nd = ss.LiteFlowNet(weights=net.weights, downscale=p.flow_downscale)
+    seq = synthetic.translating_sequence(frames=3, height=96, width=160, step=(2, 1), seed=8)
+    got = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), p, nd))
+
+    def cnn_fn(a, fa, b, fb):
+        uv = fo.flow(net.weights, fa, fb, downscale=p.flow_downscale)
+        return uv, np.ones(uv.shape[:2], bool)
+
+    want = dict(orc.stabilize_stream(seq.inputs, seq.processed,
+                                     orc.Params(k1=p.k1, k2=p.k2, alpha=p.alpha, lam=p.lam, eta=p.eta,
+                                                kappa=p.kappa, iterations=p.iterations), cnn_fn))
+    assert sorted(got) == sorted(want)
+    for t in want:
+        assert float(np.abs(got[t] - want[t]).max()) <= 1e-3, t
+
+
+def test_downscale_validation(ss):
+    with pytest.raises(ValueError, match="downscale must be 1, 2 or 4"):
+        ss.LiteFlowNet(seed=0, downscale=3)
