@@ -547,6 +547,7 @@ int Run::pyramid_impl(int slot, const float *img, int c, cudaStream_t st)
         in_ld = C;
     }
     prof.dump("pyramid");
+    conv_trace_dump("pyramid");
     return SS_OK;
 }
 
@@ -602,6 +603,7 @@ int Run::flow_impl(int a, int b, float *uv, uint8_t *valid, cudaStream_t st)
     }
     prof.mark("final", st);
     prof.dump("flow");
+    conv_trace_dump("flow");
     return rc;
 }
 

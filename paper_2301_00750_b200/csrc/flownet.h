@@ -66,7 +66,8 @@ enum ConvMode { CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
 
 // kind 0: bf16 operands (kind::f16); kind 1: 3xTF32 (kind::tf32)
 // TMA-fed warp-specialised 3xTF32 conv (flownet_tma.cu)
-int launch_conv_tma(const ConvParams &p, int prec, cudaStream_t st);  // prec: 1 3xTF32, 0 bf16
+int launch_conv_tma(const ConvParams &p, int prec, cudaStream_t st);
+void conv_trace_dump(const char *what);  // SS_CONV_TRACE diagnostics  // prec: 1 3xTF32, 0 bf16
 int prepare_conv_tma();
 int prepare_flow_kernels();
 int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, int np, int T);

@@ -38,6 +38,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -75,7 +76,25 @@ struct ConvArgs {
     const float *bias;
     float *out;
     float *ws;  // split-K partials [part][split][M][np] (null: final output)
+    unsigned long long *trace;  // SS_CONV_TRACE: globaltimer stamps of CTA 0 (diagnostics)
 };
+
+// Diagnostics build only (make EXTRA=-DSS_CONV_TRACE_BUILD, then run with
+// SS_CONV_TRACE=1): the null checks alone cost ~2% of the 1080p step when
+// compiled in, so the default build has none.
+__device__ __forceinline__ void trace_at(const ConvArgs &a, int k)
+{
+#ifdef SS_CONV_TRACE_BUILD
+    if (a.trace && blockIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[k] = t;
+    }
+#else
+    (void)a;
+    (void)k;
+#endif
+}
 
 // unit u -> (part, split, tile): units = parts * splits * n_tiles
 struct ConvUnit {
@@ -170,6 +189,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     // warp index through a shuffle: the compiler then knows it (and every
     // role branch) is warp-uniform and keeps descriptors in uniform registers
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) trace_at(a, 0);
     const uint32_t acc_cols = (uint32_t)((PREC ? 2 : 1) * np + 31) / 32 * 32;
     uint32_t tcols = 32;
     while (tcols < 2 * acc_cols) tcols <<= 1;
@@ -196,6 +216,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
     const uint32_t rowb = (uint32_t)a.cpp * 4u;
+    if (threadIdx.x == 0) trace_at(a, 1);
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -214,6 +235,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         }
         __syncwarp();
         pdl_wait();  // the activations are the previous kernel's output
+        if (lane == 0) trace_at(a, 2);
         uint32_t ga = 0, gb = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
             const ConvUnit cu = conv_unit(a, u);
@@ -238,6 +260,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     if (elect_one()) {
                         const uint32_t dst = smem_u32(aslots + sa * 2 * a.a_slot);
                         mbar_expect_tx(&a_full[sa], (uint32_t)a.a_box);
+                        if (ga < 9) trace_at(a, 12 + 4 * ga);
                         if (AMODE == 1) {
                             tma_tile_3d(dst, &tmA, cb * a.cpp, x0, y0, &a_full[sa]);
                         } else if (AMODE == 2) {
@@ -293,6 +316,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 if (a_event<AMODE>(st, kb, grp)) {
                     sa = (int)(ga % (uint32_t)NA);
                     mbar_wait(&a_conv[sa], (ga / NA) & 1);
+                    if (ga == 0 && lane == 0) trace_at(a, 5);
                     ++ga;
                 }
                 const int s = BRES ? st : (int)(gb % (uint32_t)S);
@@ -343,6 +367,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             }
             mma_commit_elect(&acc_full[acc]);
             __syncwarp();
+            if (uc == 0 && lane == 0) trace_at(a, 6);
+            if (uc < 9 && lane == 0) trace_at(a, 12 + 4 * uc + 2);
         }
     } else if (warp < 6) {
         // ---------------- epilogue ----------------
@@ -353,6 +379,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             const uint32_t acc = uc & 1;
             mbar_wait(&acc_full[acc], (uc >> 1) & 1);
             tc_fence_after();
+            if (uc == 0 && warp == 2 && lane == 0) trace_at(a, 7);
             const ConvUnit cu = conv_unit(a, u);
             const int tile = cu.tile, split = cu.split;
             const int cout = min(np, a.Cout - cu.part * np);  // this part's live channels
@@ -404,9 +431,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     }
                 }
             }
+            if (uc == 0 && warp == 2 && lane == 0) trace_at(a, 11);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            if (uc == 0 && warp == 2 && lane == 0) trace_at(a, 8);
+            if (uc < 9 && warp == 2 && lane == 0) trace_at(a, 12 + 4 * uc + 3);
         }
     } else {
         // ---------------- converters: A -> (hi in place, lo beside) ----------------
@@ -423,6 +453,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 if (!ev) continue;
                 const int sa = (int)(ga % (uint32_t)NA);
                 mbar_wait(&a_full[sa], (ga / NA) & 1);
+                if (ga == 0 && t == 0) trace_at(a, 3);
+                if (ga < 9 && t == 0) trace_at(a, 12 + 4 * ga + 1);
                 ++ga;
                 float4 *ar = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot);
                 if (PREC) {
@@ -455,11 +487,13 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_conv[sa]);
+                if (ga == 1 && t == 0) trace_at(a, 4);
             }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) trace_at(a, 9);
     if (threadIdx.x == 0) pdl_trigger();  // dependents launch as this grid drains
     if (warp == 1) {
         tc_fence_after();
@@ -606,6 +640,26 @@ int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, in
     return SS_OK;
 }
 
+// SS_CONV_TRACE=1 (diagnostics): every conv launch stamps CTA 0's milestones
+// (globaltimer) into a mapped host ring; conv_trace_dump prints them
+static unsigned long long *trace_host = nullptr, *trace_dev = nullptr;
+static int trace_n = 0;
+constexpr int TRACE_SLOTS = 128, TRACE_K = 48;  // 12 milestones + 4 per unit for 9 units
+static unsigned long long *conv_trace_slot()
+{
+#ifndef SS_CONV_TRACE_BUILD
+    return nullptr;
+#endif
+    static const bool on = getenv("SS_CONV_TRACE") != nullptr;
+    if (!on) return nullptr;
+    if (!trace_host) {
+        if (cudaHostAlloc(&trace_host, TRACE_SLOTS * TRACE_K * 8, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+        memset(trace_host, 0, TRACE_SLOTS * TRACE_K * 8);
+        cudaHostGetDevicePointer(&trace_dev, trace_host, 0);
+    }
+    return trace_dev + (size_t)(trace_n++ % TRACE_SLOTS) * TRACE_K;
+}
+
 using ConvKernel = void (*)(CUtensorMap, CUtensorMap, ConvArgs);
 
 static ConvKernel conv_kernel(int prec, int amode, bool res)
@@ -731,8 +785,12 @@ static int launch_parts(const ConvParams &p, const CUtensorMap &tmA, int prec, i
     static const int sk_f = getenv("SS_SPLITK_F") ? std::max(1, atoi(getenv("SS_SPLITK_F"))) : 4;
     static const int sk_max = getenv("SS_SPLITK_MAX") ? std::max(1, atoi(getenv("SS_SPLITK_MAX"))) : 8;
     const int tiles_all = a.n_tiles * parts;
+    // the CTAs this launch may use: units beyond them run as a second round,
+    // so the split count rounds DOWN (est5_1 at 1080p: 24 tiles x 7 splits =
+    // 168 units on 148 SMs took two rounds; x 6 = 144 takes one)
+    const int avail = p.grid_cap > 0 ? std::min(p.grid_cap, n_sm_tma) : n_sm_tma;
     if (p.ws && tiles_all * sk_f < n_sm_tma && a.nk_all >= 4) {
-        splits = std::min(std::min((n_sm_tma + tiles_all - 1) / tiles_all, a.nk_all / 2), sk_max);
+        splits = std::min(std::min(std::max(avail / tiles_all, 1), a.nk_all / 2), sk_max);
         const size_t need = (size_t)parts * splits * a.M * np;
         if (need > p.ws_floats) splits = (int)(p.ws_floats / ((size_t)parts * a.M * np));
         splits = std::max(splits, 1);
@@ -742,6 +800,7 @@ static int launch_parts(const ConvParams &p, const CUtensorMap &tmA, int prec, i
     a.splits = splits;
     a.ws = splits > 1 ? p.ws : nullptr;
     a.units = tiles_all * splits;
+    a.trace = conv_trace_slot();
     // SS_CONV_GRID_MAX (tests): fewer persistent CTAs, so small layers also
     // walk several units per CTA (TMEM accumulator alternation, ring wrap)
     static const int grid_max = getenv("SS_CONV_GRID_MAX") ? std::max(1, atoi(getenv("SS_CONV_GRID_MAX"))) : 0;
@@ -755,6 +814,28 @@ static int launch_parts(const ConvParams &p, const CUtensorMap &tmA, int prec, i
     if (splits > 1)
         return launch_splitk_reduce(p.ws, splits, a.M, np, p.Cout, p.bias, p.act, p.out, p.out_ld, st, parts);
     return SS_OK;
+}
+
+void conv_trace_dump(const char *what)
+{
+    if (!trace_host || !trace_n) return;
+    cudaDeviceSynchronize();
+    static const char *names[12] = {"entry", "setup", "pdl_ok", "A_land", "A_conv", "mma_go",
+                                         "mma_done", "epi_go", "epi_done", "exit", "epi_ld1", "epi_loop"};
+    for (int i = 0; i < trace_n && i < TRACE_SLOTS; ++i) {
+        const unsigned long long *t = trace_host + (size_t)i * TRACE_K;
+        fprintf(stderr, "[conv-trace] %s #%d", what, i);
+        for (int k = 1; k < 12; ++k)
+            fprintf(stderr, " %s=%+.2f", names[k], t[k] ? (double)(t[k] - t[0]) * 1e-3 : -1.0);
+        fprintf(stderr, " us\n");
+        for (int u = 0; u < 9 && t[12 + 4 * u]; ++u)
+            fprintf(stderr, "[conv-trace]    unit %d: A_issue %+.2f A_land %+.2f mma_done %+.2f epi_done %+.2f\n", u,
+                    (double)(t[12 + 4 * u] - t[0]) * 1e-3, (double)(t[13 + 4 * u] - t[0]) * 1e-3,
+                    t[14 + 4 * u] ? (double)(t[14 + 4 * u] - t[0]) * 1e-3 : -1.0,
+                    t[15 + 4 * u] ? (double)(t[15 + 4 * u] - t[0]) * 1e-3 : -1.0);
+    }
+    memset(trace_host, 0, TRACE_SLOTS * TRACE_K * 8);
+    trace_n = 0;
 }
 
 int launch_conv_tma(const ConvParams &p, int prec, cudaStream_t st)
