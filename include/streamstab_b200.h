@@ -158,6 +158,17 @@ SS_API int ss_push_pair(ss_session *s, int64_t position, const void *I, const vo
 SS_API int ss_stage_pair(ss_session *s, int64_t position, const void *I, const void *P, int dtype,
                          int where);
 SS_API int64_t ss_solved_through(const ss_session *s);
+/* Assign SessionState.solved_through / prev_output (the reference's dataclass
+ * fields, consistency.py:305-319, read by _snippet :342-345): resume a stream
+ * from a known O_{t-1}.  mode SS_STATE_POSITION sets solved_through only;
+ * SS_STATE_OUTPUT also uploads prev_output (H, W, c_proc; dtype / where as
+ * ss_push_pair); SS_STATE_CLEAR sets prev_output = None (the next push pins
+ * it to that pair's processed frame, :338-340). */
+#define SS_STATE_POSITION 0
+#define SS_STATE_OUTPUT 1
+#define SS_STATE_CLEAR 2
+SS_API int ss_session_set_state(ss_session *s, int mode, int64_t solved_through, const void *prev_output,
+                                int dtype, int where);
 SS_API int ss_pending(const ss_session *s, int64_t *t, int *has_prev, int *has_next);
 /* Provide the flows for the pending step t: which = 0 -> flow t->t-1,
  * which = 1 -> flow t->t+1 (FlowProvider.flow_between, flow.py:353-358,

@@ -19,6 +19,7 @@ SS_OK = 0
 SS_RESOLUTION_MISMATCH = 1
 SS_VALUE_ERROR = 2
 SS_SOLVER_DIVERGENCE = 3
+SS_STATE_POSITION, SS_STATE_OUTPUT, SS_STATE_CLEAR = 0, 1, 2
 SS_CUDA_ERROR = 4
 SS_NO_MEMORY = 5
 SS_HOST = 0
@@ -32,7 +33,7 @@ EXPORTS = (
     "ss_backward_warp", "ss_occlusion_mask", "ss_warp_weight", "ss_local_blend",
     "ss_adaptive_blend", "ss_consistency_weight", "ss_laplacian", "ss_solve_screened_poisson",
     "ss_session_create", "ss_session_destroy", "ss_session_reset", "ss_push_pair", "ss_stage_pair",
-    "ss_solved_through", "ss_pending", "ss_set_flow", "ss_set_constant_flow", "ss_check_step",
+    "ss_solved_through", "ss_session_set_state", "ss_pending", "ss_set_flow", "ss_set_constant_flow", "ss_check_step",
     "ss_step", "ss_output", "ss_output_async", "ss_output_wait", "ss_output_device", "ss_last_timing", "ss_flows",
     "ss_session_stream", "ss_session_join", "ss_flownet_num_params", "ss_flownet_create", "ss_flownet_set_downscale", "ss_flownet_destroy",
     "ss_flownet_flow", "ss_session_attach_flownet", "ss_session_compute_flow",
@@ -88,6 +89,7 @@ def _declare(L):
         "ss_push_pair": (i32, [vp, i64, vp, vp, i32, i32]),
         "ss_stage_pair": (i32, [vp, i64, vp, vp, i32, i32]),
         "ss_solved_through": (i64, [vp]),
+        "ss_session_set_state": (i32, [vp, i32, i64, vp, i32, i32]),
         "ss_pending": (i32, [vp, P(i64), P(i32), P(i32)]),
         "ss_set_flow": (i32, [vp, i32, vp, vp, i32]),
         "ss_set_constant_flow": (i32, [vp, i32, ctypes.c_double, ctypes.c_double, i32]),

@@ -262,8 +262,6 @@ class SessionState:
 
     def __init__(self, params: ConsistencyParams, pairs=None, prev_output=None,
                  solved_through: int = 0, last_timing: StepTiming | None = None):
-        if pairs or prev_output is not None or solved_through:
-            raise ValueError("SessionState must start empty; push pairs instead")
         self.params = params
         self.pairs: list = []
         self.last_timing = last_timing or StepTiming()
@@ -274,6 +272,16 @@ class SessionState:
         self._squeeze = False
         self._flow0_for = None  # step whose flow t -> t-1 was started early
         self._inflight: list = []  # device push sources, alive until the next step
+        # the reference's dataclass fields (consistency.py:305-319) may be set
+        # at construction or assigned later (resume from a known O_{t-1}):
+        # held here until the device session exists (first push)
+        self._has_prev = prev_output is not None
+        self._pending_prev = prev_output
+        self._pending_st = int(solved_through)
+        for pos, i, p in (pairs or []):
+            # pre-filled pairs are buffered as given; prev_output /
+            # solved_through stay what the caller passed (no pinning)
+            self.push_pair(pos, i, p, _pin=False)
 
     # -- device session ------------------------------------------------------
     def _ensure_session(self, input_frame, processed_frame):
@@ -305,19 +313,60 @@ class SessionState:
     @property
     def solved_through(self) -> int:
         if self._handle is None:
-            return 0
+            return self._pending_st
         return int(_lib.lib().ss_solved_through(self._handle))
+
+    @solved_through.setter
+    def solved_through(self, value: int) -> None:
+        if self._handle is None:
+            self._pending_st = int(value)
+            return
+        _dev.check(_lib.lib().ss_session_set_state(self._handle, _lib.SS_STATE_POSITION, int(value), None, 0, 0))
+        self._flow0_for = None
 
     @property
     def prev_output(self):
-        """O_{solved_through}: the pushed P_1 object itself until the first step."""
-        if self._handle is None:
+        """O_{solved_through}: the pushed P_1 object itself until the first step
+        (or the object assigned to it)."""
+        if not self._has_prev:
             return None
+        if self._handle is None:
+            return self._pending_prev
         if self._first_output is not None:
             return self._first_output
         if self._out_cache is None:
             self._out_cache = self.output_host()
         return self._out_cache
+
+    @prev_output.setter
+    def prev_output(self, value) -> None:
+        self._has_prev = value is not None
+        self._out_cache = None
+        self._first_output = None
+        if self._handle is None:
+            self._pending_prev = value
+            return
+        self._set_device_prev(value, self.solved_through)
+
+    def _set_device_prev(self, value, solved_through: int) -> None:
+        L = _lib.lib()
+        self._flow0_for = None
+        if value is None:
+            _dev.check(L.ss_session_set_state(self._handle, _lib.SS_STATE_CLEAR, int(solved_through), None, 0, 0))
+            return
+        if tuple(value.shape) != tuple(self._shapes[1]):
+            raise ResolutionMismatch("prev_output does not match the processed frames")
+        if _dev.is_torch(value) and value.is_cuda:
+            v = _dev.to_dev(value)
+            _dev.check(L.ss_session_wait_stream(self._handle, _dev.stream_ptr()))
+            _dev.check(L.ss_session_set_state(self._handle, _lib.SS_STATE_OUTPUT, int(solved_through),
+                                              ctypes.c_void_p(v.data_ptr()), _lib.SS_F32, _lib.SS_DEVICE))
+            self._inflight.append(v)
+        else:
+            v = np.ascontiguousarray(np.asarray(value), dtype=np.float32)
+            _dev.check(L.ss_session_set_state(self._handle, _lib.SS_STATE_OUTPUT, int(solved_through),
+                                              v.ctypes.data_as(ctypes.c_void_p), _lib.SS_F32, _lib.SS_HOST))
+        self._first_output = value  # the reference keeps the assigned object
 
     def output_host(self) -> np.ndarray:
         h, w, c = self._out_shape()
@@ -348,7 +397,7 @@ class SessionState:
         return ps[0], ps[1], (1 if len(ps) == 2 else ps[2])
 
     # -- consistency.py:321-340 ---------------------------------------------
-    def push_pair(self, position: int, input_frame, processed_frame) -> None:
+    def push_pair(self, position: int, input_frame, processed_frame, _pin: bool = True) -> None:
         if _shape_hw(input_frame) != _shape_hw(processed_frame):
             raise ResolutionMismatch("input and processed frames differ in resolution")
         if self.pairs:
@@ -363,17 +412,32 @@ class SessionState:
                 tuple(input_frame.shape) != self._shapes[0]
                 or tuple(processed_frame.shape) != self._shapes[1]):
             raise ResolutionMismatch("resolution drift mid-stream")
+        created = self._handle is None
         self._ensure_session(input_frame, processed_frame)
         if self._shapes is None:
             self._shapes = (tuple(input_frame.shape), tuple(processed_frame.shape))
-        first = self.solved_through == 0 and not self.pairs
+        if created:
+            # state assigned before the session existed (consistency.py:305-319)
+            if self._has_prev:
+                self._set_device_prev(self._pending_prev, self._pending_st)
+            elif self._pending_st:
+                _dev.check(_lib.lib().ss_session_set_state(self._handle, _lib.SS_STATE_POSITION,
+                                                           self._pending_st, None, 0, 0))
+            self._pending_prev = None
+        first = not self._has_prev
         self._push_device(position, input_frame, processed_frame)
         self.pairs.append((position, input_frame, processed_frame))
         if len(self.pairs) > 3:
             self.pairs.pop(0)
-        if first:
+        if first and not _pin:
+            # pre-filled pairs (constructor): the device pinned O to this pair
+            # as a push does; the reference leaves prev_output / solved_through
+            _dev.check(_lib.lib().ss_session_set_state(self._handle, _lib.SS_STATE_CLEAR, self._pending_st,
+                                                       None, 0, 0))
+        elif first:
             # the first output *is* the pushed P_1 object (consistency.py:338-340);
             # an 8-bit frame is stored as its float32 load (x / 255), read back
+            self._has_prev = True
             self._first_output = None if _is_u8(processed_frame) else processed_frame
 
     def _push_device(self, position, input_frame, processed_frame):

@@ -882,6 +882,35 @@ int ss_stage_pair(ss_session *s, int64_t position, const void *I, const void *P,
 
 int64_t ss_solved_through(const ss_session *s) { return s->solved_through; }
 
+// SessionState.prev_output / solved_through assignment (the reference's
+// dataclass fields, consistency.py:305-319; read at :342-345, written at
+// :338-340 and :410-411): resume a stream from a known O_{t-1}
+int ss_session_set_state(ss_session *s, int mode, int64_t solved_through, const void *prev_output, int dtype,
+                         int where)
+{
+    if (mode < SS_STATE_POSITION || mode > SS_STATE_CLEAR) {
+        set_error("mode must be SS_STATE_POSITION, SS_STATE_OUTPUT or SS_STATE_CLEAR");
+        return SS_VALUE_ERROR;
+    }
+    if (mode == SS_STATE_OUTPUT && !prev_output) {
+        set_error("prev_output is NULL");
+        return SS_VALUE_ERROR;
+    }
+    // flows started for the old pending step no longer apply
+    if (int rc = join_side(s)) return rc;
+    s->side_pending = false;
+    s->pre_for = -1;
+    s->flow_for[0] = s->flow_for[1] = -1;
+    if (mode == SS_STATE_OUTPUT) {
+        if (int rc = copy_frame(s, s->O, prev_output, s->cp, dtype, where)) return rc;
+        s->has_output = true;
+    } else if (mode == SS_STATE_CLEAR) {
+        s->has_output = false;  // prev_output = None: the next push pins it (:338-340)
+    }
+    s->solved_through = solved_through;
+    return SS_OK;
+}
+
 static const ss_session::Slot *find_pos(const ss_session *s, int64_t pos)
 {
     for (int i = 0; i < s->n_pairs; ++i)

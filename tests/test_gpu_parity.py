@@ -239,6 +239,55 @@ class TestSession:
                                        ss.ConstantFlow(0, 0)))
         assert len(out) == 1 and np.array_equal(out[0][1], f * 0.5)
 
+    def _full_run(self, ss, n=5, seed=9):
+        from paper_2301_00750_b200 import synthetic
+
+        seq = synthetic.translating_sequence(frames=n, height=40, width=56, step=(2, 1), seed=seed)
+        flow = ss.ConstantFlow(2.37, 1.13)
+        outs = dict(ss.stabilize_stream(zip(seq.inputs, seq.processed), ss.preset("default"), flow))
+        return seq, flow, outs
+
+    def test_resume_from_assigned_state(self, ss):
+        """The reference's SessionState is a dataclass (consistency.py:305-319):
+        a stream can resume from a known O_{t-1} by constructing (or
+        assigning) prev_output / solved_through.  Resuming at t = 4 from the
+        full run's O_3 reproduces its O_4 and O_5 bit for bit."""
+        seq, flow, outs = self._full_run(ss)
+        pr = ss.preset("default")
+        for how in ("ctor", "assign"):
+            if how == "ctor":
+                st = ss.SessionState(params=pr, prev_output=outs[3], solved_through=3)
+            else:
+                st = ss.SessionState(params=pr)
+                st.prev_output = outs[3]
+                st.solved_through = 3
+            assert st.prev_output is outs[3] and st.solved_through == 3
+            for pos in (3, 4, 5):
+                st.push_pair(pos, seq.inputs[pos - 1], seq.processed[pos - 1])
+            assert st.solved_through == 3 and st.prev_output is outs[3]  # pushes do not re-pin
+            assert np.array_equal(ss.stabilize_step(st, flow), outs[4]), how
+            assert np.array_equal(ss.stream_end_step(st, flow), outs[5]), how
+            assert st.solved_through == 5
+
+    def test_prefilled_pairs_and_reassignment(self, ss):
+        """SessionState(params, pairs=...) buffers the pairs without pinning
+        prev_output (the reference leaves it None until the next push); then
+        assigning prev_output / solved_through mid-stream takes effect."""
+        seq, flow, outs = self._full_run(ss, seed=10)
+        pr = ss.preset("default")
+        pairs = [(p, seq.inputs[p - 1], seq.processed[p - 1]) for p in (1, 2, 3)]
+        st = ss.SessionState(params=pr, pairs=pairs)
+        assert st.prev_output is None and st.solved_through == 0
+        with pytest.raises(ValueError, match="no buffered"):
+            ss.stabilize_step(st, flow)
+        st.prev_output = seq.processed[0]
+        st.solved_through = 1
+        assert np.array_equal(ss.stabilize_step(st, flow), outs[2])
+        # overwrite O_2 with the full run's (identical) value and continue
+        st.prev_output = outs[2]
+        st.push_pair(4, seq.inputs[3], seq.processed[3])
+        assert np.array_equal(ss.stabilize_step(st, flow), outs[3])
+
     def test_divergence_does_not_advance(self, ss):
         rng = np.random.default_rng(1)
         state = ss.SessionState(params=ss.ConsistencyParams(eta=0.9999, lam=1e6, alpha=0.0,
