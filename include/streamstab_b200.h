@@ -206,9 +206,11 @@ typedef struct ss_flownet ss_flownet;
 /* Number of float32 parameters the network expects (liteflownet.n_params). */
 SS_API int64_t ss_flownet_num_params(void);
 /* Upload weights (host float32, liteflownet.flatten_weights layout) to the
- * current device.  precision: SS_FLOW_FP32 (3xTF32 on tcgen05 tensor cores:
- * fp32-class accuracy) or SS_FLOW_BF16 (tcgen05, bf16 operands, fp32
- * accumulation). */
+ * current device.  precision: SS_FLOW_FP32 (fp32-class products on tcgen05
+ * tensor cores: split-bf16 -- x = hi + lo in bf16, three products, fp32
+ * accumulation -- on the 3x3 stride-1 layers, 3xTF32 on the others;
+ * SS_FP32_IMPL=tf32x3 selects 3xTF32 everywhere) or SS_FLOW_BF16 (tcgen05,
+ * bf16 operands, fp32 accumulation). */
 enum ss_flow_precision { SS_FLOW_FP32 = 0, SS_FLOW_BF16 = 1 };
 SS_API int ss_flownet_create(const float *weights, int64_t n, int precision, ss_flownet **out);
 /* Provider downscale (replaces FlowOptions.downscale, flow.py:34, :183-188,

@@ -1210,7 +1210,11 @@ int ss_flows(const ss_session *s, int which, float *uv_dst, uint8_t *valid_dst, 
 // fp32 -> 3xTF32 on tcgen05 (fp32-class accuracy); bf16 -> bf16 tcgen05
 static int conv_mode_for(int precision)
 {
-    return precision == SS_FLOW_BF16 ? fn::CONV_TC_BF16 : fn::CONV_TC_TF32X3;
+    if (precision == SS_FLOW_BF16) return fn::CONV_TC_BF16;
+    // the fp32-class path: split-bf16 on the 3x3 stride-1 layers, 3xTF32 on the
+    // others (flownet.cu); SS_FP32_IMPL=tf32x3 runs every layer in 3xTF32
+    static const bool tf32 = getenv("SS_FP32_IMPL") && !strcmp(getenv("SS_FP32_IMPL"), "tf32x3");
+    return tf32 ? fn::CONV_TC_TF32X3 : fn::CONV_TC_BF16X2;
 }
 
 int64_t ss_flownet_num_params(void) { return fn::Weights::expected_params(); }

@@ -65,6 +65,7 @@ Weights::~Weights()
     cudaFree(block);
     cudaFree(tma_block);
     cudaFree(bf_block);
+    cudaFree(bs_block);
 }
 
 int Weights::expected_params()
@@ -214,6 +215,55 @@ int Weights::upload(const float *host, int64_t n)
         l.tma_T_bf = tma_taps_per_stage(l.k, l.stride, l.dil, l.cin, np, 0);
         const int kblocks = l.k * l.k * ((l.cin + 31) / 32);
         if (int rc = encode_weight_map_bf16(&l.tmB_bf, l.wt_bf, kblocks, l.cout_pad, np, l.tma_T_bf)) return rc;
+    }
+
+    // split-bf16 path: [kblocks][parts][hi np rows; lo np rows][32] bf16,
+    // hi = rn(w), lo = rn(w - hi) (the fp32 path's [hi; lo] arrangement)
+    auto bf16_rn = [](float f) {
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+    };
+    auto bf16_f = [](uint16_t b) {
+        const uint32_t u = (uint32_t)b << 16;
+        float f;
+        std::memcpy(&f, &u, 4);
+        return f;
+    };
+    std::vector<uint16_t> bsh(bt_total * 2, 0);
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        const int taps = l.k * l.k, N = l.cout_pad;
+        const int parts = (N + 127) / 128, np = N / parts;
+        const float *wl = dev.data() + woff[i];
+        uint16_t *dst = bsh.data() + 2 * obt[i];
+        for (int tap = 0; tap < taps; ++tap)
+            for (int c = 0; c < l.cin; ++c) {
+                const size_t kb = (size_t)(c / 32) * taps + tap;
+                for (int n = 0; n < l.cout; ++n) {
+                    const float f = wl[(size_t)(tap * l.cin + c) * N + n];
+                    const uint16_t hb = bf16_rn(f);
+                    const int part = n / np, nn = n - part * np;
+                    const size_t row = (size_t)part * 2 * np + nn;
+                    dst[(kb * 2 * N + row) * 32 + c % 32] = hb;
+                    dst[(kb * 2 * N + row + np) * 32 + c % 32] = bf16_rn(f - bf16_f(hb));
+                }
+            }
+    }
+    cudaFree(bs_block);
+    bs_block = nullptr;
+    SS_CUDA_TRY(cudaMalloc(&bs_block, bsh.size() * sizeof(uint16_t)));
+    SS_CUDA_TRY(cudaMemcpy(bs_block, bsh.data(), bsh.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    for (size_t i = 0; i < layers.size(); ++i) {
+        auto &l = layers[i];
+        if (l.dw) continue;
+        const int parts = (l.cout_pad + 127) / 128, np = l.cout_pad / parts;
+        l.wt_bs = static_cast<uint16_t *>(bs_block) + 2 * obt[i];
+        l.tma_T_bs = tma_taps_per_stage(l.k, l.stride, l.dil, l.cin, np, 2);
+        const int kblocks = l.k * l.k * ((l.cin + 31) / 32);
+        if (int rc = encode_weight_map_bf16_rows(&l.tmB_bs, l.wt_bs, kblocks, 2 * l.cout_pad, 2 * np, l.tma_T_bs))
+            return rc;
     }
     return SS_OK;
 }
@@ -394,11 +444,16 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
     p.Ho = (Hi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.Wo = (Wi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.act = L.act;
-    const bool bf = conv_mode_ == CONV_TC_BF16;
-    p.tmB = bf ? &L.tmB_bf : &L.tmB;
+    // split-bf16 serves the 3x3 stride-1 layers (halo tiles: K = 16 per MMA
+    // halves their MMA count); the stride-2 (im2col / phase) and 1x1 layers
+    // keep 3xTF32, whose in-place hi / lo conversion is cheaper there
+    // (measured per layer at 1080p: pyr3a 24.6 vs 38.8 us, ref*_pw 22.5 vs 28.8 us)
+    const bool split_ok = L.k == 3 && L.stride == 1;
+    const int prec = conv_mode_ == CONV_TC_BF16 ? 0 : (conv_mode_ == CONV_TC_BF16X2 && split_ok ? 2 : 1);
+    p.tmB = prec == 0 ? &L.tmB_bf : (prec == 2 ? &L.tmB_bs : &L.tmB);
     p.grid_cap = grid_cap_;
-    p.tma_T = bf ? L.tma_T_bf : L.tma_T;
-    return launch_conv_tma(p, bf ? 0 : 1, st);
+    p.tma_T = prec == 0 ? L.tma_T_bf : (prec == 2 ? L.tma_T_bs : L.tma_T);
+    return launch_conv_tma(p, prec, st);
 }
 
 // capture fn(st) into a graph (thread-local capture mode) and instantiate it

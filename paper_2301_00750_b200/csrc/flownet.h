@@ -62,7 +62,7 @@ struct ConvParams {
     int tma_T = 1;              // taps per weight stage of that map
 };
 
-enum ConvMode { CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2 };
+enum ConvMode { CONV_TC_BF16 = 1, CONV_TC_TF32X3 = 2, CONV_TC_BF16X2 = 3 };
 
 // kind 0: bf16 operands (kind::f16); kind 1: 3xTF32 (kind::tf32)
 // TMA-fed warp-specialised 3xTF32 conv (flownet_tma.cu)
@@ -73,6 +73,7 @@ int prepare_flow_kernels();
 int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, int np, int T);
 int tma_taps_per_stage(int k, int stride, int dil, int cin, int np, int prec);
 int encode_weight_map_bf16(CUtensorMap *m, const void *wt, int kblocks, int rows, int np, int T);
+int encode_weight_map_bf16_rows(CUtensorMap *m, const void *wt, int kblocks, int rows, int box_rows, int T);
 int launch_splitk_reduce(const float *ws, int splits, int M, int N, int Cout, const float *bias,
                          int act, float *out, int out_ld, cudaStream_t st, int parts = 1);
 int launch_depthwise(const float *in, int ld_in, int H, int W, int C, const float *w, int dil,
@@ -105,6 +106,10 @@ struct LayerDev {
     const void *wt_bf = nullptr;
     int tma_T_bf = 1;
     alignas(64) CUtensorMap tmB_bf;
+    // split-bf16 path: [kblock][part][hi np rows; lo np rows][32 channels] bf16
+    const void *wt_bs = nullptr;
+    int tma_T_bs = 1;
+    alignas(64) CUtensorMap tmB_bs;
 };
 
 // Weights on one device, in liteflownet.layer_table() order.
@@ -113,6 +118,7 @@ struct Weights {
     float *block = nullptr;
     float *tma_block = nullptr;
     void *bf_block = nullptr;
+    void *bs_block = nullptr;
     ~Weights();
     static int expected_params();
     int upload(const float *host, int64_t n);

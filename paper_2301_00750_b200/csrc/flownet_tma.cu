@@ -154,6 +154,21 @@ __device__ __forceinline__ void mma_step_bf16(uint32_t d, uint64_t a_, uint64_t 
         : "memory");
 }
 
+// one K = 16 step of split-bf16 (PREC 2): a_hi x [w_hi; w_lo] (N = 2 np) and
+// a_lo x w_hi (N = np, accumulating into the first np columns), elected lane
+__device__ __forceinline__ void mma_step_bf16x2(uint32_t d, uint64_t ah, uint64_t al, uint64_t b, uint32_t id2,
+                                                uint32_t id1, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %6, 1;\n\t}" ::"r"(d),
+        "l"(ah), "l"(al), "l"(b), "r"(acc), "r"(id2), "r"(id1)
+        : "memory");
+}
+
 // physical 16-byte chunk of logical chunk c in row r of a swizzled tile with
 // rows of rb bytes (SWIZZLE_{128,64,32}B; the tile base is 1024-aligned)
 __device__ __forceinline__ int swz_chunk(int c, int r, int rb)
@@ -168,6 +183,10 @@ __device__ __forceinline__ bool a_event(int st, int kb, int grp)
     return AMODE == 0 || st == kb || grp == 0;
 }
 
+// PREC 2: split-bf16 (fp32-class): a = a_hi + a_lo, w = w_hi + w_lo with
+// bf16 terms (hi = round-to-nearest, lo = the rounded remainder, ~16
+// significant bits each side), D = a_hi w_hi + a_hi w_lo + a_lo w_hi in fp32
+// -- the 3xTF32 scheme on kind::f16, K = 16 per MMA at the bf16 rate;
 // PREC 1: 3xTF32 (fp32-class); PREC 0: bf16 operands (converted from the fp32
 // activations in shared memory, kind::f16), fp32 accumulation
 template <int PREC, int AMODE, bool BRES>
@@ -298,10 +317,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         const uint32_t id2 = idesc(2u, 128u, (uint32_t)(2 * np)), id1 = idesc(2u, 128u, (uint32_t)np);
         const uint32_t idb = idesc(1u, 128u, (uint32_t)np);
         // bf16 operand rows are half as wide as the fp32 rows they come from
-        const uint32_t arb = PREC ? rowb : rowb / 2;
+        const uint32_t arb = PREC == 1 ? rowb : rowb / 2;
         const uint32_t alay = arb == 128 ? 2u : (arb == 64 ? 4u : 6u);
         const uint32_t sbo = (AMODE == 0 ? 8u : (uint32_t)a.halo_w) * arb;
-        const uint32_t bstride = PREC ? (uint32_t)(2 * np * 128) : (uint32_t)(np * 64);
+        const uint32_t bstride = PREC == 1 ? (uint32_t)(2 * np * 128) : (uint32_t)((PREC == 2 ? 2 : 1) * np * 64);
+        const uint32_t idh2 = idesc(1u, 128u, (uint32_t)(2 * np)), idh1 = idb;  // split-bf16 shapes
         if (BRES) mbar_wait(&b_full[0], 0);
         uint32_t ga = 0, gb = 0, uc = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
@@ -324,7 +344,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 tc_fence_after();
                 const int tap0 = grp * a.T, nt = min(a.T, a.taps - tap0);
                 const int live = min(a.cpp, a.cin - cb * a.cpp);
-                const int nks = PREC ? (live + 7) >> 3 : (live + 15) >> 4;
+                const int nks = PREC == 1 ? (live + 7) >> 3 : (live + 15) >> 4;
                 const uint32_t araw = smem_u32(aslots + sa * 2 * a.a_slot);
                 const uint32_t b0 = smem_u32(bst + s * a.b_stage);
                 int ky = tap0 / a.k, kx = tap0 - ky * a.k;
@@ -333,11 +353,19 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     if (AMODE == 1)
                         off = (uint32_t)((ky * a.halo_w + kx) * a.dil) * arb;
                     else if (AMODE == 2)
-                        off = (uint32_t)(((ky & 1) * 2 + (kx & 1)) * (PREC ? a.ph_bytes : a.ph_bytes / 2)) +
+                        off = (uint32_t)(((ky & 1) * 2 + (kx & 1)) * (PREC == 1 ? a.ph_bytes : a.ph_bytes / 2)) +
                               (uint32_t)((ky >> 1) * a.halo_w + (kx >> 1)) * arb;
                     // B rows hold 32 channels: a narrow A row (cpp < 32) only
                     // ever meets channel block 0, whose first cpp channels align
-                    if (PREC) {
+                    if (PREC == 2) {
+                        // hi / lo bf16 copies in the second half of the slot
+                        const uint64_t ah = sdesc_sw(araw + a.a_slot + off, sbo, alay);
+                        const uint64_t al = sdesc_sw(araw + a.a_slot + a.a_slot / 2 + off, sbo, alay);
+                        const uint64_t bd = sdesc_sw(b0 + j * bstride, 512u, 4u);  // 64-byte rows
+                        for (int i = 0; i < nks; ++i)  // K = 16 bf16 = 32 bytes per MMA
+                            mma_step_bf16x2(d, ah + 2 * i, al + 2 * i, bd + 2 * i, idh2, idh1,
+                                            (st > kb || j > 0 || i > 0) ? 1u : 0u);
+                    } else if (PREC) {
                         const uint64_t ah = sdesc_sw(araw + off, sbo, alay);
                         const uint64_t al = sdesc_sw(araw + a.a_slot + off, sbo, alay);
                         const uint64_t bd = sdesc_sw128(b0 + j * bstride);
@@ -457,7 +485,30 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 if (ga < 9 && t == 0) trace_at(a, 12 + 4 * ga + 1);
                 ++ga;
                 float4 *ar = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot);
-                if (PREC) {
+                if (PREC == 2) {
+                    // fp32 row r -> bf16 hi / lo rows (rowb / 2 bytes, swizzled for
+                    // that width): hi = rn(v), lo = rn(v - hi)
+                    uint8_t *bh = aslots + sa * 2 * a.a_slot + a.a_slot, *bl = bh + a.a_slot / 2;
+                    const int rb = (int)rowb, rb2 = rb / 2, cpr = rb / 16;
+                    for (int j = t; j < n16; j += 128) {
+                        const int r = j / cpr, pc = j - r * cpr;
+                        const int lc = swz_chunk(pc, r, rb);
+                        const float4 v = ar[j];
+                        const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y), h23 = __floats2bfloat162_rn(v.z, v.w);
+                        const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+                        const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - f01.x, v.y - f01.y),
+                                             l23 = __floats2bfloat162_rn(v.z - f23.x, v.w - f23.y);
+                        uint2 qh, ql;
+                        qh.x = *reinterpret_cast<const uint32_t *>(&h01);
+                        qh.y = *reinterpret_cast<const uint32_t *>(&h23);
+                        ql.x = *reinterpret_cast<const uint32_t *>(&l01);
+                        ql.y = *reinterpret_cast<const uint32_t *>(&l23);
+                        const int bc = swz_chunk(lc >> 1, r, rb2);
+                        const int o = r * rb2 + bc * 16 + (lc & 1) * 8;
+                        *reinterpret_cast<uint2 *>(bh + o) = qh;
+                        *reinterpret_cast<uint2 *>(bl + o) = ql;
+                    }
+                } else if (PREC) {
                     float4 *lo = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot + a.a_slot);
                     for (int j = t; j < n16; j += 128) {
                         const float4 v = ar[j];
@@ -590,7 +641,7 @@ static int amode_for(int k, int stride, int dil, int cin)
 int tma_taps_per_stage(int k, int stride, int dil, int cin, int np, int prec)
 {
     if (amode_for(k, stride, dil, cin) == 0) return 1;  // im2col: one tap per stage
-    const int tap_bytes = prec ? 2 * np * 128 : np * 64;
+    const int tap_bytes = prec == 1 ? 2 * np * 128 : (prec == 2 ? 2 : 1) * np * 64;
     return std::max(1, std::min(k * k, 36864 / tap_bytes));
 }
 
@@ -598,6 +649,13 @@ int tma_taps_per_stage(int k, int stride, int dil, int cin, int np, int prec)
 // rows, SWIZZLE_64B): per stage one box of 32 K x np rows x T kblocks
 int encode_weight_map_bf16(CUtensorMap *m, const void *wt, int kblocks, int rows, int np, int T)
 {
+    return encode_weight_map_bf16_rows(m, wt, kblocks, rows, np, T);
+}
+
+// box of 32 K x box_rows x T kblocks over [kblocks][rows][32] bf16
+int encode_weight_map_bf16_rows(CUtensorMap *m, const void *wt, int kblocks, int rows, int box_rows, int T)
+{
+    const int np = box_rows;
     auto fn = tiled_fn();
     if (!fn) {
         set_error("cuTensorMapEncodeTiled unavailable");
@@ -664,13 +722,16 @@ using ConvKernel = void (*)(CUtensorMap, CUtensorMap, ConvArgs);
 
 static ConvKernel conv_kernel(int prec, int amode, bool res)
 {
-    static const ConvKernel tab[2][3][2] = {
+    static const ConvKernel tab[3][3][2] = {
         {{k_conv_tc3<0, 0, false>, k_conv_tc3<0, 0, true>},
          {k_conv_tc3<0, 1, false>, k_conv_tc3<0, 1, true>},
          {k_conv_tc3<0, 2, false>, k_conv_tc3<0, 2, true>}},
         {{k_conv_tc3<1, 0, false>, k_conv_tc3<1, 0, true>},
          {k_conv_tc3<1, 1, false>, k_conv_tc3<1, 1, true>},
-         {k_conv_tc3<1, 2, false>, k_conv_tc3<1, 2, true>}}};
+         {k_conv_tc3<1, 2, false>, k_conv_tc3<1, 2, true>}},
+        {{k_conv_tc3<2, 0, false>, k_conv_tc3<2, 0, true>},
+         {k_conv_tc3<2, 1, false>, k_conv_tc3<2, 1, true>},
+         {k_conv_tc3<2, 2, false>, k_conv_tc3<2, 2, true>}}};
     return tab[prec][amode][res ? 1 : 0];
 }
 
@@ -679,7 +740,7 @@ int prepare_conv_tma()
     static bool done = false;
     if (done) return SS_OK;
     if (int rc = prepare_flow_kernels()) return rc;
-    for (int prec = 0; prec < 2; ++prec)
+    for (int prec = 0; prec < 3; ++prec)
         for (int am = 0; am < 3; ++am)
             for (int res = 0; res < 2; ++res)
                 SS_CUDA_TRY(cudaFuncSetAttribute(conv_kernel(prec, am, res != 0),
@@ -746,7 +807,8 @@ static int launch_parts(const ConvParams &p, const CUtensorMap &tmA, int prec, i
     a.out_ld = p.out_ld;
     a.bias = p.bias;
     a.out = p.out;
-    a.b_stage = prec ? a.T * 2 * np * 128 : a.T * np * 64;  // [hi; lo] fp32 rows | bf16 rows
+    // [hi; lo] fp32 rows | [hi; lo] bf16 rows | bf16 rows
+    a.b_stage = prec == 1 ? a.T * 2 * np * 128 : a.T * (prec == 2 ? 2 : 1) * np * 64;
     const int bar_bytes = 1024 + 512;
     // weights resident for the whole launch when every stage fits
     static const bool res_on = getenv("SS_CONV_BRES") == nullptr || strcmp(getenv("SS_CONV_BRES"), "0");
@@ -855,7 +917,7 @@ int launch_conv_tma(const ConvParams &p, int prec, cudaStream_t st)
     }
     static const bool wide = getenv("SS_CONV_CPP32") != nullptr;
     // bf16: a K = 16 MMA needs >= 16 channels per row
-    const int cmin = prec ? 8 : 16;
+    const int cmin = prec == 1 ? 8 : 16;
     const int cpp = (wide && amode != 2) ? 32 : std::max(cmin, p.Cin <= 8 ? 8 : (p.Cin <= 16 ? 16 : 32));
     const int halo_w = HT_W + 2 * p.pad, halo_h = HT_H + 2 * p.pad;
     alignas(64) CUtensorMap tmA;

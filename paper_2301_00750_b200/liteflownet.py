@@ -170,8 +170,10 @@ class LiteFlowNet:
     straight into the session's HBM flow slots and caches each ring frame's
     feature pyramid, so a step computes one new pyramid and two estimator
     passes.  ``flow_between`` is the stateless form (FlowField out).
-    precision: "fp32" (3xTF32 on tcgen05: fp32-class accuracy) or "bf16"
-    (bf16 operands on tcgen05, fp32 accumulation).
+    precision: "fp32" (fp32-class products on tcgen05: split-bf16 -- each
+    operand as hi + lo bf16, three products, fp32 accumulation -- on the 3x3
+    stride-1 layers, 3xTF32 on the stride-2 and 1x1 ones) or "bf16" (bf16
+    operands on tcgen05, fp32 accumulation).
     downscale: FlowOptions.downscale semantics (flow.py:34, :183-188) -- the
     network runs on ``box_downscale(frame, d)`` and the flow is
     ``resize_bilinear``'d back times d; callers pass the preset's
