@@ -374,9 +374,9 @@ class Env:
 
 
 FLOW_DESC = {"fp32": "lite flow CNN, fp32-class tcgen05 convs (split-bf16: operands as hi + lo bf16, 3 products, "
-                     "fp32 accumulation, on the 3x3 stride-1 layers; 3xTF32 on the stride-2 / 1x1 ones), fp32 "
-                     "activations, random-init seeded weights; 1080p flow EPE vs the float64 CPU restatement: "
-                     "max 4.2e-4 px, mean 9.3e-5 px",
+                     "fp32 accumulation, on the 3x3 halo-tile layers; 3xTF32 on the im2col stride-2 / 1x1 ones), "
+                     "fp32 activations, random-init seeded weights; 1080p flow EPE vs the float64 CPU restatement: "
+                     "max 4.3e-4 px, mean 9.5e-5 px",
              "bf16": "lite flow CNN, bf16 tcgen05 convs, random-init seeded weights",
              "dis": "reference built-in DIS flow (BuiltinFlow, FlowOptions()) on GPU, "
                     "bit-identical to flow.py (tests/test_gpu_fullsize.py)",

@@ -444,11 +444,12 @@ static int conv(const LayerDev &L, const float *in, int in_ld, int Hi, int Wi, f
     p.Ho = (Hi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.Wo = (Wi + 2 * p.pad - L.dil * (L.k - 1) - 1) / L.stride + 1;
     p.act = L.act;
-    // split-bf16 serves the 3x3 stride-1 layers (halo tiles: K = 16 per MMA
-    // halves their MMA count); the stride-2 (im2col / phase) and 1x1 layers
-    // keep 3xTF32, whose in-place hi / lo conversion is cheaper there
-    // (measured per layer at 1080p: pyr3a 24.6 vs 38.8 us, ref*_pw 22.5 vs 28.8 us)
-    const bool split_ok = L.k == 3 && L.stride == 1;
+    // split-bf16 serves the 3x3 layers with halo tiles (stride 1, and the
+    // stride-2 phase tiles of <= 16 input channels): K = 16 per MMA halves
+    // their MMA count; the im2col stride-2 and the 1x1 layers keep 3xTF32,
+    // whose in-place hi / lo conversion is cheaper there (1080p, 8 converter
+    // warps: pyr3a 22.5 vs 30.5 us, ref*_pw ~21 vs ~25 us; pyr2a 33.0 vs 30.7)
+    const bool split_ok = L.k == 3 && (L.stride == 1 || L.cin <= 16);
     const int prec = conv_mode_ == CONV_TC_BF16 ? 0 : (conv_mode_ == CONV_TC_BF16X2 && split_ok ? 2 : 1);
     p.tmB = prec == 0 ? &L.tmB_bf : (prec == 2 ? &L.tmB_bs : &L.tmB);
     p.grid_cap = grid_cap_;

@@ -26,7 +26,7 @@
 // (T taps per stage for narrow layers, so a stage carries enough MMA work).
 //
 // Warp roles (persistent CTAs, one per SM, walking (tile, K-split) units):
-//   warp 0      TMA producer          warps 6-9  converters (A -> hi, lo)
+//   warp 0      TMA producer          warps 6-13 converters (A -> hi, lo)
 //   warp 1      MMA issuer            warps 2-5  epilogue (TMEM -> bias, act,
 //                                                 fp32 NHWC or split-K partials)
 // TMEM holds two accumulators, so the epilogue of a unit overlaps the MMAs of
@@ -60,7 +60,13 @@ using namespace tc;
 
 namespace {
 
-constexpr int TM_THREADS = 320;
+// converter warps (6 .. 6 + NCONV - 1): 8 measured best for the split-bf16
+// conversion (4: 388, 8: 401, 12: 399, 16: 398 frames/s at 1080p)
+#ifndef SS_CONV_NCONV
+#define SS_CONV_NCONV 8
+#endif
+constexpr int NCONV = SS_CONV_NCONV;
+constexpr int TM_THREADS = 32 * (6 + NCONV);
 constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA
 constexpr int HT_H = 16, HT_W = 8;  // halo-mode output tile (rows x columns)
 
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < NA; ++i) {
             mbar_init(&a_full[i], 1);
-            mbar_init(&a_conv[i], 4);
+            mbar_init(&a_conv[i], NCONV);
             mbar_init(&a_empty[i], 1);
         }
         for (int s = 0; s < S; ++s) {
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     // that width): hi = rn(v), lo = rn(v - hi)
                     uint8_t *bh = aslots + sa * 2 * a.a_slot + a.a_slot, *bl = bh + a.a_slot / 2;
                     const int rb = (int)rowb, rb2 = rb / 2, cpr = rb / 16;
-                    for (int j = t; j < n16; j += 128) {
+                    for (int j = t; j < n16; j += 32 * NCONV) {
                         const int r = j / cpr, pc = j - r * cpr;
                         const int lc = swz_chunk(pc, r, rb);
                         const float4 v = ar[j];
@@ -510,7 +516,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     }
                 } else if (PREC) {
                     float4 *lo = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot + a.a_slot);
-                    for (int j = t; j < n16; j += 128) {
+                    for (int j = t; j < n16; j += 32 * NCONV) {
                         const float4 v = ar[j];
                         const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
 #if !SS_TF32_HW_TRUNCATES
@@ -523,7 +529,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     // bytes, swizzled for that width) in the second half of the slot
                     uint8_t *bf = aslots + sa * 2 * a.a_slot + a.a_slot;
                     const int rb = (int)rowb, rb2 = rb / 2, cpr = rb / 16;
-                    for (int j = t; j < n16; j += 128) {
+                    for (int j = t; j < n16; j += 32 * NCONV) {
                         const int r = j / cpr, pc = j - r * cpr;
                         const int lc = swz_chunk(pc, r, rb);  // logical chunk: channels 4 lc .. 4 lc + 3
                         const float4 v = ar[j];
