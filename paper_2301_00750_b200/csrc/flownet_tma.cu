@@ -42,6 +42,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "flownet.h"
 #include "ss_common.cuh"
@@ -706,7 +707,7 @@ int encode_weight_map(CUtensorMap *m, const float *wt, int kblocks, int rows, in
 
 // SS_CONV_TRACE=1 (diagnostics): every conv launch stamps CTA 0's milestones
 // (globaltimer) into a mapped host ring; conv_trace_dump prints them
-static unsigned long long *trace_host = nullptr, *trace_dev = nullptr;
+static unsigned long long *trace_dev = nullptr;  // device ring (stamps stay off the PCIe path)
 static int trace_n = 0;
 constexpr int TRACE_SLOTS = 128, TRACE_K = 48;  // 12 milestones + 4 per unit for 9 units
 static unsigned long long *conv_trace_slot()
@@ -716,10 +717,9 @@ static unsigned long long *conv_trace_slot()
 #endif
     static const bool on = getenv("SS_CONV_TRACE") != nullptr;
     if (!on) return nullptr;
-    if (!trace_host) {
-        if (cudaHostAlloc(&trace_host, TRACE_SLOTS * TRACE_K * 8, cudaHostAllocMapped) != cudaSuccess) return nullptr;
-        memset(trace_host, 0, TRACE_SLOTS * TRACE_K * 8);
-        cudaHostGetDevicePointer(&trace_dev, trace_host, 0);
+    if (!trace_dev) {
+        if (cudaMalloc(&trace_dev, TRACE_SLOTS * TRACE_K * 8) != cudaSuccess) return nullptr;
+        cudaMemset(trace_dev, 0, TRACE_SLOTS * TRACE_K * 8);
     }
     return trace_dev + (size_t)(trace_n++ % TRACE_SLOTS) * TRACE_K;
 }
@@ -886,10 +886,13 @@ static int launch_parts(const ConvParams &p, const CUtensorMap &tmA, int prec, i
 
 void conv_trace_dump(const char *what)
 {
-    if (!trace_host || !trace_n) return;
+    if (!trace_dev || !trace_n) return;
     cudaDeviceSynchronize();
+    std::vector<unsigned long long> hst((size_t)TRACE_SLOTS * TRACE_K);
+    cudaMemcpy(hst.data(), trace_dev, hst.size() * 8, cudaMemcpyDeviceToHost);
+    const unsigned long long *trace_host = hst.data();
     static const char *names[12] = {"entry", "setup", "pdl_ok", "A_land", "A_conv", "mma_go",
-                                         "mma_done", "epi_go", "epi_done", "exit", "epi_ld1", "epi_loop"};
+                                    "mma_done", "epi_go", "epi_done", "exit", "epi_ld1", "epi_loop"};
     for (int i = 0; i < trace_n && i < TRACE_SLOTS; ++i) {
         const unsigned long long *t = trace_host + (size_t)i * TRACE_K;
         fprintf(stderr, "[conv-trace] %s #%d", what, i);
@@ -902,7 +905,7 @@ void conv_trace_dump(const char *what)
                     t[14 + 4 * u] ? (double)(t[14 + 4 * u] - t[0]) * 1e-3 : -1.0,
                     t[15 + 4 * u] ? (double)(t[15 + 4 * u] - t[0]) * 1e-3 : -1.0);
     }
-    memset(trace_host, 0, TRACE_SLOTS * TRACE_K * 8);
+    cudaMemset(trace_dev, 0, TRACE_SLOTS * TRACE_K * 8);
     trace_n = 0;
 }
 
