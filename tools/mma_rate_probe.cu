@@ -107,8 +107,14 @@ __global__ void probe_conv(int np, int rowb, int reps, int vary, int sep, long l
             const uint64_t ah = desc(smem_u32(ahi) + off, 10 * rowb, lay), al = desc(smem_u32(alo) + off, 10 * rowb, lay);
             const uint64_t bd = desc(smem_u32(bs) + tap * 4096, 1024, 2);
             mma_tf32(tmem, ah, bd, id2, r > 0 ? 1u : 0u);
-            // sep: the a_lo product into its own columns [2 np, 3 np) (summed later)
-            mma_tf32(sep ? tmem + 2 * np : tmem, al, bd, id1, (sep && r == 0) ? 0u : 1u);
+            // sep 1: the a_lo product into its own columns [2 np, 3 np) (summed later)
+            // sep 3: same shape (N = 2 np) into the same columns; 4: same shape, own columns
+            if (sep == 3)
+                mma_tf32(tmem, al, bd, id2, 1u);
+            else if (sep == 4)
+                mma_tf32(tmem + 2 * np, al, bd, id2, r == 0 ? 0u : 1u);
+            else
+                mma_tf32(sep ? tmem + 2 * np : tmem, al, bd, id1, (sep && r == 0) ? 0u : 1u);
         }
         mma_commit(&mbar);
         mbar_wait(&mbar, 0);
@@ -141,18 +147,19 @@ int main()
             }
     cudaFuncSetAttribute(probe_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     printf("conv pattern: per K step MMA(N = 2 np, a_hi) + MMA(N = np, a_lo)\n");
+    for (int rowb : {64})
     for (int np : {16, 32, 64})
-        for (int sep : {0, 2})
+        for (int sep : {0, 1, 2, 3, 4})
         for (int vary : {0, 1}) {
-            probe_conv<<<1, 128, 80 * 1024>>>(np, 64, reps, vary, sep, d);
+            probe_conv<<<1, 128, 80 * 1024>>>(np, rowb, reps, vary, sep, d);
             if (cudaDeviceSynchronize() != cudaSuccess) {
                 printf("error conv np=%d\n", np);
                 return 1;
             }
             long long c;
             cudaMemcpy(&c, d, sizeof c, cudaMemcpyDeviceToHost);
-            printf("np=%3d %s descriptors %s: %6.1f clk per K step (2 MMAs)\n", np,
-                   sep == 2 ? "grouped     " : (sep ? "separate acc" : "interleaved "), vary ? "varying" : "fixed  ", (double)c / reps);
+            printf("rowb=%3d np=%3d %s descriptors %s: %6.1f clk per K step (2 MMAs)\n", rowb, np,
+                   sep == 2 ? "grouped     " : sep == 1 ? "separate acc" : sep == 3 ? "same shape  " : sep == 4 ? "same+sepacc " : "interleaved ", vary ? "varying" : "fixed  ", (double)c / reps);
         }
     return 0;
 }
