@@ -494,26 +494,30 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 float4 *ar = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot);
                 if (PREC == 2) {
                     // fp32 row r -> bf16 hi / lo rows (rowb / 2 bytes, swizzled for
-                    // that width): hi = rn(v), lo = rn(v - hi)
+                    // that width): hi = rn(v), lo = rn(v - hi).  One thread per
+                    // 16-byte bf16 chunk (8 channels = two fp32 chunks): two
+                    // LDS.128, two STS.128
                     uint8_t *bh = aslots + sa * 2 * a.a_slot + a.a_slot, *bl = bh + a.a_slot / 2;
-                    const int rb = (int)rowb, rb2 = rb / 2, cpr = rb / 16;
-                    for (int j = t; j < n16; j += 32 * NCONV) {
-                        const int r = j / cpr, pc = j - r * cpr;
-                        const int lc = swz_chunk(pc, r, rb);
-                        const float4 v = ar[j];
-                        const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y), h23 = __floats2bfloat162_rn(v.z, v.w);
-                        const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
-                        const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - f01.x, v.y - f01.y),
-                                             l23 = __floats2bfloat162_rn(v.z - f23.x, v.w - f23.y);
-                        uint2 qh, ql;
-                        qh.x = *reinterpret_cast<const uint32_t *>(&h01);
-                        qh.y = *reinterpret_cast<const uint32_t *>(&h23);
-                        ql.x = *reinterpret_cast<const uint32_t *>(&l01);
-                        ql.y = *reinterpret_cast<const uint32_t *>(&l23);
-                        const int bc = swz_chunk(lc >> 1, r, rb2);
-                        const int o = r * rb2 + bc * 16 + (lc & 1) * 8;
-                        *reinterpret_cast<uint2 *>(bh + o) = qh;
-                        *reinterpret_cast<uint2 *>(bl + o) = ql;
+                    const int rb = (int)rowb, rb2 = rb / 2;
+                    const int sh = rb2 == 64 ? 2 : 1;  // log2(bf16 chunks per row): rb2 is 64 or 32
+                    const int n8 = n16 / 2;
+                    for (int q = t; q < n8; q += 32 * NCONV) {
+                        const int r = q >> sh, k = q & ((1 << sh) - 1);
+                        const float4 v0 = ar[r * (2 << sh) + swz_chunk(2 * k, r, rb)];
+                        const float4 v1 = ar[r * (2 << sh) + swz_chunk(2 * k + 1, r, rb)];
+                        const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                        uint32_t hw[4], lw[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+                            const float2 hf = __bfloat1622float2(h);
+                            const __nv_bfloat162 l = __floats2bfloat162_rn(f[2 * e] - hf.x, f[2 * e + 1] - hf.y);
+                            hw[e] = *reinterpret_cast<const uint32_t *>(&h);
+                            lw[e] = *reinterpret_cast<const uint32_t *>(&l);
+                        }
+                        const int o = r * rb2 + swz_chunk(k, r, rb2) * 16;
+                        *reinterpret_cast<uint4 *>(bh + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                        *reinterpret_cast<uint4 *>(bl + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
                     }
                 } else if (PREC) {
                     float4 *lo = reinterpret_cast<float4 *>(aslots + sa * 2 * a.a_slot + a.a_slot);
