@@ -532,18 +532,20 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 } else {
                     // fp32 row r (rowb bytes, swizzled) -> bf16 row r (rowb / 2
                     // bytes, swizzled for that width) in the second half of the slot
+                    // one thread per 16-byte bf16 chunk (two fp32 chunks), as in PREC 2
                     uint8_t *bf = aslots + sa * 2 * a.a_slot + a.a_slot;
-                    const int rb = (int)rowb, rb2 = rb / 2, cpr = rb / 16;
-                    for (int j = t; j < n16; j += 32 * NCONV) {
-                        const int r = j / cpr, pc = j - r * cpr;
-                        const int lc = swz_chunk(pc, r, rb);  // logical chunk: channels 4 lc .. 4 lc + 3
-                        const float4 v = ar[j];
-                        const __nv_bfloat162 b01 = __floats2bfloat162_rn(v.x, v.y), b23 = __floats2bfloat162_rn(v.z, v.w);
-                        uint2 q;
-                        q.x = *reinterpret_cast<const uint32_t *>(&b01);
-                        q.y = *reinterpret_cast<const uint32_t *>(&b23);
-                        const int bc = swz_chunk(lc >> 1, r, rb2);
-                        *reinterpret_cast<uint2 *>(bf + r * rb2 + bc * 16 + (lc & 1) * 8) = q;
+                    const int rb = (int)rowb, rb2 = rb / 2;
+                    const int sh = rb2 == 64 ? 2 : 1;  // log2(bf16 chunks per row)
+                    const int n8 = n16 / 2;
+                    for (int q = t; q < n8; q += 32 * NCONV) {
+                        const int r = q >> sh, k = q & ((1 << sh) - 1);
+                        const float4 v0 = ar[r * (2 << sh) + swz_chunk(2 * k, r, rb)];
+                        const float4 v1 = ar[r * (2 << sh) + swz_chunk(2 * k + 1, r, rb)];
+                        const __nv_bfloat162 b0 = __floats2bfloat162_rn(v0.x, v0.y), b1 = __floats2bfloat162_rn(v0.z, v0.w),
+                                             b2 = __floats2bfloat162_rn(v1.x, v1.y), b3 = __floats2bfloat162_rn(v1.z, v1.w);
+                        *reinterpret_cast<uint4 *>(bf + r * rb2 + swz_chunk(k, r, rb2) * 16) =
+                            make_uint4(*reinterpret_cast<const uint32_t *>(&b0), *reinterpret_cast<const uint32_t *>(&b1),
+                                       *reinterpret_cast<const uint32_t *>(&b2), *reinterpret_cast<const uint32_t *>(&b3));
                     }
                 }
                 fence_proxy_async();
