@@ -26,8 +26,8 @@
 // (T taps per stage for narrow layers, so a stage carries enough MMA work).
 //
 // Warp roles (persistent CTAs, one per SM, walking (tile, K-split) units):
-//   warp 0      TMA producer          warps 6-13 converters (A -> hi, lo)
-//   warp 1      MMA issuer            warps 2-5  epilogue (TMEM -> bias, act,
+//   warp 0      TMA producer          warps 10-17 converters (A -> hi, lo)
+//   warp 1      MMA issuer            warps 2-9  epilogue (TMEM -> bias, act,
 //                                                 fp32 NHWC or split-K partials)
 // TMEM holds two accumulators, so the epilogue of a unit overlaps the MMAs of
 // the next.  Producer and MMA warps run converged; one elected lane issues.
@@ -67,7 +67,14 @@ namespace {
 #define SS_CONV_NCONV 8
 #endif
 constexpr int NCONV = SS_CONV_NCONV;
-constexpr int TM_THREADS = 32 * (6 + NCONV);
+// epilogue warps (2 .. 2 + NEPI - 1): 4 (one per TMEM lane quarter) or 8 (two
+// per quarter, each draining half of the accumulator columns)
+#ifndef SS_CONV_NEPI
+#define SS_CONV_NEPI 8
+#endif
+constexpr int NEPI = SS_CONV_NEPI;
+constexpr int CONV0 = 2 + NEPI;  // first converter warp
+constexpr int TM_THREADS = 32 * (2 + NEPI + NCONV);
 constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA
 constexpr int HT_H = 16, HT_W = 8;  // halo-mode output tile (rows x columns)
 
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 4);
+            mbar_init(&acc_empty[i], NEPI);
         }
         fence_barrier_init();
     }
@@ -405,9 +412,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             if (uc == 0 && lane == 0) trace_at(a, 6);
             if (uc < 9 && lane == 0) trace_at(a, 12 + 4 * uc + 2);
         }
-    } else if (warp < 6) {
+    } else if (warp < CONV0) {
         // ---------------- epilogue ----------------
         const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int eh = (warp - 2) / 4;  // NEPI = 8: which half of the columns
         pdl_wait();
         uint32_t uc = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
@@ -433,7 +441,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 pix = (size_t)oy * a.W + ox;
             }
             const uint32_t t0 = tmem + acc * acc_cols + ((uint32_t)(q * 32) << 16);
-            for (int c0 = 0; c0 < np; c0 += 16) {
+            const int cstep = NEPI == 8 ? 32 : 16;  // NEPI = 8: the two warps of a quarter alternate 16-column chunks
+            for (int c0 = NEPI == 8 ? 16 * eh : 0; c0 < np; c0 += cstep) {
                 float v[16];
                 tmem_ld16(t0 + c0, v);
                 if (PREC) {
@@ -475,7 +484,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         }
     } else {
         // ---------------- converters: A -> (hi in place, lo beside) ----------------
-        const int t = threadIdx.x - 192;
+        const int t = threadIdx.x - 32 * CONV0;
         const int n16 = a.a_slot / 16;  // whole slot (phase padding included)
         uint32_t ga = 0;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
