@@ -664,6 +664,8 @@ int tma_taps_per_stage(int k, int stride, int dil, int cin, int np, int prec)
 {
     if (amode_for(k, stride, dil, cin) == 0) return 1;  // im2col: one tap per stage
     const int tap_bytes = prec == 1 ? 2 * np * 128 : (prec == 2 ? 2 : 1) * np * 64;
+    // ~36 KB of weights per stage (a smaller stage costs more: 18 KB for
+    // split-bf16 measured 408 -> 394 frames/s; larger ones do not fit 2 stages)
     return std::max(1, std::min(k * k, 36864 / tap_bytes));
 }
 
@@ -833,8 +835,12 @@ static int launch_parts(const ConvParams &p, const CUtensorMap &tmA, int prec, i
     const int bar_bytes = 1024 + 512;
     // weights resident for the whole launch when every stage fits
     static const bool res_on = getenv("SS_CONV_BRES") == nullptr || strcmp(getenv("SS_CONV_BRES"), "0");
-    a.b_res = res_on && parts == 1 &&
-              2 * a.na * a.a_slot + a.nk_all * a.b_stage + bar_bytes + a.nk_all * 16 <= SMEM_MAX;
+    const bool res_fits = parts == 1 &&
+                          2 * a.na * a.a_slot + a.nk_all * a.b_stage + bar_bytes + a.nk_all * 16 <= SMEM_MAX;
+    // streaming needs 2 stages beside the A slots; a layer that cannot stream
+    // keeps its weights resident even under SS_CONV_BRES=0
+    const bool can_stream = (SMEM_MAX - 2 * a.na * a.a_slot - bar_bytes) / a.b_stage >= 2 || amode == 0;
+    a.b_res = res_fits && (res_on || !can_stream);
     if (a.b_res) {
         a.stages = a.nk_all;
     } else {
