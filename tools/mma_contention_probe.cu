@@ -43,13 +43,15 @@ __global__ void __launch_bounds__(NT, 1) probe(int np, int reps, int mode, long 
     uint8_t *base = (uint8_t *)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
     uint8_t *ahi = base, *alo = base + 16 * 1024, *bs = base + 32 * 1024;  // A 16 KB each, B 9 x 4 KB
     uint8_t *side = base + 80 * 1024;                                         // 64 KB converter traffic
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t mbar, ubar[2];
     __shared__ uint32_t tslot;
     __shared__ volatile int stop;
     const int tid = threadIdx.x, warp = tid >> 5;
     for (int i = tid; i < (144 * 1024) / 4; i += NT) reinterpret_cast<float *>(base)[i] = 0.001f;
     if (tid == 0) {
         mbar_init(&mbar, 1);
+        mbar_init(&ubar[0], 1);
+        mbar_init(&ubar[1], 1);
         fence_barrier_init();
         stop = 0;
     }
@@ -65,12 +67,22 @@ __global__ void __launch_bounds__(NT, 1) probe(int np, int reps, int mode, long 
             const uint32_t lay = 6, sbo = 10 * rowb;
             const uint32_t id2 = idesc(1u, 128u, (uint32_t)(2 * np)), id1 = idesc(1u, 128u, (uint32_t)np);
             long long t0 = clock64();
+            // mode bit 4: per "unit" of 9 K steps the conv kernel's bookkeeping --
+            // a fresh accumulation (acc = 0) in the other TMEM accumulator and two
+            // commits (slot free, accumulator full) to barriers nobody waits on
+            const bool units = mode & 4;
+            uint32_t d = tmem;
             for (int r = 0; r < reps; ++r) {
                 const int tap = r % 9;
+                if (units && tap == 0 && r > 0) {
+                    mma_commit(&ubar[0]);
+                    mma_commit(&ubar[1]);
+                    d = d == tmem ? tmem + 128 : tmem;
+                }
                 const uint32_t off = (uint32_t)(((tap / 3) * 10 + tap % 3) * rowb);
                 const uint64_t bd = desc(smem_u32(bs) + tap * 4096, 512, 4);
-                mma_f16(tmem, desc(smem_u32(ahi) + off, sbo, lay), bd, id2, r > 0 ? 1u : 0u);
-                mma_f16(tmem, desc(smem_u32(alo) + off, sbo, lay), bd, id1, 1u);
+                mma_f16(d, desc(smem_u32(ahi) + off, sbo, lay), bd, id2, (units ? tap > 0 : r > 0) ? 1u : 0u);
+                mma_f16(d, desc(smem_u32(alo) + off, sbo, lay), bd, id1, 1u);
             }
             mma_commit(&mbar);
             mbar_wait(&mbar, 0);
@@ -115,9 +127,10 @@ int main()
     const size_t smem = 148 * 1024;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int reps = 1800;
-    const char *names[4] = {"alone", "+ TMEM loads", "+ smem traffic", "+ both"};
-    for (int np : {16, 32, 64})
-        for (int mode = 0; mode < 4; ++mode) {
+    const char *names[8] = {"alone", "+ TMEM loads", "+ smem traffic", "+ both",
+                            "units", "units + TMEM", "units + smem", "units + both"};
+    for (int np : {16, 32})
+        for (int mode = 0; mode < 8; ++mode) {
             probe<<<1, NT, smem>>>(np, reps, mode, d);
             if (cudaDeviceSynchronize() != cudaSuccess) {
                 printf("error np=%d mode=%d\n", np, mode);
