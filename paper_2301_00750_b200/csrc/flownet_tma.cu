@@ -362,6 +362,37 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 const uint32_t araw = smem_u32(aslots + sa * 2 * a.a_slot);
                 const uint32_t b0 = smem_u32(bst + s * a.b_stage);
                 int ky = tap0 / a.k, kx = tap0 - ky * a.k;
+                if (AMODE == 1) {
+                    // halo views: the descriptors' start-address fields (addr >> 4)
+                    // advance by fixed steps per tap, so the stage's base
+                    // descriptors are built once and each tap adds its offset
+                    const uint32_t cstep = ((uint32_t)a.dil * arb) >> 4;
+                    const uint32_t rstep = ((uint32_t)(a.halo_w * a.dil) * arb) >> 4;
+                    uint32_t o16 = (uint32_t)ky * rstep + (uint32_t)kx * cstep;
+                    const uint64_t bstep = bstride >> 4;
+                    uint64_t bdj = PREC == 1 ? sdesc_sw128(b0) : sdesc_sw(b0, 512u, 4u);
+                    const uint64_t da0 = sdesc_sw(araw + (PREC == 1 ? 0u : (uint32_t)a.a_slot), sbo, alay);
+                    const uint64_t dl0 = sdesc_sw(araw + (uint32_t)a.a_slot + (PREC == 2 ? (uint32_t)a.a_slot / 2 : 0u),
+                                                  sbo, alay);
+                    for (int j = 0; j < nt; ++j, bdj += bstep) {
+                        const uint64_t ad = da0 + o16, ld = dl0 + o16;
+                        for (int i = 0; i < nks; ++i) {
+                            const uint32_t acc = (st > kb || j > 0 || i > 0) ? 1u : 0u;
+                            if (PREC == 2)
+                                mma_step_bf16x2(d, ad + 2 * i, ld + 2 * i, bdj + 2 * i, idh2, idh1, acc);
+                            else if (PREC == 1)
+                                mma_step(d, ad + 2 * i, ld + 2 * i, bdj + 2 * i, id2, id1, acc);
+                            else
+                                mma_step_bf16(d, ad + 2 * i, bdj + 2 * i, idb, acc);
+                        }
+                        if (++kx == a.k) {
+                            kx = 0;
+                            o16 += rstep - (uint32_t)(a.k - 1) * cstep;
+                        } else {
+                            o16 += cstep;
+                        }
+                    }
+                } else
                 for (int j = 0; j < nt; ++j) {
                     uint32_t off = 0;
                     if (AMODE == 1)
