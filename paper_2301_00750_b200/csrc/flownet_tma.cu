@@ -183,6 +183,48 @@ __device__ __forceinline__ void mma_step_bf16x2(uint32_t d, uint64_t ah, uint64_
         : "memory");
 }
 
+// The same MMA steps with each 64-bit smem descriptor given as its low word
+// (start address, LBO) and a high word shared by the A operands (SBO, layout):
+// the halo loop then advances descriptors with 32-bit adds only
+__device__ __forceinline__ void mma_step_w(uint32_t d, uint32_t ahl, uint32_t all, uint32_t ahw, uint32_t bl,
+                                           uint32_t bhw, uint32_t id2, uint32_t id1, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 ah, al, bd;\n\t"
+        "mov.b64 ah, {%1, %3};\n\tmov.b64 al, {%2, %3};\n\tmov.b64 bd, {%4, %5};\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bd, %7, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bd, %8, 1;\n\t}" ::"r"(d),
+        "r"(ahl), "r"(all), "r"(ahw), "r"(bl), "r"(bhw), "r"(acc), "r"(id2), "r"(id1)
+        : "memory");
+}
+__device__ __forceinline__ void mma_step_bf16x2_w(uint32_t d, uint32_t ahl, uint32_t all, uint32_t ahw, uint32_t bl,
+                                                  uint32_t bhw, uint32_t id2, uint32_t id1, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 ah, al, bd;\n\t"
+        "mov.b64 ah, {%1, %3};\n\tmov.b64 al, {%2, %3};\n\tmov.b64 bd, {%4, %5};\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah, bd, %7, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], al, bd, %8, 1;\n\t}" ::"r"(d),
+        "r"(ahl), "r"(all), "r"(ahw), "r"(bl), "r"(bhw), "r"(acc), "r"(id2), "r"(id1)
+        : "memory");
+}
+__device__ __forceinline__ void mma_step_bf16_w(uint32_t d, uint32_t al_, uint32_t ahw, uint32_t bl, uint32_t bhw,
+                                                uint32_t id, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 ad, bd;\n\t"
+        "mov.b64 ad, {%1, %2};\n\tmov.b64 bd, {%3, %4};\n\t"
+        "setp.ne.b32 p, %5, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %6, p;\n\t}" ::"r"(d),
+        "r"(al_), "r"(ahw), "r"(bl), "r"(bhw), "r"(acc), "r"(id)
+        : "memory");
+}
+
 // physical 16-byte chunk of logical chunk c in row r of a swizzled tile with
 // rows of rb bytes (SWIZZLE_{128,64,32}B; the tile base is 1024-aligned)
 __device__ __forceinline__ int swz_chunk(int c, int r, int rb)
@@ -369,21 +411,26 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     const uint32_t cstep = ((uint32_t)a.dil * arb) >> 4;
                     const uint32_t rstep = ((uint32_t)(a.halo_w * a.dil) * arb) >> 4;
                     uint32_t o16 = (uint32_t)ky * rstep + (uint32_t)kx * cstep;
-                    const uint64_t bstep = bstride >> 4;
-                    uint64_t bdj = PREC == 1 ? sdesc_sw128(b0) : sdesc_sw(b0, 512u, 4u);
+                    const uint32_t bstep = bstride >> 4;
+                    const uint64_t bd0 = PREC == 1 ? sdesc_sw128(b0) : sdesc_sw(b0, 512u, 4u);
                     const uint64_t da0 = sdesc_sw(araw + (PREC == 1 ? 0u : (uint32_t)a.a_slot), sbo, alay);
                     const uint64_t dl0 = sdesc_sw(araw + (uint32_t)a.a_slot + (PREC == 2 ? (uint32_t)a.a_slot / 2 : 0u),
                                                   sbo, alay);
-                    for (int j = 0; j < nt; ++j, bdj += bstep) {
-                        const uint64_t ad = da0 + o16, ld = dl0 + o16;
+                    // low words advance, high words (SBO, layout) are per operand constants
+                    const uint32_t ahw = (uint32_t)(da0 >> 32), bhw = (uint32_t)(bd0 >> 32);
+                    uint32_t bl = (uint32_t)bd0;
+                    const uint32_t al0 = (uint32_t)da0, ll0 = (uint32_t)dl0;
+                    const uint32_t acc0 = st > kb ? 1u : 0u;
+                    for (int j = 0; j < nt; ++j, bl += bstep) {
+                        const uint32_t al = al0 + o16, ll = ll0 + o16;
                         for (int i = 0; i < nks; ++i) {
-                            const uint32_t acc = (st > kb || j > 0 || i > 0) ? 1u : 0u;
+                            const uint32_t acc = (j | i) ? 1u : acc0;
                             if (PREC == 2)
-                                mma_step_bf16x2(d, ad + 2 * i, ld + 2 * i, bdj + 2 * i, idh2, idh1, acc);
+                                mma_step_bf16x2_w(d, al + 2 * i, ll + 2 * i, ahw, bl + 2 * i, bhw, idh2, idh1, acc);
                             else if (PREC == 1)
-                                mma_step(d, ad + 2 * i, ld + 2 * i, bdj + 2 * i, id2, id1, acc);
+                                mma_step_w(d, al + 2 * i, ll + 2 * i, ahw, bl + 2 * i, bhw, id2, id1, acc);
                             else
-                                mma_step_bf16(d, ad + 2 * i, bdj + 2 * i, idb, acc);
+                                mma_step_bf16_w(d, al + 2 * i, ahw, bl + 2 * i, bhw, idb, acc);
                         }
                         if (++kx == a.k) {
                             kx = 0;
