@@ -379,9 +379,19 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         const uint32_t bstride = PREC == 1 ? (uint32_t)(2 * np * 128) : (uint32_t)((PREC == 2 ? 2 : 1) * np * 64);
         const uint32_t idh2 = idesc(1u, 128u, (uint32_t)(2 * np)), idh1 = idb;  // split-bf16 shapes
         if (BRES) mbar_wait(&b_full[0], 0);
+        // running ring positions / phases instead of per-event divisions (the
+        // MMA warp's instruction stream paces the thin layers)
         uint32_t ga = 0, gb = 0, uc = 0;
+        uint32_t a_pos = 0, a_ph = 0, b_pos = 0, b_ph = 0;
+        // (part, split, tile) of unit u, advanced by gridDim.x per iteration
+        ConvUnit cu = conv_unit(a, blockIdx.x);
         for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
-            const int split = conv_unit(a, u).split;
+            const int split = cu.split;
+            cu.tile += gridDim.x;
+            while (cu.tile >= a.n_tiles) {
+                cu.tile -= a.n_tiles;
+                if (++cu.split == a.splits) cu.split = 0;
+            }
             const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
             const uint32_t acc = uc & 1;
             mbar_wait(&acc_empty[acc], ((uc >> 1) & 1) ^ 1);
@@ -390,13 +400,23 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             int cb = kb / a.sp_cb, grp = kb - cb * a.sp_cb, sa = 0;
             for (int st = kb; st < ke; ++st, ++gb) {
                 if (a_event<AMODE>(st, kb, grp)) {
-                    sa = (int)(ga % (uint32_t)NA);
-                    mbar_wait(&a_conv[sa], (ga / NA) & 1);
+                    sa = (int)a_pos;
+                    mbar_wait(&a_conv[sa], a_ph);
                     if (ga == 0 && lane == 0) trace_at(a, 5);
                     ++ga;
+                    if (++a_pos == (uint32_t)NA) {
+                        a_pos = 0;
+                        a_ph ^= 1;
+                    }
                 }
-                const int s = BRES ? st : (int)(gb % (uint32_t)S);
-                if (!BRES) mbar_wait(&b_full[s], (gb / S) & 1);
+                const int s = BRES ? st : (int)b_pos;
+                if (!BRES) {
+                    mbar_wait(&b_full[s], b_ph);
+                    if (++b_pos == (uint32_t)S) {
+                        b_pos = 0;
+                        b_ph ^= 1;
+                    }
+                }
                 tc_fence_after();
                 const int tap0 = grp * a.T, nt = min(a.T, a.taps - tap0);
                 const int live = min(a.cpp, a.cin - cb * a.cpp);
