@@ -312,8 +312,18 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         pdl_wait();  // the activations are the previous kernel's output
         if (lane == 0) trace_at(a, 2);
         uint32_t ga = 0, gb = 0;
+        uint32_t a_pos = 0, a_ph = 1, b_pos = 0, b_ph = 1;  // empty-slot waits start on the "free" parity
+        ConvUnit nx = conv_unit(a, blockIdx.x);
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const ConvUnit cu = conv_unit(a, u);
+            const ConvUnit cu = nx;
+            nx.tile += gridDim.x;
+            while (nx.tile >= a.n_tiles) {
+                nx.tile -= a.n_tiles;
+                if (++nx.split == a.splits) {
+                    nx.split = 0;
+                    ++nx.part;
+                }
+            }
             const int tile = cu.tile, split = cu.split, prow = a.part_row + cu.part * a.part_rows;
             int x0, y0;
             if (AMODE == 0) {
@@ -330,8 +340,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             for (int st = kb; st < ke; ++st, ++gb) {
                 const int tap0 = grp * a.T;
                 if (a_event<AMODE>(st, kb, grp)) {
-                    const int sa = (int)(ga % (uint32_t)NA);
-                    mbar_wait(&a_empty[sa], ((ga / NA) & 1) ^ 1);
+                    const int sa = (int)a_pos;
+                    mbar_wait(&a_empty[sa], a_ph);
+                    if (++a_pos == (uint32_t)NA) {
+                        a_pos = 0;
+                        a_ph ^= 1;
+                    }
                     if (elect_one()) {
                         const uint32_t dst = smem_u32(aslots + sa * 2 * a.a_slot);
                         mbar_expect_tx(&a_full[sa], (uint32_t)a.a_box);
@@ -353,8 +367,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                     ++ga;
                 }
                 if (!BRES) {
-                    const int s = (int)(gb % (uint32_t)S);
-                    mbar_wait(&b_empty[s], ((gb / S) & 1) ^ 1);
+                    const int s = (int)b_pos;
+                    mbar_wait(&b_empty[s], b_ph);
+                    if (++b_pos == (uint32_t)S) {
+                        b_pos = 0;
+                        b_ph ^= 1;
+                    }
                     if (elect_one()) {
                         mbar_expect_tx(&b_full[s], (uint32_t)a.b_stage);
                         tma_tile_3d(smem_u32(bst + s * a.b_stage), &tmB, 0, prow, cb * a.taps + tap0,
@@ -584,17 +602,27 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         // ---------------- converters: A -> (hi in place, lo beside) ----------------
         const int t = threadIdx.x - 32 * CONV0;
         const int n16 = a.a_slot / 16;  // whole slot (phase padding included)
-        uint32_t ga = 0;
+        uint32_t ga = 0, a_pos = 0, a_ph = 0;
+        ConvUnit nx = conv_unit(a, blockIdx.x);
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const int split = conv_unit(a, u).split;
+            const int split = nx.split;
+            nx.tile += gridDim.x;
+            while (nx.tile >= a.n_tiles) {
+                nx.tile -= a.n_tiles;
+                if (++nx.split == a.splits) nx.split = 0;
+            }
             const int kb = split * a.k_per_split, ke = min(kb + a.k_per_split, a.nk_all);
             int grp = kb % a.sp_cb;
             for (int st = kb; st < ke; ++st) {
                 const bool ev = a_event<AMODE>(st, kb, grp);
                 if (++grp == a.sp_cb) grp = 0;
                 if (!ev) continue;
-                const int sa = (int)(ga % (uint32_t)NA);
-                mbar_wait(&a_full[sa], (ga / NA) & 1);
+                const int sa = (int)a_pos;
+                mbar_wait(&a_full[sa], a_ph);
+                if (++a_pos == (uint32_t)NA) {
+                    a_pos = 0;
+                    a_ph ^= 1;
+                }
                 if (ga == 0 && t == 0) trace_at(a, 3);
                 if (ga < 9 && t == 0) trace_at(a, 12 + 4 * ga + 1);
                 ++ga;
