@@ -100,9 +100,93 @@ __global__ void __launch_bounds__(256) k_depthwise(const float *__restrict__ in,
         if (x0 + p < W) *reinterpret_cast<float4 *>(out + ((long)y * W + x0 + p) * ld_out + c) = acc[p];
 }
 
+// Tap-sharing variant: a thread owns 4 channels x a 4 x 2 grid of pixels
+// spaced by the dilation d (columns x, x+d, x+2d, x+3d; rows y, y+d), so its
+// outputs' taps coincide: 6 distinct columns x 4 distinct rows = 24 float4
+// loads for 32 outputs (the row-adjacent layout above loads 36 for 16 at
+// d >= 4).  Per output the FMA order is the same (ky outer, kx inner).
+constexpr int DWS_PX = 4, DWS_PY = 2;
+__global__ void __launch_bounds__(256) k_depthwise_s(const float *__restrict__ in, int ld, int H, int W, int C,
+                                                    const float *__restrict__ w, int dil, float *__restrict__ out,
+                                                    int ld_out)
+{
+    pdl_wait();
+    const int C4 = C / 4;
+    // pixel groups: x = bx * 4d + r + k d (r < d, k < 4), y = by * 2d + q + j d (q < d, j < 2)
+    const int gx = (W + DWS_PX * dil - 1) / (DWS_PX * dil), gy = (H + DWS_PY * dil - 1) / (DWS_PY * dil);
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long ng = (long)gx * gy * dil * dil;
+    if (i >= ng * C4) return;
+    const int c = (int)(i % C4) * 4;
+    long g = i / C4;
+    const int r = (int)(g % dil);
+    g /= dil;
+    const int q = (int)(g % dil);
+    g /= dil;
+    const int bx = (int)(g % gx), by = (int)(g / gx);
+    const int x0 = bx * DWS_PX * dil + r, y0 = by * DWS_PY * dil + q;
+    float4 k[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) k[t] = __ldg(reinterpret_cast<const float4 *>(w + t * C + c));
+    float4 acc[DWS_PY][DWS_PX];
+#pragma unroll
+    for (int j = 0; j < DWS_PY; ++j)
+#pragma unroll
+        for (int p = 0; p < DWS_PX; ++p) acc[j][p] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // input rows y0 + (m - 1) d, m = 0 .. DWS_PY + 1; columns x0 + (n - 1) d, n = 0 .. DWS_PX + 1
+#pragma unroll
+    for (int m = 0; m < DWS_PY + 2; ++m) {
+        const int iy = y0 + (m - 1) * dil;
+        float4 v[DWS_PX + 2];
+        const bool rok = iy >= 0 && iy < H;
+        const float *row = in + (long)(rok ? iy : 0) * W * ld + c;
+#pragma unroll
+        for (int n = 0; n < DWS_PX + 2; ++n) {
+            const int ix = x0 + (n - 1) * dil;
+            v[n] = (rok && ix >= 0 && ix < W) ? __ldg(reinterpret_cast<const float4 *>(row + (long)ix * ld))
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        // this input row is tap row ky = m - j for output row j
+#pragma unroll
+        for (int j = 0; j < DWS_PY; ++j) {
+            const int ky = m - j;
+            if (ky < 0 || ky > 2) continue;
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx) {
+                const float4 kk = k[ky * 3 + kx];
+#pragma unroll
+                for (int p = 0; p < DWS_PX; ++p) {
+                    const float4 vv = v[p + kx];
+                    acc[j][p].x = fmaf(vv.x, kk.x, acc[j][p].x);
+                    acc[j][p].y = fmaf(vv.y, kk.y, acc[j][p].y);
+                    acc[j][p].z = fmaf(vv.z, kk.z, acc[j][p].z);
+                    acc[j][p].w = fmaf(vv.w, kk.w, acc[j][p].w);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < DWS_PY; ++j) {
+        const int y = y0 + j * dil;
+        if (y >= H) continue;
+#pragma unroll
+        for (int p = 0; p < DWS_PX; ++p) {
+            const int x = x0 + p * dil;
+            if (x < W) *reinterpret_cast<float4 *>(out + ((long)y * W + x) * ld_out + c) = acc[j][p];
+        }
+    }
+}
+
 int launch_depthwise(const float *in, int ld, int H, int W, int C, const float *w, int dil,
                      float *out, int ld_out, cudaStream_t st)
 {
+    static const bool shared_taps = getenv("SS_DW") == nullptr || strcmp(getenv("SS_DW"), "rows");
+    if (shared_taps) {
+        const long gx = (W + DWS_PX * dil - 1) / (DWS_PX * dil), gy = (H + DWS_PY * dil - 1) / (DWS_PY * dil);
+        const long n = gx * gy * dil * dil * (C / 4);
+        return launch_pdl("k_depthwise_s", k_depthwise_s, dim3(blocks_for(n, 256)), dim3(256), 0, st, in, ld, H, W,
+                          C, w, dil, out, ld_out);
+    }
     const long n = (long)H * ((W + DW_PX - 1) / DW_PX) * (C / 4);
     return launch_pdl("k_depthwise", k_depthwise, dim3(blocks_for(n, 256)), dim3(256), 0, st, in, ld, H, W, C,
                       w, dil, out, ld_out);
