@@ -533,6 +533,127 @@ __global__ void __launch_bounds__(64 * CS) k_corr(const float *__restrict__ f1, 
     }
 }
 
+// Register-blocked variant (fine levels): a thread owns 8 horizontally adjacent
+// pixels of one tile row and one dy, all 9 dx, so per float4 of channels it
+// reads its 8 f1 vectors and streams the 16 w2 vectors of the row window once
+// (24 LDS.128 for 288 FMAs; the 2-pixel layout above needs 32 for 216).
+// Thread t of a channel group: row = t & 7, segment = (t >> 3) & 1, dy = t >> 4
+// (8 consecutive threads read 8 rows: distinct bank groups).  Channel groups
+// add their partial sums in group order at the end, like k_corr.
+template <int DY, int CS>
+__global__ void __launch_bounds__(16 * DY * CS) k_corr8(const float *__restrict__ f1, const float *__restrict__ w2,
+                                                        int C, int H, int W, float *__restrict__ x, int xld,
+                                                        int copy_f1)
+{
+    constexpr int WR = CR_TH + DY - 1;
+    constexpr int NTG = 16 * DY, NT = NTG * CS, CPG = CR_CK / CS;
+    static_assert(CPG % 4 == 0, "channel groups are float4 multiples");
+    pdl_wait();
+    extern __shared__ __align__(16) float cr_smem[];
+    float(*sw)[CR_W2F] = reinterpret_cast<float(*)[CR_W2F]>(cr_smem);
+    float(*sf)[CR_F1F] = reinterpret_cast<float(*)[CR_F1F]>(cr_smem + 2 * CR_W2F);
+    const int tid = threadIdx.x, grp = tid / NTG;
+    const int t = tid - grp * NTG;
+    const int row = t & 7, seg = (t >> 3) & 1, j = t >> 4;
+    const int bx = blockIdx.x * CR_TW, by = blockIdx.y * CR_TH;
+    const int dy0 = (int)blockIdx.z * DY - CR_HALO;
+
+    auto load = [&](int buf, int c0) {
+        for (int i = tid; i < WR * CR_WW * 4; i += NT) {
+            const int q = i & 3, px = (i >> 2) % CR_WW, r = (i >> 2) / CR_WW;
+            const int gy = by + r + dy0, gx = bx - CR_HALO + px;
+            const bool ok = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            cp_async16(&sw[buf][r * CR_W2P + px * CR_PX + q * 4],
+                       w2 + ((long)(ok ? gy : 0) * W + (ok ? gx : 0)) * C + c0 + q * 4, ok);
+        }
+        for (int i = tid; i < CR_TH * CR_TW * 4; i += NT) {
+            const int q = i & 3, px = (i >> 2) % CR_TW, r = (i >> 2) / CR_TW;
+            const int gy = by + r, gx = bx + px;
+            const bool ok = gy < H && gx < W;
+            cp_async16(&sf[buf][r * CR_F1P + px * CR_PX + q * 4],
+                       f1 + ((long)(ok ? gy : 0) * W + (ok ? gx : 0)) * C + c0 + q * 4, ok);
+        }
+        cp_async_commit();
+    };
+
+    float acc[8][9];
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+        for (int d = 0; d < 9; ++d) acc[p][d] = 0.f;
+
+    const int nch = C / CR_CK;
+    load(0, 0);
+    for (int k = 0; k < nch; ++k) {
+        const int buf = k & 1;
+        if (k + 1 < nch) {
+            load(buf ^ 1, (k + 1) * CR_CK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        if (copy_f1 && (int)blockIdx.z == 4 / DY) {  // f1 -> x[:, 96 + c], one dy group does it
+            for (int i = tid; i < CR_TH * CR_TW * 4; i += NT) {
+                const int q = i & 3, px = (i >> 2) % CR_TW, r = (i >> 2) / CR_TW;
+                const int gy = by + r, gx = bx + px;
+                if (gy < H && gx < W)
+                    *reinterpret_cast<float4 *>(x + ((long)gy * W + gx) * xld + 96 + k * CR_CK + q * 4) =
+                        *reinterpret_cast<const float4 *>(&sf[buf][r * CR_F1P + px * CR_PX + q * 4]);
+            }
+        }
+        const float *a = &sf[buf][row * CR_F1P + seg * 8 * CR_PX];
+        const float *w = &sw[buf][(row + j) * CR_W2P + seg * 8 * CR_PX];
+#pragma unroll
+        for (int c = grp * CPG; c < grp * CPG + CPG; c += 4) {
+            float4 av[8];
+#pragma unroll
+            for (int p = 0; p < 8; ++p) av[p] = *reinterpret_cast<const float4 *>(a + p * CR_PX + c);
+#pragma unroll
+            for (int n = 0; n < 16; ++n) {
+                const float4 b = *reinterpret_cast<const float4 *>(w + n * CR_PX + c);
+#pragma unroll
+                for (int p = 0; p < 8; ++p) {
+                    const int d = n - p;
+                    if (d < 0 || d > 8) continue;
+                    acc[p][d] = fmaf(av[p].x, b.x, fmaf(av[p].y, b.y, fmaf(av[p].z, b.z, fmaf(av[p].w, b.w, acc[p][d]))));
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (CS > 1) {
+        float *red = cr_smem;
+        constexpr int NV = 72;
+        static_assert((CS - 1) * NV * NTG <= 2 * (CR_W2F + CR_F1F), "reduction fits the staging buffers");
+        if (grp > 0) {
+#pragma unroll
+            for (int p = 0; p < 8; ++p)
+#pragma unroll
+                for (int d = 0; d < 9; ++d) red[((grp - 1) * NV + p * 9 + d) * NTG + t] = acc[p][d];
+        }
+        __syncthreads();
+        if (grp > 0) return;
+#pragma unroll
+        for (int g = 1; g < CS; ++g)
+#pragma unroll
+            for (int p = 0; p < 8; ++p)
+#pragma unroll
+                for (int d = 0; d < 9; ++d) acc[p][d] += red[((g - 1) * NV + p * 9 + d) * NTG + t];
+    }
+    const float inv = 1.f / (float)C;
+    const int y = by + row;
+    if (y >= H) return;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const int xx = bx + seg * 8 + p;
+        if (xx >= W) continue;
+        float *dst = x + ((long)y * W + xx) * xld + (dy0 + CR_HALO + j) * 9;
+#pragma unroll
+        for (int d = 0; d < 9; ++d) dst[d] = leaky(acc[p][d] * inv);
+    }
+}
+
 // one-time kernel attributes (call outside stream capture)
 int prepare_flow_kernels()
 {
@@ -541,6 +662,8 @@ int prepare_flow_kernels()
     SS_CUDA_TRY(cudaFuncSetAttribute(k_corr<3, CR_CS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(2 * (CR_W2F + CR_F1F) * sizeof(float))));
     SS_CUDA_TRY(cudaFuncSetAttribute(k_corr<1, CR_CS_COARSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(2 * (CR_W2F + CR_F1F) * sizeof(float))));
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_corr8<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(2 * (CR_W2F + CR_F1F) * sizeof(float))));
     done = true;
     return SS_OK;
@@ -563,6 +686,10 @@ int launch_corr(const float *f1, const float *w2, int C, int H, int W, float *x,
                           W, x, xld, copy_f1 ? 1 : 0);
     }
     const dim3 grid((W + CR_TW - 1) / CR_TW, (H + CR_TH - 1) / CR_TH, 3);
+    static const bool blocked = getenv("SS_CORR") == nullptr || strcmp(getenv("SS_CORR"), "pairs");
+    if (blocked)
+        return launch_pdl("k_corr8", k_corr8<3, 4>, grid, dim3(16 * 3 * 4), smem, st, f1, w2, C, H, W, x, xld,
+                          copy_f1 ? 1 : 0);
     return launch_pdl("k_corr", k_corr<3, CR_CS_FINE>, grid, dim3(64 * CR_CS_FINE), smem, st, f1, w2, C, H, W, x,
                       xld, copy_f1 ? 1 : 0);
 }
