@@ -1314,6 +1314,599 @@ static int launch_tma(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st
                           st, maps, a);
 }
 
+// ---------------------------------------------------------------------------
+// v4: row streaming with a time skew (round 2).
+//
+// v2 recomputes an 8-pixel apron on all four sides of every 128 x 64 region
+// (1.52x the committed work).  v4 removes the vertical apron almost entirely:
+// a CTA owns a 256-column strip of one channel plane over a segment of rows
+// and streams down it one row per step, every iteration level of the pass
+// alive at once, each a row behind the one before it -- at step s level k
+// updates row s - k (s - k - 1 in the second warp group), whose N / C / S
+// inputs (level k - 1, rows r - 1 .. r + 1) and momentum input (level k - 2,
+// row r) were produced in the previous steps and sit in per-level register
+// rings.  Only the 8-row ramps at the ends of a segment are redundant, and
+// they shrink as a trapezoid (level k computes only the rows that reach a
+// committed row); the horizontal apron is 8 of 256 columns per side.
+//   * 4 warps per CTA, 2 CTAs per SM: warps (xh, grp): column half xh
+//     (lane l owns columns 4l .. 4l + 3 of its 128) and level group grp
+//     (levels 1-4 or 5-8).  Group 0 hands level 4 (and level 3, the momentum
+//     input of level 5) to group 1 through a 4-row shared-memory ring; the
+//     halves exchange their boundary columns through a tiny parity buffer.
+//     One CTA barrier per step orders all of it (written at step s, read at
+//     step s + 1 or s + 2).
+//   * The five input planes (O, O_prev, A, lapP, wc) stream into a 16-row
+//     shared-memory ring through TMA (one 256 x 1 box per plane and row,
+//     8 rows ahead, O / O_prev with L2 evict_first, the pass-invariant A,
+//     lapP, wc with evict_last so they stay L2-resident across the passes).
+//   * A / lapP / wc of the rows a group is updating live in a 4-row register
+//     ring (each row read from shared memory once per group, not once per
+//     level: per-level shared loads would bound the kernel).
+//   * Packed FP32: pairs are columns (4l, 4l + 1), (4l + 2, 4l + 3); N / S /
+//     centre / momentum operands are ring pairs as they stand, W / E are
+//     three re-packs per level-step with two warp shuffles.
+// Per element the reference op sequence is unchanged (sgd_u64), so iterates
+// are bit-identical to v2 / numpy.  Requires w % 4 == 0 (any h).
+//
+// Measured (B200, 1080p, 150 iterations): 1.24 ms against v2's 1.06 ms, so v2
+// stays the default (SS_SOLVER=v4 selects this one).  The redundancy is down
+// from 1.52x to ~1.2x, but the instruction count is not: a lane's block per
+// level-step is 4 x 1 elements (v2's is 4 x 8), so the W / E re-packs, edge
+// exchange, loads, max tracking and per-step bookkeeping are amortised over 4
+// elements instead of 32 (v2: ~75% of the loop's instructions are packed FP32,
+// v4: ~40%), and the per-level register rings (202 registers) cap the SM at
+// 8 warps with a CTA barrier per row: issue efficiency ~40%.  Steps taken on
+// the way (ncu): LDS.64 pairs instead of vector loads + moves, chunked TMA
+// (one wait / issue per 4 rows), the fast / slow step split (instruction
+// fetch stalls), the edge buffer instead of shuffles, unpredicated tracking:
+// 1.93 -> 1.24 ms.  Rows
+// outside the image are the replicate ghosts: row -1 = row 0 and row h =
+// row h - 1 of the same level, written into the ring slot the neighbour
+// reads.  A partial last pass (iterations % 8) runs levels above `iters` as
+// copies.
+namespace v4 {
+constexpr int K = 8;
+constexpr int SW = 256;         // strip width (2 warps x 32 lanes x 4 columns)
+constexpr int OW = SW - 2 * K;  // committed columns per strip
+constexpr int RING = 16;        // staged input rows: 4 chunks of 4
+constexpr int CH = 4;           // rows per TMA chunk (one mbarrier)
+constexpr int NCH = RING / CH;
+constexpr int HAND = 4;         // group 0 -> group 1 handoff rows
+constexpr int PLANES = 5;       // O, O_prev, A, lapP, wc
+constexpr int ROWF = PLANES * SW;
+constexpr int THREADS = 128;
+constexpr uint32_t CHUNK_TX = PLANES * CH * SW * sizeof(float);
+constexpr int EDGEF = 2 * K * 2 * 66 + 4 * 2 * 66;  // edge buffers (E8 + E4 below)
+constexpr size_t SMEM = ((size_t)RING * ROWF + (size_t)HAND * 2 * SW + EDGEF) * sizeof(float) +
+                        NCH * sizeof(uint64_t);
+}  // namespace v4
+
+struct V4Ctx {
+    float *ring, *hand, *edge;
+    uint64_t *full;
+    int y_start, y_last0, seg_y0, seg_y1, h, w;
+    int col;                 // lane's first column within the strip (xh * 128 + 4 * lane)
+    bool lft, rgt, colc;     // image left / right edge lane, committed column block
+    int L;                   // lane index over both halves (xh * 32 + lane)
+    uint32_t ld0, ld1;       // shared addresses of the lane's column pairs in ring row 0, plane 0
+    uint32_t hd0, hd1;       // the same in handoff row 0
+    int iters;
+    V2Consts k;
+};
+
+__device__ __forceinline__ int v4_lo(const V4Ctx &c, int k) { return max(0, c.seg_y0 - v4::K + k); }
+__device__ __forceinline__ int v4_hi(const V4Ctx &c, int k) { return min(c.h - 1, c.seg_y1 - 1 + v4::K - k); }
+// ring layout: chunk slot [plane][row in chunk][column] (one 256 x 4 TMA box
+// per plane and chunk)
+__device__ __forceinline__ int v4_idx(const V4Ctx &c, int r, int plane)
+{
+    const int n = r - c.y_start;
+    return ((((n >> 2) & (v4::NCH - 1)) * v4::PLANES + plane) * v4::CH + (n & 3)) * v4::SW;
+}
+__device__ __forceinline__ float *v4_row(const V4Ctx &c, int r, int plane) { return c.ring + v4_idx(c, r, plane); }
+// byte offset of (row r, plane) from the ring start
+__device__ __forceinline__ uint32_t v4_off(const V4Ctx &c, int r, int plane) { return (uint32_t)v4_idx(c, r, plane) * 4; }
+// wait for the chunk holding row r
+__device__ __forceinline__ void v4_wait_row(const V4Ctx &c, int r)
+{
+    const int j = (r - c.y_start) >> 2;
+    mbar_wait(c.full + (j & (v4::NCH - 1)), (uint32_t)(j >> 2) & 1u);
+}
+// The lane's columns c0..c3 live as the natural pairs (c0, c1), (c2, c3).
+// Each row loads as two 8-byte loads straight into the ring's register pairs:
+// the second address comes from a base ptxas cannot relate to the first (c.o8
+// holds 8 at run time), so it does not fuse them into one 16-byte load, whose
+// aligned register quad the ring slots do not occupy (that cost a move per
+// register).
+__device__ __forceinline__ void v4_ld(const V4Ctx &c, uint32_t off, u64 (&d)[2])
+{
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(d[0]) : "r"(c.ld0 + off) : "memory");
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(d[1]) : "r"(c.ld1 + off) : "memory");
+}
+__device__ __forceinline__ void v4_cp(u64 (&d)[2], const u64 (&s)[2])
+{
+    d[0] = s[0];
+    d[1] = s[1];
+}
+
+// W / E neighbours across lanes and across the two column halves go through
+// a small shared "edge" buffer: a level publishes each lane's first and last
+// column (c0, c3) when it produces a row, and the next level reads its
+// neighbours' values one step later (after the CTA barrier), so the loads
+// can issue at the top of the step.  Layout [parity][level][c0 | c3][1 + 64 + 1]
+// (lane index + 1 over both halves; the pads are the strip's outer apron);
+// level 4 -> 5 crosses the group boundary two steps later and has a 4-deep
+// ring of its own.
+namespace v4 {
+constexpr int EW = 66;
+constexpr int E8 = 2 * K * 2 * EW;  // [2][K][2][EW]
+constexpr int E4 = 4 * 2 * EW;      // [4][2][EW]
+}  // namespace v4
+__device__ __forceinline__ float *v4_e(const V4Ctx &c, int par, int lvl)
+{
+    return c.edge + (par * v4::K + lvl) * 2 * v4::EW;
+}
+__device__ __forceinline__ float *v4_e4(const V4Ctx &c, int slot) { return c.edge + v4::E8 + slot * 2 * v4::EW; }
+// publish a produced row's edge columns into edge block e
+__device__ __forceinline__ void v4_pub(const V4Ctx &c, float *e, const u64 (&U)[2])
+{
+    e[c.L + 1] = lo32(U[0]);
+    e[v4::EW + c.L + 1] = hi32(U[1]);
+}
+// the W (column c0 - 1) and E (column c3 + 1) neighbours from edge block e
+__device__ __forceinline__ void v4_nb(const V4Ctx &c, const float *e, float &wv, float &ev)
+{
+    wv = e[v4::EW + c.L];
+    ev = e[c.L + 2];
+}
+
+// one level-step for the lane's 4 columns: C / N / S = level k - 1 rows
+// r, r - 1, r + 1; M = level k - 2 row r; AR = A, lapP, wc of row r;
+// wv / ev = the W / E neighbours of columns c0 / c3
+__device__ __forceinline__ void v4_update(const V4Ctx &c, const u64 (&C)[2], const u64 (&N)[2],
+                                          const u64 (&S)[2], const u64 (&M)[2],
+                                          const u64 (&AR)[3][2], float wv, float ev, u64 (&U)[2])
+{
+    if (c.lft) wv = lo32(C[0]);  // replicate boundary: the neighbour is the cell itself
+    if (c.rgt) ev = hi32(C[1]);
+    // C[0] = (c0, c1), C[1] = (c2, c3): W / E of C[0] = (c-1, c0) / (c1, c2),
+    // of C[1] = (c1, c2) / (c3, c4)
+    const u64 W0 = pk(wv, lo32(C[0])), E0 = pk(hi32(C[0]), lo32(C[1])), E1 = pk(hi32(C[1]), ev);
+    U[0] = sgd_u64(C[0], M[0], N[0], S[0], W0, E0, AR[1][0], AR[0][0], AR[2][0], c.k.eta, c.k.kap,
+                   c.k.m4, c.k.z);
+    U[1] = sgd_u64(C[1], M[1], N[1], S[1], E0, E1, AR[1][1], AR[0][1], AR[2][1], c.k.eta, c.k.kap,
+                   c.k.m4, c.k.z);
+}
+
+// The per-pass maximum feeds only the grey-zone test, where any superset of
+// the iterates is conservative (a false alarm costs an exact replay, never a
+// wrong result), so every computed value is tracked, apron and ramp garbage
+// included: that is finite, since it is computed from image data, TMA zero
+// fill, or the zeroed ring rows before the segment start (two FMNMX3 per
+// level-step instead of a predicated select per value; the predicate cost 13%).
+__device__ __forceinline__ void v4_track(const V4Ctx &, int, const u64 (&U)[2], float &mx)
+{
+    mx = fmaxf(fmaxf(mx, fabsf(lo32(U[0]))), fabsf(hi32(U[0])));
+    mx = fmaxf(fmaxf(mx, fabsf(lo32(U[1]))), fabsf(hi32(U[1])));
+}
+
+// level k (ring Lk) at row r = s - D from ring Lp (level k - 1) and momentum
+// pairs M; Q = (s - y_start) & 3 selects the ring slots at compile time;
+// pub = where the new row's edge columns go (nullptr: no consumer)
+template <int Q, int D, int KL, bool FAST>
+__device__ __forceinline__ void v4_level(const V4Ctx &c, int s, u64 (&Lk)[4][2], const u64 (&Lp)[4][2],
+                                         const u64 (&M)[2], const u64 (&AR)[3][2], float wv, float ev,
+                                         float *pub, float &mx)
+{
+    constexpr int SR = (Q - D + 64) & 3;
+    const int r = s - D;
+    if (FAST) {
+        // steady state: every level in range, no ghost row, all 8 levels live
+        v4_update(c, Lp[SR], Lp[(SR + 3) & 3], Lp[(SR + 1) & 3], M, AR, wv, ev, Lk[SR]);
+        v4_track(c, r, Lk[SR], mx);
+        if (pub) v4_pub(c, pub, Lk[SR]);
+        return;
+    }
+    if (r >= v4_lo(c, KL) && r <= v4_hi(c, KL)) {
+        if (KL <= c.iters) {
+            v4_update(c, Lp[SR], Lp[(SR + 3) & 3], Lp[(SR + 1) & 3], M, AR, wv, ev, Lk[SR]);
+            v4_track(c, r, Lk[SR], mx);
+        } else {
+            v4_cp(Lk[SR], Lp[SR]);  // partial last pass: levels above `iters` copy
+        }
+        if (pub) v4_pub(c, pub, Lk[SR]);
+        if (r == 0) v4_cp(Lk[(SR + 3) & 3], Lk[SR]);  // ghost row -1
+    } else if (r == c.h && v4_hi(c, KL) == c.h - 1) {
+        v4_cp(Lk[SR], Lk[(SR + 3) & 3]);  // ghost row h
+    }
+}
+
+struct V4G0 {
+    u64 L0[4][2], L1[4][2], L2[4][2], L3[4][2];
+    u64 AR[4][3][2];
+    u64 OP[2];
+};
+struct V4G1 {
+    u64 L4[4][2], L3[4][2], L5[4][2], L6[4][2], L7[4][2];
+    u64 AR[4][3][2];
+};
+
+// group 0 (levels 1-4) at step s
+template <int Q, bool FAST>
+__device__ __forceinline__ void v4_g0_step(const V4Ctx &c, V4G0 &g, int s, float &mx)
+{
+    using namespace v4;
+    // neighbours of the rows levels 0..3 produced in the previous step
+    const int pp = (s - 1) & 1, pn = s & 1;
+    float wv[4], ev[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v4_nb(c, v4_e(c, pp, k), wv[k], ev[k]);
+    // level 0: the pass input O, row s
+    if (FAST) {
+        if (Q == 0 && s <= c.y_last0) v4_wait_row(c, s);  // fast steps start chunk-aligned
+        v4_ld(c, v4_off(c, s, 0), g.L0[Q]);
+        v4_pub(c, v4_e(c, pn, 0), g.L0[Q]);
+    } else if (s <= v4_hi(c, 0)) {
+        v4_wait_row(c, s);
+        v4_ld(c, v4_off(c, s, 0), g.L0[Q]);
+        v4_pub(c, v4_e(c, pn, 0), g.L0[Q]);
+        if (s == 0) v4_cp(g.L0[(Q + 3) & 3], g.L0[Q]);
+    } else if (s == c.h) {
+        v4_cp(g.L0[Q], g.L0[(Q + 3) & 3]);
+    }
+    // row s - 1: O_prev (level 1's momentum input) and A / lapP / wc
+    const int r1 = s - 1;
+    if (FAST || (r1 >= v4_lo(c, 1) && r1 <= v4_hi(c, 1))) {
+        const uint32_t o1 = v4_off(c, r1, 1);
+        v4_ld(c, o1, g.OP);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) v4_ld(c, o1 + (p + 1) * CH * SW * 4, g.AR[(Q + 3) & 3][p]);
+    }
+    v4_level<Q, 1, 1, FAST>(c, s, g.L1, g.L0, g.OP, g.AR[(Q + 3) & 3], wv[0], ev[0], v4_e(c, pn, 1), mx);
+    v4_level<Q, 2, 2, FAST>(c, s, g.L2, g.L1, g.L0[(Q + 2) & 3], g.AR[(Q + 2) & 3], wv[1], ev[1],
+                            v4_e(c, pn, 2), mx);
+    v4_level<Q, 3, 3, FAST>(c, s, g.L3, g.L2, g.L1[(Q + 1) & 3], g.AR[(Q + 1) & 3], wv[2], ev[2],
+                            v4_e(c, pn, 3), mx);
+    // level 4 (row s - 4): straight into the handoff ring with level 3's row
+    const int r4 = s - 4;
+    if (FAST || (r4 >= v4_lo(c, 4) && r4 <= v4_hi(c, 4))) {
+        constexpr int SR = Q;  // (Q - 4) & 3
+        u64 U[2];
+        if (FAST || 4 <= c.iters) {
+            v4_update(c, g.L3[SR], g.L3[(SR + 3) & 3], g.L3[(SR + 1) & 3], g.L2[SR], g.AR[SR], wv[3], ev[3], U);
+            v4_track(c, r4, U, mx);
+        } else {
+            v4_cp(U, g.L3[SR]);
+        }
+        v4_pub(c, v4_e4(c, s & 3), U);
+        float *hd = c.hand + (r4 & (HAND - 1)) * 2 * SW + c.col;
+        *reinterpret_cast<float4 *>(hd) = make_float4(lo32(U[0]), hi32(U[0]), lo32(U[1]), hi32(U[1]));
+        *reinterpret_cast<float4 *>(hd + SW) =
+            make_float4(lo32(g.L3[SR][0]), hi32(g.L3[SR][0]), lo32(g.L3[SR][1]), hi32(g.L3[SR][1]));
+    }
+}
+
+// group 1 (levels 5-8) at step s; level 8 and its level-7 row are the pass outputs
+template <int Q, bool FAST>
+__device__ __forceinline__ void v4_g1_step(const V4Ctx &c, V4G1 &g, const BlockedArgs &a, int ch,
+                                           int gx0, int s, float &mx, bool &nan_seen)
+{
+    using namespace v4;
+    const int pp = (s - 1) & 1, pn = s & 1;
+    float wv[4], ev[4];
+    v4_nb(c, v4_e4(c, (s - 2) & 3), wv[0], ev[0]);  // level 4, produced two steps ago
+#pragma unroll
+    for (int k = 1; k < 4; ++k) v4_nb(c, v4_e(c, pp, 4 + k), wv[k], ev[k]);
+    // receive level 4 / level 3 row s - 5
+    {
+        constexpr int SR = (Q + 3) & 3;
+        const int r = s - 5;
+        if (FAST || (r >= v4_lo(c, 4) && r <= v4_hi(c, 4))) {
+            const uint32_t ho = (uint32_t)((r & (HAND - 1)) * 2 * SW * 4);
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(g.L4[SR][0]) : "r"(c.hd0 + ho) : "memory");
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(g.L4[SR][1]) : "r"(c.hd1 + ho) : "memory");
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(g.L3[SR][0]) : "r"(c.hd0 + ho + SW * 4) : "memory");
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(g.L3[SR][1]) : "r"(c.hd1 + ho + SW * 4) : "memory");
+            if (!FAST && r == 0) v4_cp(g.L4[(SR + 3) & 3], g.L4[SR]);
+        } else if (r == c.h && v4_hi(c, 4) == c.h - 1) {
+            v4_cp(g.L4[SR], g.L4[(SR + 3) & 3]);
+        }
+    }
+    // A / lapP / wc of row s - 6
+    {
+        const int r = s - 6;
+        if (FAST || (r >= v4_lo(c, 5) && r <= v4_hi(c, 5))) {
+            // no wait: group 0 waited for this chunk at least 5 CTA barriers ago
+#pragma unroll
+            for (int p = 0; p < 3; ++p) v4_ld(c, v4_off(c, r, 2 + p), g.AR[(Q + 2) & 3][p]);
+        }
+    }
+    v4_level<Q, 6, 5, FAST>(c, s, g.L5, g.L4, g.L3[(Q + 2) & 3], g.AR[(Q + 2) & 3], wv[0], ev[0],
+                            v4_e(c, pn, 5), mx);
+    v4_level<Q, 7, 6, FAST>(c, s, g.L6, g.L5, g.L4[(Q + 1) & 3], g.AR[(Q + 1) & 3], wv[1], ev[1],
+                            v4_e(c, pn, 6), mx);
+    v4_level<Q, 8, 7, FAST>(c, s, g.L7, g.L6, g.L5[Q], g.AR[Q], wv[2], ev[2], v4_e(c, pn, 7), mx);
+    // level 8 (row s - 9) -> the pass outputs
+    const int r8 = s - 9;
+    if (FAST || (r8 >= v4_lo(c, 8) && r8 <= v4_hi(c, 8))) {
+        constexpr int SR = (Q + 3) & 3;
+        u64 U[2];
+        if (FAST || 8 <= c.iters) {
+            v4_update(c, g.L7[SR], g.L7[(SR + 3) & 3], g.L7[(SR + 1) & 3], g.L6[SR], g.AR[SR], wv[3], ev[3], U);
+            v4_track(c, r8, U, mx);
+        } else {
+            v4_cp(U, g.L7[SR]);
+        }
+        if (c.colc && r8 >= c.seg_y0 && r8 < c.seg_y1) {
+            const float o[4] = {lo32(U[0]), hi32(U[0]), lo32(U[1]), hi32(U[1])};
+            nan_seen |= o[0] != o[0] || o[1] != o[1] || o[2] != o[2] || o[3] != o[3];
+            const long q = (long)r8 * a.w + gx0;
+            if (a.hwc_out) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a.hwc_out[(q + j) * a.c + ch] = fminf(fmaxf(o[j], 0.0f), 1.0f);
+            } else {
+                const long plane = (long)ch * a.h * a.w;
+                *reinterpret_cast<float4 *>(a.Oout + plane + q) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4 *>(a.Oprev_out + plane + q) =
+                    make_float4(lo32(g.L7[SR][0]), hi32(g.L7[SR][0]), lo32(g.L7[SR][1]), hi32(g.L7[SR][1]));
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void tma_load_3d_pol(float *dst, const CUtensorMap *map, int x, int y, int z,
+                                                uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+        :
+        : "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z),
+          "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_pol(float *dst, const CUtensorMap *map, int x, int y,
+                                                uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        :
+        : "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
+          "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(v4::THREADS, 2)
+    k_sgd_v4(const __grid_constant__ TmaMaps maps, BlockedArgs a, int n_strips, int seg_len, uint32_t o8)
+{
+    using namespace v4;
+    extern __shared__ __align__(1024) float smem_v4[];
+    V4Ctx c;
+    c.ring = smem_v4;
+    c.hand = c.ring + RING * ROWF;
+    c.edge = c.hand + HAND * 2 * SW;
+    c.full = reinterpret_cast<uint64_t *>(c.edge + EDGEF);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int xh = warp & 1, grp = warp >> 1;
+    const int n_segs = (a.h + seg_len - 1) / seg_len;
+    const int u = blockIdx.x;
+    const int ch = u / (n_strips * n_segs);
+    const int rem = u - ch * n_strips * n_segs;
+    const int seg = rem / n_strips, strip = rem - seg * n_strips;
+    const int x0 = strip * OW - K;
+    c.seg_y0 = seg * seg_len;
+    c.seg_y1 = min(a.h, c.seg_y0 + seg_len);
+    c.h = a.h;
+    c.w = a.w;
+    c.y_start = max(0, c.seg_y0 - K);
+    const int y_last0 = min(a.h - 1, c.seg_y1 - 1 + K);
+    c.y_last0 = y_last0;
+    c.col = xh * 128 + 4 * lane;
+    const int gx0 = x0 + c.col;
+    c.lft = gx0 == 0;
+    c.rgt = gx0 + 4 == a.w;
+    c.colc = gx0 >= x0 + K && gx0 + 4 <= x0 + SW - K && gx0 >= 0 && gx0 + 4 <= a.w;
+    c.ld0 = smem_u32(c.ring + c.col);
+    c.ld1 = c.ld0 + o8;  // == ld0 + 8, opaque to ptxas
+    c.hd0 = smem_u32(c.hand + c.col);
+    c.hd1 = c.hd0 + o8;
+    c.L = xh * 32 + lane;
+    c.iters = a.iters;
+    c.k.eta = pk(a.eta, a.eta);
+    c.k.kap = pk(a.kappa, a.kappa);
+    c.k.m4 = pk(-4.0f, -4.0f);
+    c.k.z = pk(a.negzero, a.negzero);
+
+    uint64_t pol_first, pol_last;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+    const bool issuer = threadIdx.x == 0;
+    // chunk j = rows y_start + 4j .. + 3; the pass-invariant planes first
+    auto issue_const = [&](int j) {
+        const int slot = j & (NCH - 1), r = c.y_start + CH * j;
+        float *dst = c.ring + slot * PLANES * CH * SW;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(smem_u32(c.full + slot)), "r"(CHUNK_TX) : "memory");
+        tma_load_3d_pol(dst + 2 * CH * SW, &maps.A, x0, r, ch, c.full + slot, pol_last);
+        tma_load_3d_pol(dst + 3 * CH * SW, &maps.L, x0, r, ch, c.full + slot, pol_last);
+        tma_load_2d_pol(dst + 4 * CH * SW, &maps.W, x0, r, c.full + slot, pol_last);
+    };
+    auto issue_iter = [&](int j) {
+        const int slot = j & (NCH - 1), r = c.y_start + CH * j;
+        float *dst = c.ring + slot * PLANES * CH * SW;
+        tma_load_3d_pol(dst + 0 * CH * SW, &maps.O, x0, r, ch, c.full + slot, pol_first);
+        tma_load_3d_pol(dst + 1 * CH * SW, &maps.Op, x0, r, ch, c.full + slot, pol_first);
+    };
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int i = threadIdx.x; i < EDGEF + HAND * 2 * SW; i += THREADS) c.hand[i] = 0.0f;
+    // ring slots 2 and 3 hold "rows" y_start - 8 .. - 1 until chunks 2 and 3
+    // arrive: read as ramp garbage by the fast steps, they must be finite
+    for (int i = threadIdx.x; i < 2 * PLANES * CH * SW / 4; i += THREADS)
+        reinterpret_cast<float4 *>(c.ring + 2 * PLANES * CH * SW)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (issuer) {
+        for (int i = 0; i < NCH; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(c.full + i)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // the pass-invariant planes of the first chunks load while the previous pass drains
+        for (int j = 0; j < 2 && c.y_start + CH * j <= y_last0; ++j) issue_const(j);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int j = 0; j < 2 && c.y_start + CH * j <= y_last0; ++j) issue_iter(j);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __syncthreads();
+
+    const int s_end = c.seg_y1 + K;  // level 8 reaches row seg_y1 - 1
+    // Fast (branch-free) steps compute every level on every step: rows
+    // outside a level's valid cone are garbage that never reaches a committed
+    // row (the cone argument of the apron), no chunk is waited for that was
+    // not issued, and tracking / stores look at committed rows only.  Slow
+    // steps remain where a ghost row is written (a level at row 0 or row h:
+    // image top / bottom), and for a partial pass (levels above `iters` copy).
+    int f_lo = 1 << 30, f_hi = -(1 << 30);
+    if (a.iters == K) {
+        f_lo = c.y_start == 0 ? (grp == 0 ? 8 : 12) : c.y_start;  // past the row-0 ghost steps, phase 0
+        f_hi = y_last0 == a.h - 1 ? (grp == 0 ? a.h - 1 : a.h + 4) : (1 << 30);
+    }
+    float mx = 0.0f;
+    bool nan_seen = false;
+    // at the third step of chunk j, chunk j + 2 goes into the slot chunk j - 2
+    // held (its last row was last read, by group 1, one step earlier)
+    auto issue_ahead = [&](int s) {
+        const int n = s - c.y_start;
+        const int j = (n >> 2) + 2;
+        if (issuer && (n & 3) == 2 && c.y_start + CH * j <= y_last0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_const(j);
+            issue_iter(j);
+        }
+    };
+    // Steps run as: slow (range-checked) steps until the phase is 0 inside
+    // the fast window, then the fast steps four at a time as straight-line
+    // code (the ring phase is compile-time in each), then slow steps to the
+    // end.  Keeping the hot loop free of the slow variants' code matters:
+    // interleaved, instruction fetch stalls dominated.
+    // (both groups run the same steps: the fast loop may overshoot s_end by up
+    // to 3 garbage steps, except in a segment at the image bottom)
+    const int s_last = f_hi > a.h + 8 ? c.y_start + ((s_end - c.y_start + 4) & ~3) - 1 : s_end;
+    auto aligned_fast = [&](int s) { return ((s - c.y_start) & 3) == 0 && s >= f_lo && s + 3 <= f_hi; };
+    if (grp == 0) {
+        V4G0 g;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                g.L0[i][j] = g.L1[i][j] = g.L2[i][j] = g.L3[i][j] = 0ull;
+                g.AR[i][0][j] = g.AR[i][1][j] = g.AR[i][2][j] = 0ull;
+            }
+        }
+        g.OP[0] = g.OP[1] = 0ull;
+        auto slow = [&](int s) {
+            issue_ahead(s);
+            switch ((s - c.y_start) & 3) {
+            case 0: v4_g0_step<0, false>(c, g, s, mx); break;
+            case 1: v4_g0_step<1, false>(c, g, s, mx); break;
+            case 2: v4_g0_step<2, false>(c, g, s, mx); break;
+            default: v4_g0_step<3, false>(c, g, s, mx); break;
+            }
+            __syncthreads();
+        };
+        int s = c.y_start;
+        for (; s <= s_last && !aligned_fast(s); ++s) slow(s);
+        for (; s <= s_last && s + 3 <= f_hi; s += 4) {
+            v4_g0_step<0, true>(c, g, s, mx);
+            __syncthreads();
+            v4_g0_step<1, true>(c, g, s + 1, mx);
+            __syncthreads();
+            issue_ahead(s + 2);
+            v4_g0_step<2, true>(c, g, s + 2, mx);
+            __syncthreads();
+            v4_g0_step<3, true>(c, g, s + 3, mx);
+            __syncthreads();
+        }
+        for (; s <= s_last; ++s) slow(s);
+    } else {
+        V4G1 g;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                g.L4[i][j] = g.L3[i][j] = g.L5[i][j] = g.L6[i][j] = g.L7[i][j] = 0ull;
+                g.AR[i][0][j] = g.AR[i][1][j] = g.AR[i][2][j] = 0ull;
+            }
+        }
+        auto slow = [&](int s) {
+            switch ((s - c.y_start) & 3) {
+            case 0: v4_g1_step<0, false>(c, g, a, ch, gx0, s, mx, nan_seen); break;
+            case 1: v4_g1_step<1, false>(c, g, a, ch, gx0, s, mx, nan_seen); break;
+            case 2: v4_g1_step<2, false>(c, g, a, ch, gx0, s, mx, nan_seen); break;
+            default: v4_g1_step<3, false>(c, g, a, ch, gx0, s, mx, nan_seen); break;
+            }
+            __syncthreads();
+        };
+        int s = c.y_start;
+        for (; s <= s_last && !aligned_fast(s); ++s) slow(s);
+        for (; s <= s_last && s + 3 <= f_hi; s += 4) {
+            v4_g1_step<0, true>(c, g, a, ch, gx0, s, mx, nan_seen);
+            __syncthreads();
+            v4_g1_step<1, true>(c, g, a, ch, gx0, s + 1, mx, nan_seen);
+            __syncthreads();
+            v4_g1_step<2, true>(c, g, a, ch, gx0, s + 2, mx, nan_seen);
+            __syncthreads();
+            v4_g1_step<3, true>(c, g, a, ch, gx0, s + 3, mx, nan_seen);
+            __syncthreads();
+        }
+        for (; s <= s_last; ++s) slow(s);
+    }
+    push_maxbits(nan_seen ? 0x7fffffffu : __float_as_uint(mx), a.maxbits);
+}
+
+// strips x segments x channels, one CTA each, 2 CTAs per SM: as many row
+// segments as fill the SMs once (the segment ramps are the only vertical
+// redundancy, so fewer, longer segments are better)
+static void v4_grid(int h, int w, int c, int n_sm, int &n_strips, int &seg_len, int &n_units)
+{
+    n_strips = (w + v4::OW - 1) / v4::OW;
+    int n_segs = std::max(1, (2 * n_sm) / (c * n_strips));
+    n_segs = std::min(n_segs, std::max(1, h / 32));
+    seg_len = (h + n_segs - 1) / n_segs;
+    n_segs = (h + seg_len - 1) / seg_len;
+    n_units = c * n_strips * n_segs;
+}
+
+static int launch_v4(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
+{
+    static bool attr = false;
+    if (!attr) {
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_v4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v4::SMEM));
+        // two CTAs per SM need the full shared-memory carve-out
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_v4, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        if (getenv("SS_SOLVER_DEBUG")) {
+            int nb = 0;
+            SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sgd_v4, v4::THREADS, v4::SMEM));
+            fprintf(stderr, "[solver] k_sgd_v4: %d CTAs per SM, %zu B shared each\n", nb, v4::SMEM);
+        }
+        attr = true;
+    }
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        SS_CUDA_TRY(cudaGetDevice(&dev));
+        SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    int n_strips, seg_len, n_units;
+    v4_grid(a.h, a.w, a.c, n_sm, n_strips, seg_len, n_units);
+    static bool said = false;
+    if (!said && getenv("SS_SOLVER_DEBUG")) {
+        fprintf(stderr, "[solver] k_sgd_v4: %d strips, segments of %d rows, %d CTAs\n", n_strips, seg_len, n_units);
+        said = true;
+    }
+    return fn::launch_pdl("k_sgd_v4", k_sgd_v4, dim3(n_units), dim3(v4::THREADS), v4::SMEM, st, maps, a,
+                          n_strips, seg_len, (uint32_t)8);
+}
+
 // tensor maps over planar (c, h, w) float32 arrays (cuTensorMapEncodeTiled
 // through the runtime's driver entry point; no -lcuda)
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
@@ -1330,7 +1923,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
     return fn;
 }
 
-static int make_map(CUtensorMap *m, const float *base, int w, int h, int c, bool planes)
+static int make_map(CUtensorMap *m, const float *base, int w, int h, int c, bool planes,
+                    int box_w = blk::RW, int box_h = blk::RH)
 {
     auto fn = encode_fn();
     if (!fn) {
@@ -1339,7 +1933,7 @@ static int make_map(CUtensorMap *m, const float *base, int w, int h, int c, bool
     }
     const cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)c};
     const cuuint64_t strides[2] = {(cuuint64_t)w * 4, (cuuint64_t)w * h * 4};
-    const cuuint32_t box[3] = {blk::RW, blk::RH, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, planes ? 3 : 2,
                           const_cast<float *>(base), dims, strides, box, estr,
@@ -1560,7 +2154,8 @@ int solver_variant()
     // 0 = streaming (one iteration per launch), 1 = blocked LDG, 2 = blocked
     // TMA (2 x 8 blocks), 3 = v2 (4 x 8 blocks; w % 4 == h % 8 == 0), 4 = v2
     // with 4 x 4 blocks (h % 4 == 0), 5 = v3 (v2 on 2-CTA clusters; measured
-    // slower than v2 at 1080p, see the v3 comment)
+    // slower than v2 at 1080p, see the v3 comment), 6 = v4 (row streaming;
+    // w % 4 == 0)
     static int v = [] {
         const char *e = getenv("SS_SOLVER");
         if (e && !strcmp(e, "stream")) return 0;
@@ -1568,6 +2163,7 @@ int solver_variant()
         if (e && !strcmp(e, "tma")) return 2;
         if (e && !strcmp(e, "v2r4")) return 4;
         if (e && !strcmp(e, "v3")) return 5;
+        if (e && !strcmp(e, "v4")) return 6;
         return 3;
     }();
     return v;
@@ -1646,9 +2242,10 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
     const long hw = (long)wk.h * wk.w;
     const long n = hw * wk.c;
     int variant = solver_variant();
+    if (variant == 6 && (wk.w % 4 != 0 || !encode_fn())) variant = 3;
     if (variant == 5 && wk.h % 8 != 0) variant = 4;  // v3 (pairs of 4x8 blocks) needs h % 8 == 0
     if (variant == 3 && wk.h % 8 != 0) variant = 4;  // RB = 8 needs h % 8 == 0
-    if (variant >= 3 && (wk.w % 4 != 0 || wk.h % 4 != 0)) variant = 2;
+    if (variant >= 3 && variant != 6 && (wk.w % 4 != 0 || wk.h % 4 != 0)) variant = 2;
     if (variant >= 2 && (wk.w % 4 != 0 || !encode_fn())) variant = 1;
     const int K = variant >= 3 ? v2::K : variant == 2 ? tma_k() : K_LDG;
     const int n_pass = variant ? (iters + K - 1) / K : 0;
@@ -1657,17 +2254,19 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
         SS_CUDA_TRY(cudaMemsetAsync(wk.maxbits, 0, (size_t)n_pass * sizeof(unsigned), st));
         TmaMaps m_init, m_set[2];
         if (variant >= 2) {
+            // v4 streams rows: one 256 x 4 box per plane and chunk
+            const int bw = variant == 6 ? v4::SW : blk::RW, bh = variant == 6 ? v4::CH : blk::RH;
             TmaMaps base;
-            if ((rc = make_map(&base.A, A, wk.w, wk.h, wk.c, true))) return rc;
-            if ((rc = make_map(&base.L, lapP, wk.w, wk.h, wk.c, true))) return rc;
-            if ((rc = make_map(&base.W, wc, wk.w, wk.h, 1, false))) return rc;
+            if ((rc = make_map(&base.A, A, wk.w, wk.h, wk.c, true, bw, bh))) return rc;
+            if ((rc = make_map(&base.L, lapP, wk.w, wk.h, wk.c, true, bw, bh))) return rc;
+            if ((rc = make_map(&base.W, wc, wk.w, wk.h, 1, false, bw, bh))) return rc;
             m_init = base;
-            if ((rc = make_map(&m_init.O, init, wk.w, wk.h, wk.c, true))) return rc;
+            if ((rc = make_map(&m_init.O, init, wk.w, wk.h, wk.c, true, bw, bh))) return rc;
             m_init.Op = m_init.O;
             for (int k = 0; k < 2; ++k) {
                 m_set[k] = base;
-                if ((rc = make_map(&m_set[k].O, wk.O[k][0], wk.w, wk.h, wk.c, true))) return rc;
-                if ((rc = make_map(&m_set[k].Op, wk.O[k][1], wk.w, wk.h, wk.c, true))) return rc;
+                if ((rc = make_map(&m_set[k].O, wk.O[k][0], wk.w, wk.h, wk.c, true, bw, bh))) return rc;
+                if ((rc = make_map(&m_set[k].Op, wk.O[k][1], wk.w, wk.h, wk.c, true, bw, bh))) return rc;
             }
         } else {
             static bool attr = false;
@@ -1703,7 +2302,8 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
                         getenv("SS_SOLVER_ALIGNED") == nullptr;
             if (variant >= 3) {
                 const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];
-                rc = variant == 5 ? launch_v3(mp, a, st)
+                rc = variant == 6 ? launch_v4(mp, a, st)
+                     : variant == 5 ? launch_v3(mp, a, st)
                      : variant == 3 ? launch_v2<8>(mp, a, st) : launch_v2<4>(mp, a, st);
                 if (rc) return rc;
             } else if (variant == 2) {

@@ -347,12 +347,13 @@ def test_solver_v2_aligned_shapes_bitwise(ss, shape):
         assert np.array_equal(got, want), (shape, iters)
 
 
-@pytest.mark.parametrize("variant", ["v2", "v3"])
+@pytest.mark.parametrize("variant", ["v2", "v3", "v4"])
 def test_solver_many_tiles_per_cta_bitwise(ss, variant):
     """600x800x3 in a subprocess per schedule: v2 walks 8 x 13 x 3 = 312 tiles
     over 148 CTAs, v3 144 tiles over at most 74 CTA pairs (seam-row counters
-    and receive-slot parities carried across tiles); 5 and 150 iterations,
-    bit for bit."""
+    and receive-slot parities carried across tiles), v4 streams 4 strips x 18
+    segments x 3 channels (34-row segments: ramps, chunk phases and the
+    image-edge ghost rows all exercised); 5 and 150 iterations, bit for bit."""
     import os
     import subprocess
     import sys
@@ -426,6 +427,16 @@ for shape in [(61, 200, 3), (130, 124, 1), (47, 301, 3), (64, 200, 3), (132, 124
         got = ss.solve_screened_poisson(p, a, wc, ss.ConsistencyParams(iterations=it), a)
         want = orc.solve_screened_poisson(p, a, wc, orc.Params(iterations=it))
         assert np.array_equal(got, want), (shape, it)
+# the golden divergence cases: the schedule's per-pass maxima must send them
+# to the exact replay, which reports the reference's iteration
+g = np.load(sys.argv[1] + '/tests/golden/solver.npz')
+for i in range(3):
+    try:
+        ss.solve_screened_poisson(g[f"div{i}_P"], g[f"div{i}_A"], g[f"div{i}_wc"],
+                                  ss.ConsistencyParams(iterations=int(g[f"div{i}_iters"])), g[f"div{i}_A"])
+        raise AssertionError(f"div{i}: no divergence")
+    except ss.SolverDivergence as e:
+        assert e.iteration == int(g[f"div{i}_iteration"]), (i, e.iteration)
 print("ok")
 """
 
@@ -433,11 +444,12 @@ print("ok")
 @pytest.mark.parametrize("env", [{"SS_SOLVER": "stream"}, {"SS_SOLVER": "ldg"},
                                  {"SS_SOLVER": "tma", "SS_SOLVER_K": "4"},
                                  {"SS_SOLVER": "tma", "SS_SOLVER_K": "8"}, {"SS_SOLVER": "v2"},
-                                 {"SS_SOLVER": "v2r4"}, {"SS_SOLVER": "v3"}])
+                                 {"SS_SOLVER": "v2r4"}, {"SS_SOLVER": "v3"}, {"SS_SOLVER": "v4"}])
 def test_solver_variants_bitwise(ss, env):
     """Every solver schedule (streaming, blocked LDG, blocked TMA at K = 4/8,
     v2 with 4x8 (default) and 4x4 blocks, v3 = v2 on 2-CTA clusters with a
-    DSMEM seam-row exchange) produces the reference's bits."""
+    DSMEM seam-row exchange, v4 = time-skewed row streaming) produces the
+    reference's bits and divergence iterations."""
     import os
     import subprocess
     import sys
