@@ -879,6 +879,320 @@ static int launch_v2(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
 }
 
 // ---------------------------------------------------------------------------
+// mp: every pass of the solve in ONE persistent launch of the v2 tile kernel
+// (round 2).  Launched a pass per kernel, v2 pays a tail per pass (1242 1080p
+// tiles over 148 CTAs: 8.4 rounds -> 9, the last with 58 CTAs busy) and a
+// kernel boundary.  Here the (pass, tile) items are claimed in order from an
+// atomic queue, and an item of pass p > 0 starts once the tile rows around it
+// (a superset of the 3 x 3 tiles its 8-pixel apron reaches) finished pass
+// p - 1, counted per (pass, channel, tile row) -- so the next pass runs in
+// the previous one's tail.  Claims are in order: every tile an item
+// waits on is held by a CTA that is already running it, so there is no
+// deadlock even when some CTAs are not resident.  Pass p writes set p & 1 and
+// reads set (p - 1) & 1 (pass 0 reads init); a pass-(p + 1) tile overwrites
+// set (p - 1) & 1 only after its 3 x 3 neighbourhood finished pass p, i.e.
+// after every read of that region by pass p.  The next item's tile load is
+// issued at the tile start, as v2 prefetches.
+//
+// Measured (B200, 1080p, 150 iterations): 1.22 ms against v2's 1.06 ms, so v2
+// stays the default (SS_SOLVER=mp selects this one).  The tail it removes is
+// ~7% of a pass, but the scheduling thread's work sits on the CTA's critical
+// path -- every warp computes, so any wait of thread 0 (the queue atomic, the
+// release of a finished tile, the dependency loads) holds the whole CTA at the
+// next iteration barrier: barrier stalls 16% (v2: 7%), and the bookkeeping
+// raised the kernel to 252 registers.  Steps taken: 1.47 (nine acquire loads
+// tested on the spot) -> 1.28 (row counters loaded a tile ahead, the claim a
+// tile ahead) -> 1.22 ms (relaxed loads, release without a separate fence).
+struct MpMaps {
+    TmaMaps init, set[2];  // pass 0 reads init; pass p reads set[(p - 1) & 1]
+};
+struct MpArgs {
+    BlockedArgs a;           // geometry, eta / kappa / negzero, hwc_out (last pass)
+    float *Oout[2], *Opout[2];
+    int npass, iters_last;   // passes of K = 8 iterations; the last runs iters_last
+    unsigned *maxbits;       // [npass]
+    int *rows_done;          // [npass][c][tile rows]: tiles written, zero at launch
+    int *queue;              // item counter, zero at launch
+};
+
+// A relaxed load: an acquire would hold thread 0 (and so its warp and the
+// CTA's next barrier) for the L2 round trip.  The tile loads it gates are TMA
+// reads, which go to L2, where the producers' release put their stores before
+// the count moved; fence.proxy.async.global orders them after this load.
+__device__ __forceinline__ int ld_relaxed_gpu(const int *p)
+{
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int RB>
+__global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
+    k_sgd_mp(const __grid_constant__ MpMaps maps, MpArgs m)
+{
+    using namespace v2;
+    constexpr int NW = Cfg<RB>::NW, NP = Cfg<RB>::NP, THREADS = Cfg<RB>::THREADS, PAR = Cfg<RB>::PAR;
+    extern __shared__ __align__(1024) float smem_mp[];
+    float *stage = smem_mp;              // 5 x (RH x RW)
+    float *rows = stage + 5 * STAGE;     // 2 parities x PAR
+    uint64_t *bar = reinterpret_cast<uint64_t *>(rows + 2 * PAR);
+    int *sh_next = reinterpret_cast<int *>(bar + 1);
+    const BlockedArgs &a = m.a;
+    const int lane = threadIdx.x, wp = threadIdx.y;
+    const int tid = wp * 32 + lane;
+    const int ntx = (a.w + OW - 1) / OW, nty = (a.h + OH - 1) / OH;
+    const int ntiles = ntx * nty * a.c, nitems = m.npass * ntiles;
+    constexpr uint32_t TX_BYTES = 5u * STAGE * sizeof(float);
+
+    auto coords = [&](int t, int &ch, int &x, int &y) {
+        ch = t / (ntx * nty);
+        const int rem = t - ch * ntx * nty;
+        const int ty = rem / ntx, tx = rem - ty * ntx;
+        x = tx * OW - K;
+        y = ty * OH - K;
+    };
+    auto issue = [&](int item) {
+        const int pass = item / ntiles, t = item - pass * ntiles;
+        const TmaMaps &mp = pass == 0 ? maps.init : maps.set[(pass - 1) & 1];
+        int ch, x, y;
+        coords(t, ch, x, y);
+        // the region was written by other CTAs' generic stores (acquired
+        // through the flags): order them before these async-proxy reads
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(smem_u32(bar)), "r"(TX_BYTES) : "memory");
+        tma_load_3d(stage + 0 * STAGE, &mp.O, x, y, ch, bar);
+        tma_load_3d(stage + 1 * STAGE, &mp.Op, x, y, ch, bar);
+        tma_load_3d(stage + 2 * STAGE, &mp.A, x, y, ch, bar);
+        tma_load_3d(stage + 3 * STAGE, &mp.L, x, y, ch, bar);
+        tma_load_2d(stage + 4 * STAGE, &mp.W, x, y, bar);
+    };
+    // Dependencies through per-(pass, channel, tile row) completion counts:
+    // an item of pass p > 0 needs the tile rows ty - 1 .. ty + 1 of pass p - 1
+    // complete (a superset of its 3 x 3 neighbourhood, and as good: those rows
+    // were claimed ~a pass earlier).  rv = the counts of the next item's rows,
+    // loaded a tile ahead so the test at the tile start does not wait.
+    int rv[3];
+    auto rows_load = [&](int item) {
+        rv[0] = rv[1] = rv[2] = ntx;
+        const int pass = item / ntiles;
+        if (pass == 0 || item >= nitems) return;
+        const int t = item - pass * ntiles;
+        const int ch = t / (ntx * nty), ty = (t - ch * ntx * nty) / ntx;
+        const int *r = m.rows_done + ((size_t)(pass - 1) * a.c + ch) * nty;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const int yy = ty + i - 1;
+            if (yy >= 0 && yy < nty) rv[i] = ld_relaxed_gpu(r + yy);
+        }
+    };
+    auto rows_ok = [&]() { return rv[0] >= ntx && rv[1] >= ntx && rv[2] >= ntx; };
+    int pend = -1;  // item whose completion is not yet published
+    auto publish = [&](int it_) {
+        const int pass = it_ / ntiles, t = it_ - pass * ntiles;
+        const int ch = t / (ntx * nty), ty = (t - ch * ntx * nty) / ntx;
+        // the release is cumulative over every thread's stores of the tile
+        // (ordered before it by the barrier that follows them)
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(m.rows_done + ((size_t)pass * a.c + ch) * nty + ty)
+                     : "memory");
+    };
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int i = tid; i < 2 * PAR; i += THREADS) rows[i] = 0.0f;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    int n1 = 0;  // thread 0: the item after the current one
+    if (tid == 0) {
+        const int item = atomicAdd(m.queue, 1);
+        n1 = atomicAdd(m.queue, 1);
+        if (item < nitems) {
+            do rows_load(item); while (!rows_ok());
+            issue(item);
+        }
+        rows_load(n1);
+        *sh_next = item;
+    }
+    __syncthreads();
+
+    V2Consts kc;
+    kc.eta = pk(a.eta, a.eta);
+    kc.kap = pk(a.kappa, a.kappa);
+    kc.m4 = pk(-4.0f, -4.0f);
+    kc.z = pk(a.negzero, a.negzero);
+    const bool interior = lane >= K / 4 && lane < 32 - K / 4 && wp >= K / RB && wp < NW - K / RB;
+    uint32_t phase = 0;
+    unsigned bits = 0;
+    int bits_pass = -1;
+    int item = *sh_next;
+    while (item < nitems) {
+        const int pass = item / ntiles, t = item - pass * ntiles;
+        const bool last = pass == m.npass - 1;
+        const int iters = last ? m.iters_last : K;
+        int ch, rx0, ry0;
+        coords(t, ch, rx0, ry0);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        u64 X[4][NP], Y[4][NP], Av[4][NP], Lv[4][NP], Wv[4][NP];
+        {
+            auto ld = [&](int arr, u64 (&D)[4][NP]) {
+#pragma unroll
+                for (int r = 0; r < NP; ++r) {
+                    const float *plo = stage + arr * STAGE + (RB * wp + r) * RW + 4 * lane;
+                    const float4 lo = *reinterpret_cast<const float4 *>(plo);
+                    const float4 hi = *reinterpret_cast<const float4 *>(plo + NP * RW);
+                    D[0][r] = pk_reg(lo.x, hi.x, kc.z);
+                    D[1][r] = pk_reg(lo.y, hi.y, kc.z);
+                    D[2][r] = pk_reg(lo.z, hi.z, kc.z);
+                    D[3][r] = pk_reg(lo.w, hi.w, kc.z);
+                }
+            };
+            ld(0, X);
+            ld(1, Y);
+            ld(2, Av);
+            ld(3, Lv);
+            ld(4, Wv);
+        }
+        const int gx0 = rx0 + 4 * lane, gy0 = ry0 + RB * wp;
+        const bool lft = gx0 == 0, rgt = gx0 + 4 == a.w;
+        const bool inside = gx0 >= 0 && gx0 < a.w && gy0 >= 0 && gy0 < a.h;
+        const bool track = interior && inside;
+        const int sink = (NW + 2) * SLOT + lane;
+        const int n_off = wp * SLOT + 128 + lane, s_off = (wp + 2) * SLOT + lane;
+        const int t_off = gy0 == 0 ? wp * SLOT + 128 + lane : gy0 == a.h ? sink : (wp + 1) * SLOT + lane;
+        const int b_off = gy0 + RB == a.h ? (wp + 2) * SLOT + lane
+                          : gy0 + RB == 0  ? sink : (wp + 1) * SLOT + 128 + lane;
+        float *rb0 = rows, *rb1 = rows + PAR;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            rb0[t_off + j * 32] = lo32(X[j][0]);
+            rb0[b_off + j * 32] = hi32(X[j][NP - 1]);
+        }
+        __syncthreads();  // stage consumed, rows published
+        // thread 0: issue the next item's load now if its rows were complete
+        // when loaded (during the previous tile), claim the one after it
+        // (nothing waits on the atomic: first used at the tile end), publish
+        // the previous tile after the first iteration pair (its stores have
+        // drained, so the fence is cheap), load the rows of the claimed item
+        // at the last pair
+        bool issued = false;
+        int n2 = 0;
+        if (tid == 0) {
+            *sh_next = n1;
+            if (n1 < nitems && rows_ok()) {
+                issue(n1);
+                issued = true;
+            }
+            n2 = atomicAdd(m.queue, 1);
+        }
+        float mx = 0.0f;
+        for (int it = 0; it < iters; it += 2) {
+            v2_iter<RB>(X, Y, Av, Lv, Wv, rb0, rb1, n_off, s_off, t_off, b_off, lft, rgt, kc, track, mx);
+            __syncthreads();
+            if (it + 1 < iters) {
+                v2_iter<RB>(Y, X, Av, Lv, Wv, rb1, rb0, n_off, s_off, t_off, b_off, lft, rgt, kc, track, mx);
+                __syncthreads();
+            }
+            if (tid == 0) {
+                if (pend >= 0) {
+                    publish(pend);
+                    pend = -1;
+                }
+                if (!issued && n1 < nitems) {  // rare: retry with fresh counts
+                    rows_load(n1);
+                    if (rows_ok()) {
+                        issue(n1);
+                        issued = true;
+                    }
+                }
+                if (it + 2 >= iters) rows_load(n2);
+            }
+        }
+        const bool odd = iters & 1;
+        bool nan_seen = false;
+        if (interior && inside) {
+            const long plane = (long)ch * a.h * a.w;
+            float *oo = m.Oout[pass & 1], *op_out = m.Opout[pass & 1];
+#pragma unroll
+            for (int rr = 0; rr < RB; ++rr) {
+                const int q = rr % NP;
+                float o[4], op[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const u64 cur = odd ? Y[j][q] : X[j][q];
+                    const u64 prv = odd ? X[j][q] : Y[j][q];
+                    o[j] = rr < NP ? lo32(cur) : hi32(cur);
+                    op[j] = rr < NP ? lo32(prv) : hi32(prv);
+                    nan_seen |= o[j] != o[j];
+                }
+                const long qi = (long)(gy0 + rr) * a.w + gx0;
+                if (last && a.hwc_out) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        a.hwc_out[(qi + j) * a.c + ch] = fminf(fmaxf(o[j], 0.0f), 1.0f);
+                } else {
+                    *reinterpret_cast<float4 *>(oo + plane + qi) = make_float4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<float4 *>(op_out + plane + qi) = make_float4(op[0], op[1], op[2], op[3]);
+                }
+            }
+        }
+        // per-pass maxima: items come in pass order, so flush on a pass change
+        if (pass != bits_pass) {
+            if (bits_pass >= 0) push_maxbits(bits, m.maxbits + bits_pass);
+            bits = 0;
+            bits_pass = pass;
+        }
+        bits = max(bits, nan_seen ? 0x7fffffffu : __float_as_uint(mx));
+        __syncthreads();  // every store of this tile issued
+        if (tid == 0) {
+            pend = item;  // published during the next tile (or before any wait)
+            if (!issued && n1 < nitems) {
+                publish(pend);  // never wait holding an unpublished tile
+                pend = -1;
+                const int keep[3] = {rv[0], rv[1], rv[2]};  // n2's counts
+                do {
+                    __nanosleep(128);
+                    rows_load(n1);
+                } while (!rows_ok());
+                issue(n1);
+                rv[0] = keep[0];
+                rv[1] = keep[1];
+                rv[2] = keep[2];
+            }
+            n1 = n2;
+        }
+        __syncthreads();
+        item = *sh_next;
+    }
+    if (tid == 0 && pend >= 0) publish(pend);
+    if (bits_pass >= 0) push_maxbits(bits, m.maxbits + bits_pass);
+}
+
+template <int RB>
+static int launch_mp(const MpMaps &maps, const MpArgs &m, cudaStream_t st)
+{
+    using C = v2::Cfg<RB>;
+    constexpr size_t SMEM = C::SMEM + 16;
+    static bool attr = false;
+    if (!attr) {
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_mp<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+        attr = true;
+    }
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        SS_CUDA_TRY(cudaGetDevice(&dev));
+        SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int ntiles = ((m.a.w + v2::OW - 1) / v2::OW) * ((m.a.h + v2::OH - 1) / v2::OH) * m.a.c;
+    const int grid = std::min(ntiles * m.npass, n_sm);
+    return fn::launch_pdl("k_sgd_mp", k_sgd_mp<RB>, dim3(grid), dim3(32, C::NW), SMEM, st, maps, m);
+}
+
+// ---------------------------------------------------------------------------
 // v3: v2<8> on CTA pairs (round 2).  A 2-CTA thread-block cluster stacks two
 // 128 x 64 regions into one 128 x 128 region with a single 8-pixel apron, so
 // the apron recompute drops from 128*64 / (112*48) = 1.52x to
@@ -2114,6 +2428,7 @@ SolverWork::~SolverWork()
     cudaFree(d_result);
     cudaFreeHost(h_result);
     cudaFreeHost(h_maxbits);
+    cudaFree(mp_flags);
 }
 
 int SolverWork::ensure(int h_, int w_, int c_, int iterations)
@@ -2164,6 +2479,7 @@ int solver_variant()
         if (e && !strcmp(e, "v2r4")) return 4;
         if (e && !strcmp(e, "v3")) return 5;
         if (e && !strcmp(e, "v4")) return 6;
+        if (e && !strcmp(e, "mp")) return 7;
         return 3;
     }();
     return v;
@@ -2242,10 +2558,11 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
     const long hw = (long)wk.h * wk.w;
     const long n = hw * wk.c;
     int variant = solver_variant();
+    if (variant == 7 && (wk.h % 8 != 0 || wk.w % 4 != 0)) variant = 3;  // mp runs v2<8> tiles
     if (variant == 6 && (wk.w % 4 != 0 || !encode_fn())) variant = 3;
     if (variant == 5 && wk.h % 8 != 0) variant = 4;  // v3 (pairs of 4x8 blocks) needs h % 8 == 0
     if (variant == 3 && wk.h % 8 != 0) variant = 4;  // RB = 8 needs h % 8 == 0
-    if (variant >= 3 && variant != 6 && (wk.w % 4 != 0 || wk.h % 4 != 0)) variant = 2;
+    if (variant >= 3 && variant != 6 && variant != 7 && (wk.w % 4 != 0 || wk.h % 4 != 0)) variant = 2;
     if (variant >= 2 && (wk.w % 4 != 0 || !encode_fn())) variant = 1;
     const int K = variant >= 3 ? v2::K : variant == 2 ? tma_k() : K_LDG;
     const int n_pass = variant ? (iters + K - 1) / K : 0;
@@ -2277,12 +2594,54 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
                 attr = true;
             }
         }
+        if (variant == 7) {
+            // every pass in one persistent launch (k_sgd_mp)
+            // [queue][rows_done: n_pass x c x tile rows], zeroed per solve
+            const int nty = (wk.h + v2::OH - 1) / v2::OH;
+            const size_t need = 1 + (size_t)n_pass * wk.c * nty;
+            if (need > wk.mp_flags_n) {
+                cudaFree(wk.mp_flags);
+                wk.mp_flags = nullptr;
+                SS_CUDA_TRY(cudaMalloc(&wk.mp_flags, need * sizeof(int)));
+                wk.mp_flags_n = need;
+            }
+            SS_CUDA_TRY(cudaMemsetAsync(wk.mp_flags, 0, need * sizeof(int), st));
+            MpMaps mm;
+            mm.init = m_init;
+            mm.set[0] = m_set[0];
+            mm.set[1] = m_set[1];
+            MpArgs m;
+            BlockedArgs &a = m.a;
+            a.O = a.Oprev = init;
+            a.A = A;
+            a.lapP = lapP;
+            a.wc = wc;
+            a.Oout = a.Oprev_out = nullptr;
+            a.hwc_out = out_hwc;
+            a.h = wk.h; a.w = wk.w; a.c = wk.c;
+            a.iters = K;
+            a.eta = p.eta;
+            a.kappa = p.kappa;
+            a.negzero = -0.0f;
+            a.maxbits = nullptr;
+            a.aligned = 1;
+            for (int k = 0; k < 2; ++k) {
+                m.Oout[k] = wk.O[k][0];
+                m.Opout[k] = wk.O[k][1];
+            }
+            m.npass = n_pass;
+            m.iters_last = iters - (n_pass - 1) * K;
+            m.maxbits = wk.maxbits;
+            m.queue = wk.mp_flags;
+            m.rows_done = wk.mp_flags + 1;
+            if ((rc = launch_mp<8>(mm, m, st))) return rc;
+        }
         constexpr int OWL = blk::RW - 2 * K_LDG, OHL = blk::RH - 2 * K_LDG;
         const dim3 grid((wk.w + OWL - 1) / OWL, (wk.h + OHL - 1) / OHL, wk.c);
         const dim3 block(blk::PAIRS, blk::STRIPS);
         const float *src_o = init, *src_op = init;
         int set = 0;
-        for (int ps = 0; ps < n_pass; ++ps) {
+        for (int ps = 0; ps < (variant == 7 ? 0 : n_pass); ++ps) {
             BlockedArgs a;
             a.O = src_o;
             a.Oprev = src_op;

@@ -74,6 +74,8 @@ struct SolverWork {
     unsigned *d_maxbits_map = nullptr;  // its device alias
     int *d_result = nullptr;
     PairwisePlan plan;
+    int *mp_flags = nullptr;  // solver "mp": item counter + per-(pass, channel, tile row) counts
+    size_t mp_flags_n = 0;
     ~SolverWork();
     int ensure(int h, int w, int c, int iterations);
 };

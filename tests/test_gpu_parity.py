@@ -347,13 +347,14 @@ def test_solver_v2_aligned_shapes_bitwise(ss, shape):
         assert np.array_equal(got, want), (shape, iters)
 
 
-@pytest.mark.parametrize("variant", ["v2", "v3", "v4"])
+@pytest.mark.parametrize("variant", ["v2", "v3", "v4", "mp"])
 def test_solver_many_tiles_per_cta_bitwise(ss, variant):
     """600x800x3 in a subprocess per schedule: v2 walks 8 x 13 x 3 = 312 tiles
     over 148 CTAs, v3 144 tiles over at most 74 CTA pairs (seam-row counters
     and receive-slot parities carried across tiles), v4 streams 4 strips x 18
     segments x 3 channels (34-row segments: ramps, chunk phases and the
-    image-edge ghost rows all exercised); 5 and 150 iterations, bit for bit."""
+    image-edge ghost rows all exercised), mp the 312 tiles of all 19 passes as
+    one dependency-ordered queue; 5 and 150 iterations, bit for bit."""
     import os
     import subprocess
     import sys
@@ -444,12 +445,14 @@ print("ok")
 @pytest.mark.parametrize("env", [{"SS_SOLVER": "stream"}, {"SS_SOLVER": "ldg"},
                                  {"SS_SOLVER": "tma", "SS_SOLVER_K": "4"},
                                  {"SS_SOLVER": "tma", "SS_SOLVER_K": "8"}, {"SS_SOLVER": "v2"},
-                                 {"SS_SOLVER": "v2r4"}, {"SS_SOLVER": "v3"}, {"SS_SOLVER": "v4"}])
+                                 {"SS_SOLVER": "v2r4"}, {"SS_SOLVER": "v3"}, {"SS_SOLVER": "v4"},
+                                 {"SS_SOLVER": "mp"}])
 def test_solver_variants_bitwise(ss, env):
     """Every solver schedule (streaming, blocked LDG, blocked TMA at K = 4/8,
     v2 with 4x8 (default) and 4x4 blocks, v3 = v2 on 2-CTA clusters with a
-    DSMEM seam-row exchange, v4 = time-skewed row streaming) produces the
-    reference's bits and divergence iterations."""
+    DSMEM seam-row exchange, v4 = time-skewed row streaming, mp = v2 tiles of
+    every pass in one launch) produces the reference's bits and divergence
+    iterations."""
     import os
     import subprocess
     import sys
