@@ -3,7 +3,8 @@
 # root).  Every ncu command's plain run comes first in the same call (&&).
 #   launch list of the default bench step (fp32 flow, headline config only);
 #   ncu --set full: one k_sgd_v2 solver pass, K1 presolve, est3_1 (fp32 and
-#   bf16, tools/conv_probe.py launches nothing else first), corr L3.
+#   bf16, tools/conv_probe.py launches nothing else first), corr L3
+#   (k_corr8); flow time against resolution; the full default bench.
 set -x
 OUT=gpurun_out/prof2
 mkdir -p $OUT
@@ -24,6 +25,11 @@ for p in fp32 bf16; do
 done
 F="python tools/flow_prof.py fp32"
 $F > $OUT/flow_plain.log 2>&1 && \
-ncu --set full --import-source on --clock-control none --kernel-name regex:k_corr --launch-skip 3 --launch-count 1 \
+ncu --set full --import-source on --clock-control none --kernel-name regex:k_corr8 --launch-skip 1 --launch-count 1 \
     -o $OUT/corr_l3 $F > $OUT/ncu_corr.log 2>&1
+# flow time against resolution (the resolution-independent latency chain)
+python tools/flow_scale.py fp32 > $OUT/flow_scale_fp32.txt 2>&1
+python tools/flow_scale.py bf16 > $OUT/flow_scale_bf16.txt 2>&1
+# the headline bench with every config
+python bench.py > $OUT/bench_full.json 2> $OUT/bench_full.err
 ls -la $OUT
