@@ -567,10 +567,14 @@ struct Cfg {
 
 // Edge-aligned tiling (round 2).  An apron is needed only where a region
 // borders another region: at the image boundary the replicate boundary is
-// exact.  So the first region of a row (column) of tiles starts at the image
-// edge with a 120 (56) wide interior, the last one ends at the far edge, and
-// the middle ones keep the 112 x 48 interior.  1080p: 17 x 23 x 3 = 1,173
-// tiles (8 rounds on 148 SMs) instead of 18 x 23 x 3 = 1,242 (9 rounds).
+// exact.  So the first region of a row (column) of tiles can start at the
+// image edge with a 120 (56) wide interior, the last one end at the far edge,
+// and the middle ones keep the 112 x 48 interior.  1080p with x edge-aligned:
+// 17 x 23 x 3 = 1,173 tiles (8 rounds on 148 SMs) instead of 18 x 23 x 3 =
+// 1,242 (9 rounds).  Measured, an edge-aligned axis also makes each tile ~4%
+// slower (not understood: the regions' placement in memory is all that
+// changes), so an axis is edge-aligned only when that saves a round of tiles
+// (v2_geometry): 1080p x only (1.064 -> 1.003 ms); 4K and 720p neither.
 // Along one axis of length n (n % 4 == 0, region R = 128 / 64, apron K):
 // interior boundaries b_0 = 0, b_1 = min(R - K, n), b_{i+1} = min(b_i + R - 2K,
 // n - (R - K)), ..., b_T = n; region origin 0 (first), n - R (last, if T > 1),
@@ -578,12 +582,15 @@ struct Cfg {
 struct V2Axis {
     int n, R, tiles, nmid;
 };
-__host__ __device__ __forceinline__ V2Axis v2_axis(int n, int R, int K)
+__host__ __device__ __forceinline__ V2Axis v2_axis(int n, int R, int K, bool edge)
 {
     V2Axis ax;
     ax.n = n;
     ax.R = R;
-    if (n <= R) {
+    if (!edge) {  // uniform: every region has its apron, origin i * (R - 2K) - K
+        ax.tiles = (n + R - 2 * K - 1) / (R - 2 * K);
+        ax.nmid = -1;
+    } else if (n <= R) {
         ax.tiles = 1;
         ax.nmid = 0;
     } else {
@@ -596,6 +603,12 @@ __host__ __device__ __forceinline__ V2Axis v2_axis(int n, int R, int K)
 // tile i: region origin and interior [lo, hi) in region coordinates
 __host__ __device__ __forceinline__ void v2_span(const V2Axis &ax, int K, int i, int &org, int &lo, int &hi)
 {
+    if (ax.nmid < 0) {
+        org = i * (ax.R - 2 * K) - K;
+        lo = K;
+        hi = ax.R - K;
+        return;
+    }
     if (ax.tiles == 1) {
         org = 0;
         lo = 0;
@@ -738,7 +751,7 @@ __device__ __forceinline__ void v2_iter(const u64 (&X)[4][RB / 2], u64 (&Y)[4][R
     }
 }
 
-template <int RB>
+template <int RB, int EDGE>
 __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
     k_sgd_v2(const __grid_constant__ TmaMaps maps, BlockedArgs a)
 {
@@ -750,7 +763,8 @@ __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
     uint64_t *bar = reinterpret_cast<uint64_t *>(rows + 2 * PAR);
     const int lane = threadIdx.x, wp = threadIdx.y;
     const int tid = wp * 32 + lane;
-    const V2Axis axx = v2_axis(a.w, RW, K), axy = v2_axis(a.h, RH, K);
+    // the geometry is a template parameter: as a run-time flag it cost ~3%
+    const V2Axis axx = v2_axis(a.w, RW, K, EDGE & 1), axy = v2_axis(a.h, RH, K, EDGE & 2);
     const int ntx = axx.tiles, nty = axy.tiles;
     const int ntiles = ntx * nty * a.c;
     constexpr uint32_t TX_BYTES = 5u * STAGE * sizeof(float);
@@ -913,14 +927,33 @@ __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
     push_maxbits(bits_all, a.maxbits);
 }
 
+// which axes of the v2 tiling are edge-aligned (bit 0: x, bit 1: y): the
+// combination with the fewest rounds of tiles on n_sm SMs, the fewest aligned
+// axes among those (SS_SOLVER_EDGE=0..3 forces one)
+static int v2_geometry(int w, int h, int c, int n_sm)
+{
+    static const int forced = getenv("SS_SOLVER_EDGE") ? atoi(getenv("SS_SOLVER_EDGE")) & 3 : -1;
+    if (forced >= 0) return forced;
+    int best = 0, best_rounds = 1 << 30;
+    for (int e : {0, 1, 2, 3}) {
+        const long tiles = (long)v2_axis(w, v2::RW, v2::K, e & 1).tiles * v2_axis(h, v2::RH, v2::K, e & 2).tiles * c;
+        const int rounds = (int)((tiles + n_sm - 1) / n_sm);
+        if (rounds < best_rounds) {  // ties keep the earlier (fewer aligned axes; 0, 1, 2, 3)
+            best_rounds = rounds;
+            best = e;
+        }
+    }
+    return best;
+}
+
 template <int RB>
 static int launch_v2(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
 {
     using C = v2::Cfg<RB>;
     static bool attr = false;
     if (!attr) {
-        SS_CUDA_TRY(cudaFuncSetAttribute(k_sgd_v2<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM));
+        for (auto fn : {k_sgd_v2<RB, 0>, k_sgd_v2<RB, 1>, k_sgd_v2<RB, 2>, k_sgd_v2<RB, 3>})
+            SS_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
         attr = true;
     }
     static int n_sm = 0;
@@ -929,9 +962,11 @@ static int launch_v2(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
         SS_CUDA_TRY(cudaGetDevice(&dev));
         SS_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
-    const int ntiles = v2_axis(a.w, v2::RW, v2::K).tiles * v2_axis(a.h, v2::RH, v2::K).tiles * a.c;
+    const int e = v2_geometry(a.w, a.h, a.c, n_sm);
+    const int ntiles = v2_axis(a.w, v2::RW, v2::K, e & 1).tiles * v2_axis(a.h, v2::RH, v2::K, e & 2).tiles * a.c;
     const int grid = std::min(ntiles, n_sm);
-    return fn::launch_pdl("k_sgd_v2", k_sgd_v2<RB>, dim3(grid), dim3(32, C::NW), C::SMEM, st, maps, a);
+    auto kern = e == 0 ? k_sgd_v2<RB, 0> : e == 1 ? k_sgd_v2<RB, 1> : e == 2 ? k_sgd_v2<RB, 2> : k_sgd_v2<RB, 3>;
+    return fn::launch_pdl("k_sgd_v2", kern, dim3(grid), dim3(32, C::NW), C::SMEM, st, maps, a);
 }
 
 // ---------------------------------------------------------------------------

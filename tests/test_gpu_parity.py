@@ -445,14 +445,16 @@ print("ok")
 @pytest.mark.parametrize("env", [{"SS_SOLVER": "stream"}, {"SS_SOLVER": "ldg"},
                                  {"SS_SOLVER": "tma", "SS_SOLVER_K": "4"},
                                  {"SS_SOLVER": "tma", "SS_SOLVER_K": "8"}, {"SS_SOLVER": "v2"},
+                                 {"SS_SOLVER": "v2", "SS_SOLVER_EDGE": "1"}, {"SS_SOLVER": "v2", "SS_SOLVER_EDGE": "2"},
+                                 {"SS_SOLVER": "v2", "SS_SOLVER_EDGE": "3"},
                                  {"SS_SOLVER": "v2r4"}, {"SS_SOLVER": "v3"}, {"SS_SOLVER": "v4"},
                                  {"SS_SOLVER": "mp"}])
 def test_solver_variants_bitwise(ss, env):
     """Every solver schedule (streaming, blocked LDG, blocked TMA at K = 4/8,
     v2 with 4x8 (default) and 4x4 blocks, v3 = v2 on 2-CTA clusters with a
     DSMEM seam-row exchange, v4 = time-skewed row streaming, mp = v2 tiles of
-    every pass in one launch) produces the reference's bits and divergence
-    iterations."""
+    every pass in one launch; v2 also with each edge-aligned tiling forced,
+    SS_SOLVER_EDGE) produces the reference's bits and divergence iterations."""
     import os
     import subprocess
     import sys
