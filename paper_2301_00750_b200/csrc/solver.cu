@@ -769,21 +769,21 @@ __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
     const int ntiles = ntx * nty * a.c;
     constexpr uint32_t TX_BYTES = 5u * STAGE * sizeof(float);
 
-    // tile t: channel, region origin, interior [ilx, ihx) x [ily, ihy) in region coordinates
-    auto coords4 = [&](int t, int &ch, int &x, int &y, int &ilx, int &ihx, int &ily, int &ihy) {
+    // Tiles are walked incrementally: (channel, tile row, tile column) of the
+    // CTA's current tile advance by the grid's decomposition each round, and
+    // the next tile's origin is worked out before the stage wait.  The thread
+    // that issues the prefetch after the "stage consumed" barrier holds every
+    // warp at the next barrier for as long as it takes: per-tile divisions
+    // and geometry branches there cost 3-5% of the pass.
+    auto coords = [&](int t, int &ch, int &x, int &y) {
         ch = t / (ntx * nty);
         const int rem = t - ch * ntx * nty;
         const int ty = rem / ntx, tx = rem - ty * ntx;
-        v2_span(axx, K, tx, x, ilx, ihx);
-        v2_span(axy, K, ty, y, ily, ihy);
+        int lo, hi;
+        v2_span(axx, K, tx, x, lo, hi);
+        v2_span(axy, K, ty, y, lo, hi);
     };
-    auto coords = [&](int t, int &ch, int &x, int &y) {
-        int a0, a1, a2, a3;
-        coords4(t, ch, x, y, a0, a1, a2, a3);
-    };
-    auto issue = [&](int t) {
-        int ch, x, y;
-        coords(t, ch, x, y);
+    auto issue_at = [&](int ch, int x, int y) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                      :: "r"(smem_u32(bar)), "r"(TX_BYTES) : "memory");
         tma_load_3d(stage + 0 * STAGE, &maps.O, x, y, ch, bar);
@@ -824,9 +824,36 @@ __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
     kc.z = pk(a.negzero, a.negzero);
     uint32_t phase = 0;
     unsigned bits_all = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        int ch, rx0, ry0, ilx, ihx, ily, ihy;
-        coords4(t, ch, rx0, ry0, ilx, ihx, ily, ihy);
+    int cch, cty, ctx;  // the current tile
+    {
+        cch = blockIdx.x / (ntx * nty);
+        const int rem = blockIdx.x - cch * ntx * nty;
+        cty = rem / ntx;
+        ctx = rem - cty * ntx;
+    }
+    const int G = gridDim.x;
+    const int dch = G / (ntx * nty), drem = G - dch * ntx * nty, dty = drem / ntx, dtx = drem - dty * ntx;
+    for (int t = blockIdx.x; t < ntiles; t += G) {
+        const int ch = cch;
+        int rx0, ry0, ilx, ihx, ily, ihy;
+        v2_span(axx, K, ctx, rx0, ilx, ihx);
+        v2_span(axy, K, cty, ry0, ily, ihy);
+        // the next tile of this CTA and its region origin
+        int nch = cch + dch, ntyi = cty + dty, ntxi = ctx + dtx;
+        if (ntxi >= ntx) {
+            ntxi -= ntx;
+            ++ntyi;
+        }
+        if (ntyi >= nty) {
+            ntyi -= nty;
+            ++nch;
+        }
+        int nx0, ny0;
+        {
+            int lo, hi;
+            v2_span(axx, K, ntxi, nx0, lo, hi);
+            v2_span(axy, K, ntyi, ny0, lo, hi);
+        }
         // the thread's 4 x RB block commits (and is tracked) when it lies in the interior
         const bool interior = 4 * lane >= ilx && 4 * lane + 4 <= ihx && RB * wp >= ily && RB * wp + RB <= ihy;
         mbar_wait(bar, phase);
@@ -878,10 +905,13 @@ __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
             rb0[b_off + j * 32] = hi32(X[j][NP - 1]);
         }
         __syncthreads();  // stage consumed, rows published
-        if (tid == 0 && t + (int)gridDim.x < ntiles) {
+        if (tid == 0 && t + G < ntiles) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(t + gridDim.x);
+            issue_at(nch, nx0, ny0);
         }
+        cch = nch;
+        cty = ntyi;
+        ctx = ntxi;
         float mx = 0.0f;
         for (int it = 0; it < a.iters; it += 2) {
             v2_iter<RB>(X, Y, Av, Lv, Wv, rb0, rb1, n_off, s_off, t_off, b_off, lft, rgt, kc,
