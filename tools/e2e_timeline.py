@@ -45,7 +45,12 @@ for k in range(30):
     tcall("flow1", lambda: L.ss_session_compute_flow(sess, 1))
     if mode in ("full", "noout"):
         tcall("stage", lambda: L.ss_stage_pair(sess, pos + 1, host_i[(k + 1) % 4].data_ptr(), host_p[(k + 1) % 4].data_ptr(), 0, 0))
-    prm = params_struct(ConsistencyParams()); it = ctypes.c_int(0)
+    if os.environ.get("E2E_INTERACTIVE"):  # bench.py's per-frame schedule
+        prm = params_struct(ConsistencyParams(k1=0.3, k2=0.5, lam=2.0) if k % 2 == 0 else
+                            ConsistencyParams(k1=0.5, k2=0.3, lam=0.5))
+    else:
+        prm = params_struct(ConsistencyParams())
+    it = ctypes.c_int(0)
     tcall("step", lambda: L.ss_step(sess, 1, ctypes.byref(prm), ctypes.byref(it)))
     if mode == "outdev":
         tcall("out", lambda: L.ss_output_async(sess, douts[k % 2].data_ptr(), 0, 1))
