@@ -751,7 +751,7 @@ __device__ __forceinline__ void v2_iter(const u64 (&X)[4][RB / 2], u64 (&Y)[4][R
     }
 }
 
-template <int RB, int EDGE>
+template <int RB, int EDGE, bool REV>
 __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
     k_sgd_v2(const __grid_constant__ TmaMaps maps, BlockedArgs a)
 {
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
     // the first tile's constant inputs load while the previous pass drains
     if (tid == 0 && (int)blockIdx.x < ntiles) {
         int ch, x, y;
-        coords(blockIdx.x, ch, x, y);
+        coords(REV ? ntiles - 1 - (int)blockIdx.x : (int)blockIdx.x, ch, x, y);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                      :: "r"(smem_u32(bar)), "r"(TX_BYTES) : "memory");
         tma_load_3d(stage + 2 * STAGE, &maps.A, x, y, ch, bar);
@@ -826,8 +826,9 @@ __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
     unsigned bits_all = 0;
     int cch, cty, ctx;  // the current tile
     {
-        cch = blockIdx.x / (ntx * nty);
-        const int rem = blockIdx.x - cch * ntx * nty;
+        const int t0 = REV ? ntiles - 1 - (int)blockIdx.x : (int)blockIdx.x;
+        cch = t0 / (ntx * nty);
+        const int rem = t0 - cch * ntx * nty;
         cty = rem / ntx;
         ctx = rem - cty * ntx;
     }
@@ -839,14 +840,31 @@ __global__ void __launch_bounds__(v2::Cfg<RB>::THREADS, 1)
         v2_span(axx, K, ctx, rx0, ilx, ihx);
         v2_span(axy, K, cty, ry0, ily, ihy);
         // the next tile of this CTA and its region origin
-        int nch = cch + dch, ntyi = cty + dty, ntxi = ctx + dtx;
-        if (ntxi >= ntx) {
-            ntxi -= ntx;
-            ++ntyi;
-        }
-        if (ntyi >= nty) {
-            ntyi -= nty;
-            ++nch;
+        int nch, ntyi, ntxi;
+        if (REV) {  // walking the tile list backwards (odd passes)
+            nch = cch - dch;
+            ntyi = cty - dty;
+            ntxi = ctx - dtx;
+            if (ntxi < 0) {
+                ntxi += ntx;
+                --ntyi;
+            }
+            if (ntyi < 0) {
+                ntyi += nty;
+                --nch;
+            }
+        } else {
+            nch = cch + dch;
+            ntyi = cty + dty;
+            ntxi = ctx + dtx;
+            if (ntxi >= ntx) {
+                ntxi -= ntx;
+                ++ntyi;
+            }
+            if (ntyi >= nty) {
+                ntyi -= nty;
+                ++nch;
+            }
         }
         int nx0, ny0;
         {
@@ -977,12 +995,13 @@ static int v2_geometry(int w, int h, int c, int n_sm)
 }
 
 template <int RB>
-static int launch_v2(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
+static int launch_v2(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st, bool reverse)
 {
     using C = v2::Cfg<RB>;
     static bool attr = false;
     if (!attr) {
-        for (auto fn : {k_sgd_v2<RB, 0>, k_sgd_v2<RB, 1>, k_sgd_v2<RB, 2>, k_sgd_v2<RB, 3>})
+        for (auto fn : {k_sgd_v2<RB, 0, false>, k_sgd_v2<RB, 1, false>, k_sgd_v2<RB, 2, false>, k_sgd_v2<RB, 3, false>,
+                        k_sgd_v2<RB, 0, true>, k_sgd_v2<RB, 1, true>, k_sgd_v2<RB, 2, true>, k_sgd_v2<RB, 3, true>})
             SS_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
         attr = true;
     }
@@ -995,7 +1014,14 @@ static int launch_v2(const TmaMaps &maps, const BlockedArgs &a, cudaStream_t st)
     const int e = v2_geometry(a.w, a.h, a.c, n_sm);
     const int ntiles = v2_axis(a.w, v2::RW, v2::K, e & 1).tiles * v2_axis(a.h, v2::RH, v2::K, e & 2).tiles * a.c;
     const int grid = std::min(ntiles, n_sm);
-    auto kern = e == 0 ? k_sgd_v2<RB, 0> : e == 1 ? k_sgd_v2<RB, 1> : e == 2 ? k_sgd_v2<RB, 2> : k_sgd_v2<RB, 3>;
+    // odd passes walk the tiles backwards: their first tiles are the ones the
+    // previous pass wrote last, still in L2 (SS_SOLVER_SERPENTINE=0: all forward)
+    static const bool serp = getenv("SS_SOLVER_SERPENTINE") == nullptr || strcmp(getenv("SS_SOLVER_SERPENTINE"), "0");
+    const bool rev = serp && reverse;
+    auto kern = rev ? (e == 0 ? k_sgd_v2<RB, 0, true> : e == 1 ? k_sgd_v2<RB, 1, true>
+                       : e == 2 ? k_sgd_v2<RB, 2, true> : k_sgd_v2<RB, 3, true>)
+                    : (e == 0 ? k_sgd_v2<RB, 0, false> : e == 1 ? k_sgd_v2<RB, 1, false>
+                       : e == 2 ? k_sgd_v2<RB, 2, false> : k_sgd_v2<RB, 3, false>);
     return fn::launch_pdl("k_sgd_v2", kern, dim3(grid), dim3(32, C::NW), C::SMEM, st, maps, a);
 }
 
@@ -2784,7 +2810,7 @@ int solve_planar(SolverWork &wk, const float *A, const float *init, const float 
                 const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];
                 rc = variant == 6 ? launch_v4(mp, a, st)
                      : variant == 5 ? launch_v3(mp, a, st)
-                     : variant == 3 ? launch_v2<8>(mp, a, st) : launch_v2<4>(mp, a, st);
+                     : variant == 3 ? launch_v2<8>(mp, a, st, ps & 1) : launch_v2<4>(mp, a, st, ps & 1);
                 if (rc) return rc;
             } else if (variant == 2) {
                 const TmaMaps &mp = ps == 0 ? m_init : m_set[set ^ 1];
